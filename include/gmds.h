@@ -1,0 +1,163 @@
+/* gmds.h -- C-ABI of libgmds, the B200 (sm_100a) Gini-MDS hot-path engine.
+ *
+ * This is the drop-in boundary beneath the ginimds:: C++ facade
+ * (include/ginimds/ headers).  Plain pointers and sizes only; no CUDA or torch
+ * types.  Every entry point replaces one reference function, cited as
+ * /root/reference/proj/core/<file>:<line>.  Host pointers are caller-owned;
+ * device handles (gmds_dmat) are library-owned.  Functions are re-entrant;
+ * failures return a status mirroring the reference exception classes
+ * (error.hpp:9-53) and set a thread-local message (gmds_last_error()).
+ *
+ * Matrix layout: X is n x p.  GMDS_COL_MAJOR is Eigen's default (the
+ * reference's Matrix = Eigen::MatrixXd); distance matrices are symmetric, so
+ * their row- and column-major images coincide.
+ */
+#ifndef GMDS_H
+#define GMDS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gmds_status {
+  GMDS_OK = 0,
+  GMDS_INVALID_INPUT = 1,    /* ginimds::InvalidInput    (error.hpp:16-19) */
+  GMDS_INVALID_CONFIG = 2,   /* ginimds::InvalidConfig   (error.hpp:22-25) */
+  GMDS_DEGENERATE_INPUT = 3, /* ginimds::DegenerateInput (error.hpp:29-32) */
+  GMDS_NUMERIC_FAILURE = 4,  /* ginimds::NumericFailure  (error.hpp:35-38) */
+  GMDS_ERROR = 5,            /* ginimds::Error (other)                     */
+  GMDS_CUDA_ERROR = 6,       /* device failure (no reference counterpart)  */
+  GMDS_NCCL_ERROR = 7
+} gmds_status;
+
+typedef enum gmds_dtype { GMDS_F32 = 0, GMDS_F64 = 1 } gmds_dtype;
+typedef enum gmds_layout { GMDS_ROW_MAJOR = 0, GMDS_COL_MAJOR = 1 } gmds_layout;
+
+/* StressKind, embed.hpp:13 (same order). */
+typedef enum gmds_stress_kind { GMDS_KRUSKAL = 0, GMDS_HUBER = 1, GMDS_SAMMON = 2, GMDS_SMACOF = 3 } gmds_stress_kind;
+/* EmbeddingMethod, embed.hpp:15 (same order). */
+typedef enum gmds_method {
+  GMDS_M_CLASSICAL = 0,
+  GMDS_M_KRUSKAL = 1,
+  GMDS_M_HUBER = 2,
+  GMDS_M_SAMMON = 3,
+  GMDS_M_SMACOF = 4
+} gmds_method;
+
+const char* gmds_last_error(void);
+const char* gmds_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; compute calls then fail with GMDS_CUDA_ERROR). */
+int gmds_device_count(void);
+gmds_status gmds_set_device(int device);
+/* Number of libgmds kernel launches issued by this process so far (bench.py's gpu_launches). */
+int64_t gmds_launch_count(void);
+
+/* ---- rank: midrank (metrics.hpp:71-72, metrics.cpp:101-110 -> midrank_into 42-56) ----
+ * m vectors of length d, row-major (vector k at v + k*d).  ranks: m*d. */
+gmds_status gmds_midrank_batch(const double* v, int64_t m, int64_t d, double* ranks);
+
+/* Midranks of z = x_i - x_j (the ranks gen_gini_directed_impl builds,
+ * metrics.cpp:69-72, 84-93) for npairs row pairs (pairs[2k], pairs[2k+1]).
+ * ranks: npairs*p, in feature order.  Bit-exact verification path. */
+gmds_status gmds_pair_midranks(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                               const int64_t* pairs, int64_t npairs, double* ranks);
+
+/* ---- distance: gen_gini_distance (metrics.hpp:105-107, metrics.cpp:157-163) for one pair. */
+gmds_status gmds_gen_gini_distance(const double* x, int64_t dx, const double* y, int64_t dy, double nu, double* out);
+
+/* ---- pairwise_matrix, Gini branch (metrics.hpp:112, metrics.cpp:193-219 + from_matrix 169-191).
+ * nnu values of nu at once (one sort per pair serves them all).  D: host,
+ * nnu consecutive n x n matrices of out_t.  Each nu must be > 1
+ * (GiniParams, metrics.hpp:35-36). */
+gmds_status gmds_pairwise_gini(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                               const double* nus, int32_t nnu, gmds_dtype out_t, void* D);
+
+/* pairwise_matrix, Euclidean branch (metrics.cpp:220-235).  D: host n x n fp64. */
+gmds_status gmds_pairwise_euclidean(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, double* D);
+
+/* Device-resident variant for callers that keep X and D in HBM (bench,
+ * the fit path).  dX row-major on the device; dD receives nnu full n x n
+ * matrices (out_t) or, with packed != 0, nnu packed upper-triangle tile
+ * images (see gmds_packed_elems).  stream: a cudaStream_t or NULL.
+ * shard/nshards split the tile list (multi-GPU, one process per GPU): a
+ * shard writes only its own tiles. */
+gmds_status gmds_pairwise_gini_device(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus,
+                                      int32_t nnu, gmds_dtype out_t, int32_t packed, void* dD, int32_t shard,
+                                      int32_t nshards, void* stream);
+/* Elements in one packed upper-triangle image of an n x n matrix. */
+int64_t gmds_packed_elems(int64_t n);
+
+/* ---- DistanceMatrix on the device (metrics.hpp:45-57) ---- */
+typedef struct gmds_dmat gmds_dmat;
+/* DistanceMatrix::from_matrix (metrics.cpp:169-191): validates a host n x n
+ * matrix (square, zero diagonal, symmetric to 1e-12 * max(scale,1),
+ * finite, non-negative), clamps, uploads in `storage` precision. */
+gmds_status gmds_dmat_from_host(const double* D, int64_t n, gmds_dtype storage, gmds_dmat** out);
+/* pairwise_matrix(X, gini(nu)) straight into a device handle (no host D). */
+gmds_status gmds_dmat_gini(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, double nu,
+                           gmds_dtype storage, gmds_dmat** out);
+/* Same, from a device-resident row-major X (bench / large n). */
+gmds_status gmds_dmat_gini_device(const void* dX, gmds_dtype xt, int64_t n, int64_t p, double nu, gmds_dtype storage,
+                                  gmds_dmat** out);
+gmds_status gmds_dmat_download(const gmds_dmat* d, double* D_full);
+int64_t gmds_dmat_n(const gmds_dmat* d);
+void gmds_dmat_free(gmds_dmat* d);
+
+/* ---- stress (embed.hpp:61-76, embed.cpp:111-212, 462-489) ----
+ * coords: host n x q column-major (Eigen layout).  huber_delta: NaN = unset
+ * (StressConfig::huber_delta empty).  weights: host n x n or NULL (uniform). */
+gmds_status gmds_kruskal_stress(const gmds_dmat* D, const double* coords, int32_t q, double* out);
+gmds_status gmds_stress_loss(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q, double huber_delta,
+                             const double* weights, double* out);
+gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q,
+                                 double huber_delta, const double* weights, double* grad);
+
+/* classical_mds (embed.cpp:415-460): coords n x q column-major, eigvals q. */
+gmds_status gmds_classical_mds(const gmds_dmat* D, int32_t q, double* coords, double* eigvals, int32_t* clamped_count,
+                               double* clamped_mass, double* stress);
+
+/* StressConfig (embed.hpp:19-29). */
+typedef struct gmds_stress_cfg {
+  int32_t kind;         /* gmds_stress_kind */
+  double huber_delta;   /* NaN = auto (median grid, embed.cpp:499-515) */
+  const double* smacof_weights; /* host n x n or NULL */
+  int32_t max_iters;
+  double rel_tol;
+  uint64_t seed;
+} gmds_stress_cfg;
+
+typedef struct gmds_fit_result {
+  double* coords;        /* caller buffer n x q column-major */
+  double* history;       /* caller buffer, history_cap entries (may be NULL) */
+  int64_t history_cap;
+  int64_t history_len;   /* out: full length of stress_history */
+  int32_t iterations;    /* out */
+  int32_t converged;     /* out */
+  double stress;         /* out */
+  double huber_delta;    /* out: resolved delta when kind == huber */
+  int64_t passes;        /* out: device passes over D (observability) */
+} gmds_fit_result;
+
+/* minimize_stress (embed.cpp:491-532).  Y0 == NULL starts from
+ * classical_mds(D, q) exactly as the reference; a non-NULL Y0 (n x q
+ * column-major) is the seeded-init mode. */
+gmds_status gmds_minimize_stress(const gmds_dmat* D, int32_t q, const gmds_stress_cfg* cfg, const double* Y0,
+                                 gmds_fit_result* res);
+
+/* ---- tune (tune.hpp:42-56, tune.cpp:85-167) ----
+ * X host (layout lx) n x p.  grid: m strictly increasing nu > 1.
+ * mean_stress: m.  coords: n x q column-major (best / final embedding). */
+gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                         const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
+                         double* mean_stress, double* nu_star, double* coords, double* stress);
+gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                                  int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
+                                  double* nu_star, double* coords, double* stress);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GMDS_H */

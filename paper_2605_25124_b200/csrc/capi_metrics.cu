@@ -1,0 +1,280 @@
+// C-ABI: rank and distance entry points (metrics.hpp / metrics.cpp).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "lib_internal.h"
+
+namespace gmds {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(GMDS_CUDA_ERROR, "libgmds: no CUDA device visible (the engine has no CPU fallback)");
+  }
+}
+
+void check_nu(double nu) {
+  // GiniParams (metrics.hpp:35-36)
+  if (!(nu > 1.0)) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "GiniParams: nu must be > 1, got %f", nu);
+    fail(GMDS_INVALID_CONFIG, buf);
+  }
+}
+
+void check_finite_host(const void* X, gmds_dtype xt, int64_t count, const char* who) {
+  bool ok = true;
+  if (xt == GMDS_F32) {
+    const float* p = static_cast<const float*>(X);
+    for (int64_t k = 0; k < count && ok; ++k) ok = std::isfinite(p[k]);
+  } else {
+    const double* p = static_cast<const double*>(X);
+    for (int64_t k = 0; k < count && ok; ++k) ok = std::isfinite(p[k]);
+  }
+  if (!ok) fail(GMDS_INVALID_INPUT, std::string(who) + ": non-finite input entry");
+}
+
+// pow-table of gen_gini_directed_impl (metrics.cpp:73-79), folded for both
+// directions: L[h] = (pow(S(p+1-R), e) - c) - (pow(S(R), e) - c), h = 2R - 1.
+std::vector<double> build_lut(int d, const double* nus, int nnu) {
+  std::vector<double> lut(static_cast<size_t>(nnu) * 2 * d, 0.0);
+  const double inv_d = 1.0 / static_cast<double>(d);
+  for (int v = 0; v < nnu; ++v) {
+    const double exponent = nus[v] - 1.0;
+    const double c = std::pow(0.5, exponent);
+    for (int h = 1; h < 2 * d; ++h) {
+      const double rank = 0.5 * static_cast<double>(h + 1);
+      const double s_fwd = 1.0 - (rank - 0.5) * inv_d;
+      const double rank_bwd = static_cast<double>(d) + 1.0 - rank;
+      const double s_bwd = 1.0 - (rank_bwd - 0.5) * inv_d;
+      const double t_fwd = std::pow(s_fwd, exponent) - c;
+      const double t_bwd = std::pow(s_bwd, exponent) - c;
+      lut[static_cast<size_t>(v) * 2 * d + h] = t_bwd - t_fwd;
+    }
+  }
+  return lut;
+}
+
+// Host X (row- or column-major) -> device row-major copy.
+DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                                  cudaStream_t st) {
+  const size_t bytes = static_cast<size_t>(n) * p * dtype_size(xt);
+  DevBuf<unsigned char> out(bytes);
+  if (lx == GMDS_ROW_MAJOR || p == 1 || n == 1) {
+    GMDS_CUDA(cudaMemcpyAsync(out.get(), X, bytes, cudaMemcpyHostToDevice, st));
+  } else {
+    DevBuf<unsigned char> tmp(bytes);
+    GMDS_CUDA(cudaMemcpyAsync(tmp.get(), X, bytes, cudaMemcpyHostToDevice, st));
+    launch_transpose(tmp.get(), xt, n, p, out.get(), st);
+    GMDS_CUDA(cudaStreamSynchronize(st));
+  }
+  return out;
+}
+
+void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag) {
+  const std::vector<double> lut = build_lut(static_cast<int>(p), nus, nnu);
+  DevBuf<double> dlut(lut.size());
+  GMDS_CUDA(cudaMemcpyAsync(dlut.get(), lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  GiniTileArgs a{};
+  a.n = n;
+  a.d = static_cast<int>(p);
+  a.lut = dlut.get();
+  a.nnu = nnu;
+  a.packed = packed;
+  a.nb_packed = ceil_div(n, kPT);
+  a.out_stride = packed ? packed_elems(n) : n * n;
+  a.flag = dflag;
+  int64_t units;
+  if (p <= 1024) {
+    a.tile = gini_tile_size(static_cast<int>(p), xt, nnu);
+    a.nbt = ceil_div(n, a.tile);
+    units = a.nbt * (a.nbt + 1) / 2;
+  } else {
+    a.tile = 1;
+    a.nbt = n;
+    units = n * (n - 1) / 2;
+  }
+  a.tile_begin = units * shard / nshards;
+  a.tile_end = units * (shard + 1) / nshards;
+  launch_gini(a, dX, xt, dD, ot, st);
+  GMDS_CUDA(cudaStreamSynchronize(st));  // keeps dlut alive until the kernel is done
+}
+
+void check_flag(int* dflag, cudaStream_t st) {
+  int flag = 0;
+  GMDS_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  if (flag & 1) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
+}
+
+Stream::Stream() { GMDS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+Stream::~Stream() {
+  if (s) cudaStreamDestroy(s);
+}
+
+}  // namespace gmds
+
+using namespace gmds;
+
+extern "C" {
+
+const char* gmds_last_error(void) { return g_last_error.c_str(); }
+const char* gmds_version(void) { return "gmds-b200 0.1.0 (sm_100a); reference ginimds 0.1.0"; }
+
+int gmds_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+gmds_status gmds_set_device(int device) {
+  return guard([&] { GMDS_CUDA(cudaSetDevice(device)); });
+}
+
+int64_t gmds_launch_count(void) { return launch_count(); }
+
+int64_t gmds_packed_elems(int64_t n) { return packed_elems(n); }
+
+gmds_status gmds_midrank_batch(const double* v, int64_t m, int64_t d, double* ranks) {
+  return guard([&] {
+    if (d < 1) fail(GMDS_INVALID_INPUT, "midrank: input vector is empty");
+    check_finite_host(v, GMDS_F64, m * d, "midrank");
+    if (m == 0) return;
+    require_device();
+    Stream st;
+    DevBuf<double> dv(static_cast<size_t>(m * d)), dr(static_cast<size_t>(m * d));
+    GMDS_CUDA(cudaMemcpyAsync(dv.get(), v, sizeof(double) * m * d, cudaMemcpyHostToDevice, st.s));
+    launch_midrank(dv.get(), nullptr, GMDS_F64, nullptr, m, static_cast<int>(d), dr.get(), st.s);
+    GMDS_CUDA(cudaMemcpyAsync(ranks, dr.get(), sizeof(double) * m * d, cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+gmds_status gmds_pair_midranks(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                               const int64_t* pairs, int64_t npairs, double* ranks) {
+  return guard([&] {
+    if (p < 1) fail(GMDS_INVALID_INPUT, "gen_gini_directed: input vector is empty");
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    for (int64_t k = 0; k < 2 * npairs; ++k)
+      if (pairs[k] < 0 || pairs[k] >= n) fail(GMDS_INVALID_INPUT, "pair_midranks: row index out of range");
+    if (npairs == 0) return;
+    require_device();
+    Stream st;
+    DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
+    DevBuf<int64_t> dp(static_cast<size_t>(2 * npairs));
+    DevBuf<double> dr(static_cast<size_t>(npairs * p));
+    GMDS_CUDA(cudaMemcpyAsync(dp.get(), pairs, sizeof(int64_t) * 2 * npairs, cudaMemcpyHostToDevice, st.s));
+    launch_midrank(nullptr, dX.get(), xt, dp.get(), npairs, static_cast<int>(p), dr.get(), st.s);
+    GMDS_CUDA(cudaMemcpyAsync(ranks, dr.get(), sizeof(double) * npairs * p, cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+gmds_status gmds_gen_gini_distance(const double* x, int64_t dx, const double* y, int64_t dy, double nu, double* out) {
+  return guard([&] {
+    check_nu(nu);
+    if (dx != dy)
+      fail(GMDS_INVALID_INPUT,
+           "gen_gini_directed: length mismatch (" + std::to_string(dx) + " vs " + std::to_string(dy) + ")");
+    if (dx < 1) fail(GMDS_INVALID_INPUT, "gen_gini_directed: input vector is empty");
+    check_finite_host(x, GMDS_F64, dx, "gen_gini_directed");
+    check_finite_host(y, GMDS_F64, dy, "gen_gini_directed");
+    require_device();
+    Stream st;
+    std::vector<double> X2(static_cast<size_t>(2 * dx));
+    std::memcpy(X2.data(), x, sizeof(double) * dx);
+    std::memcpy(X2.data() + dx, y, sizeof(double) * dx);
+    DevBuf<double> dX(X2.size()), dD(4);
+    DevBuf<int> flag(1);
+    GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st.s));
+    GMDS_CUDA(cudaMemsetAsync(dD.get(), 0, 4 * sizeof(double), st.s));
+    GMDS_CUDA(cudaMemcpyAsync(dX.get(), X2.data(), sizeof(double) * X2.size(), cudaMemcpyHostToDevice, st.s));
+    run_gini(dX.get(), GMDS_F64, 2, dx, &nu, 1, GMDS_F64, 0, dD.get(), 0, 1, st.s, flag.get());
+    double D[4];
+    GMDS_CUDA(cudaMemcpyAsync(D, dD.get(), sizeof D, cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+    *out = D[1];  // +inf propagates as in the reference's scalar API (no matrix validation here)
+  });
+}
+
+gmds_status gmds_pairwise_gini(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                               const double* nus, int32_t nnu, gmds_dtype out_t, void* D) {
+  return guard([&] {
+    if (nnu < 1) fail(GMDS_INVALID_CONFIG, "pairwise_matrix: no nu value given");
+    for (int v = 0; v < nnu; ++v) check_nu(nus[v]);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    require_device();
+    Stream st;
+    DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
+    const size_t bytes = static_cast<size_t>(nnu) * n * n * dtype_size(out_t);
+    DevBuf<unsigned char> dD(bytes);
+    DevBuf<int> flag(1);
+    GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st.s));
+    GMDS_CUDA(cudaMemsetAsync(dD.get(), 0, bytes, st.s));
+    run_gini(dX.get(), xt, n, p, nus, nnu, out_t, 0, dD.get(), 0, 1, st.s, flag.get());
+    check_flag(flag.get(), st.s);
+    GMDS_CUDA(cudaMemcpyAsync(D, dD.get(), bytes, cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+gmds_status gmds_pairwise_euclidean(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, double* D) {
+  return guard([&] {
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    require_device();
+    Stream st;
+    DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
+    DevBuf<double> dD(static_cast<size_t>(n * n));
+    GMDS_CUDA(cudaMemsetAsync(dD.get(), 0, sizeof(double) * n * n, st.s));
+    launch_euclid(dX.get(), xt, n, static_cast<int>(p), dD.get(), st.s);
+    GMDS_CUDA(cudaMemcpyAsync(D, dD.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+    // from_matrix (metrics.cpp:169-191): Euclidean entries are finite for finite
+    // X unless a square overflows; reject like the reference.
+    for (int64_t k = 0; k < n * n; ++k)
+      if (!std::isfinite(D[k])) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
+  });
+}
+
+gmds_status gmds_pairwise_gini_device(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus,
+                                      int32_t nnu, gmds_dtype out_t, int32_t packed, void* dD, int32_t shard,
+                                      int32_t nshards, void* stream) {
+  return guard([&] {
+    if (nnu < 1) fail(GMDS_INVALID_CONFIG, "pairwise_matrix: no nu value given");
+    for (int v = 0; v < nnu; ++v) check_nu(nus[v]);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    if (nshards < 1 || shard < 0 || shard >= nshards) fail(GMDS_INVALID_CONFIG, "pairwise_matrix: bad shard");
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DevBuf<int> flag(1);
+    GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
+    run_gini(dX, xt, n, p, nus, nnu, out_t, packed, dD, shard, nshards, st, flag.get());
+    check_flag(flag.get(), st);
+  });
+}
+
+}  // extern "C"

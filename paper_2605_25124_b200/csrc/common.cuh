@@ -1,0 +1,90 @@
+// Shared host/device helpers for libgmds (status mapping, CUDA checks).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "gmds.h"
+
+namespace gmds {
+
+// Host-side error carrying a gmds_status; thrown inside the library and
+// converted to a status + thread-local message at the C-ABI boundary.
+struct Failure : std::runtime_error {
+  gmds_status status;
+  Failure(gmds_status s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] inline void fail(gmds_status s, const std::string& msg) { throw Failure(s, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(GMDS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define GMDS_CUDA(call) ::gmds::cuda_check((call), #call)
+
+inline void check_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+void set_last_error(const std::string& msg);
+
+template <typename F>
+gmds_status guard(F&& f) {
+  try {
+    f();
+    return GMDS_OK;
+  } catch (const Failure& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return GMDS_ERROR;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return GMDS_ERROR;
+  }
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline size_t dtype_size(gmds_dtype t) { return t == GMDS_F32 ? 4 : 8; }
+
+// RAII device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count) GMDS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+}  // namespace gmds

@@ -1,0 +1,24 @@
+// Device DistanceMatrix utilities (host launchers).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gmds.h"
+
+namespace gmds {
+
+struct DStats {
+  double sum_sq;   // sum_{i<j} D_ij^2
+  double sum;      // sum_{i<j} D_ij
+  double min_off;  // min_{i<j} D_ij
+  double max_off;  // max_{i<j} D_ij
+};
+
+void pack_full(const double* dfull, int64_t n, gmds_dtype storage, void* dpacked, cudaStream_t st);
+void unpack_full(const void* dpacked, gmds_dtype storage, int64_t n, double* dfull, bool square, cudaStream_t st);
+DStats packed_stats(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st);
+double packed_median(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st);
+void double_center_dev(double* dS, int64_t n, cudaStream_t st);
+
+}  // namespace gmds

@@ -1,0 +1,793 @@
+// Host orchestration of the stress path and its C-ABI: device DistanceMatrix
+// handles, stress_loss / stress_gradient / kruskal_stress, classical_mds
+// (cuSOLVER syevd on the double-centred Gram matrix), and minimize_stress
+// (Armijo gradient descent for kruskal / huber / sammon, SMACOF majorisation)
+// with the reference's control flow (embed.cpp:222-272, 296-347, 491-532).
+//
+// Per gradient-descent iteration the device makes two passes over D: one
+// gradient pass at Y (which also yields the loss at Y), and one loss pass that
+// evaluates up to four Armijo trial points (step, step/2, step/4, step/8) at
+// once; the host takes the first one that satisfies the reference's Armijo
+// test, so the accepted point is the one the reference's sequential
+// halving loop would accept.  SMACOF needs one pass per iteration: the pass
+// at Z yields loss(Z) and the Guttman transform of Z together.
+#include <cusolverDn.h>
+#include <cublas_v2.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dmat.cuh"
+#include "dmat_kernels.cuh"
+#include "fit.h"
+#include "kernels.cuh"
+#include "lib_internal.h"
+#include "stress.cuh"
+
+namespace gmds {
+
+namespace {
+
+constexpr int64_t kChunk = 4;
+constexpr double kTiny = 1e-300;  // embed.cpp:13
+
+int padded_q(int q) { return q <= 4 ? q : q; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st(st_) {
+  n = D->n;
+  nb = ceil_div(n, kPT);
+  Q = padded_q(q);
+  rows_mode = (q > 4);
+  if (!rows_mode) {
+    std::vector<int64_t> cI, cJ, sf;
+    for (int64_t I = 0; I < nb; ++I) {
+      sf.push_back(static_cast<int64_t>(cI.size()));
+      for (int64_t J0 = I; J0 < nb; J0 += kChunk) {
+        cI.push_back(I);
+        cJ.push_back(J0);
+      }
+    }
+    sf.push_back(static_cast<int64_t>(cI.size()));
+    nchunks = static_cast<int64_t>(cI.size());
+    chunk_I.alloc(cI.size());
+    chunk_J0.alloc(cJ.size());
+    strip_first.alloc(sf.size());
+    GMDS_CUDA(cudaMemcpyAsync(chunk_I.get(), cI.data(), cI.size() * 8, cudaMemcpyHostToDevice, st));
+    GMDS_CUDA(cudaMemcpyAsync(chunk_J0.get(), cJ.data(), cJ.size() * 8, cudaMemcpyHostToDevice, st));
+    GMDS_CUDA(cudaMemcpyAsync(strip_first.get(), sf.data(), sf.size() * 8, cudaMemcpyHostToDevice, st));
+    const int64_t nblk = nb * (nb + 1) / 2;
+    rowpart.alloc(static_cast<size_t>(nchunks * kPT * Q));
+    colpart.alloc(static_cast<size_t>(nblk * kPT * Q));
+    losspart.alloc(static_cast<size_t>(nchunks * kMaxCand));
+  } else {
+    nchunks = n;
+    rowpart.alloc(static_cast<size_t>(n * Q));
+    losspart.alloc(static_cast<size_t>(n * kMaxCand));
+  }
+  graw.alloc(static_cast<size_t>(n * Q));
+  Y.alloc(static_cast<size_t>(n * Q));
+  for (auto& b : cand) b.alloc(static_cast<size_t>(n * Q));
+  scal.alloc(8);
+  GMDS_CUDA(cudaStreamSynchronize(st));
+}
+
+void Engine::upload(const double* coords_colmajor, double* dst) {
+  std::vector<double> h(static_cast<size_t>(n * Q), 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < q; ++k) h[i * Q + k] = coords_colmajor[k * n + i];
+  GMDS_CUDA(cudaMemcpyAsync(dst, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+}
+
+void Engine::download(const double* src, double* coords_colmajor) {
+  std::vector<double> h(static_cast<size_t>(n * Q));
+  GMDS_CUDA(cudaMemcpyAsync(h.data(), src, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < q; ++k) coords_colmajor[k * n + i] = h[i * Q + k];
+}
+
+PassArgs Engine::args(int kind, double delta) const {
+  PassArgs a{};
+  a.D = D->ptr();
+  a.W = W;
+  a.n = n;
+  a.nb = nb;
+  a.kind = kind;
+  a.huber_delta = delta;
+  a.chunk_I = chunk_I.get();
+  a.chunk_J0 = chunk_J0.get();
+  a.chunk_len = kChunk;
+  a.nchunks = nchunks;
+  a.rowpart = rowpart.get();
+  a.colpart = colpart.get();
+  a.losspart = losspart.get();
+  return a;
+}
+
+std::vector<double> Engine::loss_raw(int kind, double delta, const double* const* Ys, int nc) {
+  PassArgs a = args(kind, delta);
+  for (int c = 0; c < nc; ++c) a.Y[c] = Ys[c];
+  a.ncand = nc;
+  launch_stress_pass(a, Q, false, D->storage, st);
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
+  std::vector<double> out(static_cast<size_t>(nc));
+  GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  ++passes;
+  return out;
+}
+
+double Engine::grad_raw(int kind, double delta, const double* Yd) {
+  if (q > 64) fail(GMDS_INVALID_INPUT, "stress gradient: embedding dimension above 64 is not supported");
+  PassArgs a = args(kind, delta);
+  a.Y[0] = Yd;
+  a.ncand = 1;
+  launch_stress_pass(a, Q, true, D->storage, st);
+  if (!rows_mode)
+    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
+  else
+    GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
+  double out = 0.0;
+  GMDS_CUDA(cudaMemcpyAsync(&out, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  ++passes;
+  return out;
+}
+
+double Engine::scale_grad(double scale) {
+  launch_scale_sqnorm(graw.get(), n * Q, scale, scal.get() + 4, st);
+  double gsq = 0.0;
+  GMDS_CUDA(cudaMemcpyAsync(&gsq, scal.get() + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  return gsq;
+}
+
+// loss value of a kind from its raw pass sum (loss_value, embed.cpp:111-159)
+double Engine::loss_of(int kind, double raw) const {
+  switch (kind) {
+    case kKruskal: return std::sqrt(raw / D->sum_sq);
+    case kSammon: return (1.0 / D->sum) * raw;
+    default: return raw;
+  }
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+void check_coords(const gmds_dmat* D, const double* coords, int q, const char* who) {
+  // embed.cpp:15-21
+  if (!D) fail(GMDS_INVALID_INPUT, std::string(who) + ": null distance matrix");
+  if (q < 1) fail(GMDS_INVALID_INPUT, std::string(who) + ": coords have no columns");
+  for (int64_t k = 0; k < D->n * q; ++k)
+    if (!std::isfinite(coords[k])) fail(GMDS_INVALID_INPUT, std::string(who) + ": non-finite coordinates");
+}
+
+struct Resolved {
+  int kind;
+  double delta = 0.0;
+  bool weighted = false;
+};
+
+// resolve_params (embed.cpp:54-109)
+Resolved resolve(const gmds_dmat* D, int kind, double huber_delta, const double* weights, const char* who) {
+  Resolved r;
+  r.kind = kind;
+  const std::string w(who);
+  switch (kind) {
+    case kKruskal:
+      if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, w + ": all-zero distance matrix");
+      break;
+    case kHuber:
+      if (std::isnan(huber_delta))
+        fail(GMDS_INVALID_CONFIG,
+             w + ": huber_delta auto mode is resolved by minimize_stress; pass an explicit delta here");
+      if (!(huber_delta > 0.0)) fail(GMDS_INVALID_CONFIG, w + ": huber_delta must be > 0");
+      r.delta = huber_delta;
+      break;
+    case kSammon:
+      if (D->n >= 2 && !(D->min_off > 0.0))
+        fail(GMDS_DEGENERATE_INPUT,
+             w + ": Sammon loss requires strictly positive off-diagonal distances (deduplicate points first)");
+      break;
+    case kSmacof:
+      if (weights) {
+        const int64_t n = D->n;
+        for (int64_t i = 0; i < n; ++i)
+          for (int64_t j = i + 1; j < n; ++j) {
+            const double a = weights[j * n + i], b = weights[i * n + j];
+            if (!(a >= 0.0) || std::abs(a - b) > 0.0)
+              fail(GMDS_INVALID_CONFIG, w + ": smacof_weights must be symmetric and nonnegative");
+          }
+        r.weighted = true;
+      }
+      break;
+    default:
+      fail(GMDS_INVALID_CONFIG, w + ": unknown stress kind");
+  }
+  return r;
+}
+
+// Packed image of the SMACOF weights (same layout and storage as D).
+DevBuf<unsigned char> upload_weights(const gmds_dmat* D, const double* weights, cudaStream_t st) {
+  const int64_t n = D->n;
+  DevBuf<double> full(static_cast<size_t>(n * n));
+  GMDS_CUDA(cudaMemcpyAsync(full.get(), weights, sizeof(double) * n * n, cudaMemcpyHostToDevice, st));
+  DevBuf<unsigned char> out(static_cast<size_t>(packed_elems(n)) * dtype_size(D->storage));
+  // weights(i, j) column-major == full[j*n + i]; the packer reads full[i*n + j] for i < j, i.e. weights(j, i):
+  // symmetric by validation, so either triangle is the same value.
+  pack_full(full.get(), n, D->storage, out.get(), st);
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  return out;
+}
+
+struct IterResult {
+  double loss = 0.0;
+  bool converged = true;
+  int iterations = 0;
+  std::vector<double> history;
+};
+
+// gradient_descent (embed.cpp:222-272) with batched Armijo trials.
+IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double rel_tol) {
+  IterResult r;
+  const int kind = rp.kind;
+  double* Yc[kMaxCand];
+  for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();
+  const double* y0 = E.Y.get();
+  double f = E.loss_of(kind, E.loss_raw(kind, rp.delta, &y0, 1)[0]);
+  r.history.push_back(f);
+  double step = 1.0;
+  constexpr double armijo = 1e-4;
+  int it = 0;
+  bool stalled = false;
+  for (; it < max_iters; ++it) {
+    const double raw = E.grad_raw(kind, rp.delta, E.Y.get());
+    double scale = 1.0;
+    if (kind == kKruskal) {
+      const double ks = std::sqrt(raw / E.D->sum_sq);
+      scale = (ks <= 0.0) ? 0.0 : 1.0 / (ks * E.D->sum_sq);  // embed.cpp:179-181
+    } else if (kind == kSammon) {
+      scale = 2.0 * (1.0 / E.D->sum);  // q = -2 * scale * e / D
+    }
+    const double grad_sq = E.scale_grad(scale);
+    if (grad_sq <= 0.0) {
+      stalled = true;
+      break;
+    }
+    double f_new = f;
+    bool accepted = false;
+    int acc_c = -1;
+    for (int halvings = 0; halvings < 60 && !accepted;) {
+      Steps s{};
+      s.n = std::min(kMaxCand, 60 - halvings);
+      double sv = step;
+      for (int c = 0; c < s.n; ++c) {
+        s.v[c] = sv;
+        sv *= 0.5;
+      }
+      launch_axpy_cand(E.Y.get(), E.graw.get(), E.n * E.Q, s, Yc, E.st);
+      const std::vector<double> raws = E.loss_raw(kind, rp.delta, Yc, s.n);
+      for (int c = 0; c < s.n; ++c) {
+        const double fc = E.loss_of(kind, raws[c]);
+        if (fc <= f - armijo * s.v[c] * grad_sq) {
+          accepted = true;
+          acc_c = c;
+          f_new = fc;
+          step = s.v[c];
+          break;
+        }
+      }
+      if (!accepted) step = sv;  // halved s.n times
+      halvings += s.n;
+    }
+    if (!accepted) {
+      stalled = true;
+      break;
+    }
+    std::swap(E.Y, E.cand[acc_c]);
+    r.history.push_back(f_new);
+    const double decrease = (f - f_new) / std::max(f, kTiny);
+    f = f_new;
+    step *= 2.0;
+    if (decrease < rel_tol) {
+      ++it;
+      stalled = true;
+      break;
+    }
+  }
+  r.loss = f;
+  r.iterations = it;
+  r.converged = stalled || it < max_iters;
+  return r;
+}
+
+// smacof_iterate (embed.cpp:296-347).  pass(Z) -> (loss(Z), B(Z) Z).
+IterResult smacof_iterate(Engine& E, const Resolved& rp, const double* dVpinv, int max_iters, double rel_tol,
+                          cublasHandle_t blas) {
+  IterResult r;
+  const int64_t n = E.n;
+  double* next = E.cand[0].get();
+  auto transform = [&](double raw_loss_unused) {
+    (void)raw_loss_unused;
+    if (!dVpinv) {
+      launch_scale(E.graw.get(), n * E.Q, static_cast<double>(n), next, E.st);  // (B Z) / n
+    } else {
+      // X+ = V^+ (B Z): column-major n x n times row-major n x Q (== column-major Q x n)^T
+      const double one = 1.0, zero = 0.0;
+      // out^T (Q x n, col-major == row-major n x Q) = (BZ)^T (Q x n) * Vpinv^T (n x n); Vpinv symmetric.
+      if (cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, E.Q, static_cast<int>(n), static_cast<int>(n), &one,
+                      E.graw.get(), E.Q, dVpinv, static_cast<int>(n), &zero, next, E.Q) != CUBLAS_STATUS_SUCCESS)
+        fail(GMDS_CUDA_ERROR, "smacof: cublasDgemm failed");
+      count_launch();
+    }
+  };
+  double f = E.grad_raw(kGuttman, 0.0, E.Y.get());  // loss(Z0) and B(Z0) Z0
+  transform(f);
+  r.history.push_back(f);
+  int it = 0;
+  bool reached = false;
+  for (; it < max_iters; ++it) {
+    std::swap(E.Y, E.cand[0]);  // coords = next
+    next = E.cand[0].get();
+    const double f_new = E.grad_raw(kGuttman, 0.0, E.Y.get());  // loss(next) (+ next transform)
+    r.history.push_back(f_new);
+    const double decrease = (f - f_new) / std::max(f, kTiny);
+    f = f_new;
+    if (decrease < rel_tol) {
+      ++it;
+      reached = true;
+      break;
+    }
+    if (it + 1 < max_iters) transform(f_new);
+  }
+  r.loss = f;
+  r.iterations = it;
+  r.converged = reached || it < max_iters;
+  return r;
+}
+
+// V^+ for weighted SMACOF (embed.cpp:303-322), n x n column-major on the device.
+DevBuf<double> weights_pinv(const double* weights, int64_t n, cudaStream_t st);
+
+}  // namespace
+
+// classical_mds (embed.cpp:415-460)
+void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigvals, int* clamped_count,
+                       double* clamped_mass, double* stress, cudaStream_t st) {
+  const int64_t n = D->n;
+  if (q < 1 || q > n - 1)
+    fail(GMDS_INVALID_INPUT, "classical_mds: target dimension must satisfy 1 <= p <= n-1, got p=" +
+                                 std::to_string(q) + " with n=" + std::to_string(n));
+  DevBuf<double> B(static_cast<size_t>(n * n));
+  unpack_full(D->ptr(), D->storage, n, B.get(), true, st);  // S = D o D
+  double_center_dev(B.get(), n, st);
+  cusolverDnHandle_t h = nullptr;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(GMDS_CUDA_ERROR, "cusolverDnCreate failed");
+  struct Guard {
+    cusolverDnHandle_t h;
+    ~Guard() { cusolverDnDestroy(h); }
+  } guard{h};
+  cusolverDnSetStream(h, st);
+  DevBuf<double> w(static_cast<size_t>(n));
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), B.get(),
+                                  static_cast<int>(n), w.get(), &lwork) != CUSOLVER_STATUS_SUCCESS)
+    fail(GMDS_NUMERIC_FAILURE, "classical_mds: eigensolver failed");
+  DevBuf<double> work(static_cast<size_t>(lwork));
+  DevBuf<int> info(1);
+  if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), B.get(),
+                       static_cast<int>(n), w.get(), work.get(), lwork, info.get()) != CUSOLVER_STATUS_SUCCESS)
+    fail(GMDS_NUMERIC_FAILURE, "classical_mds: eigensolver failed");
+  count_launch();
+  int hinfo = 0;
+  std::vector<double> lam(static_cast<size_t>(n));
+  GMDS_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(lam.data(), w.get(), n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  std::vector<double> V(static_cast<size_t>(n) * q);
+  for (int c = 0; c < q; ++c)
+    GMDS_CUDA(cudaMemcpyAsync(V.data() + static_cast<size_t>(c) * n, B.get() + (n - 1 - c) * n, n * sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  if (hinfo != 0) fail(GMDS_NUMERIC_FAILURE, "classical_mds: eigensolver failed");
+  double negative_mass = 0.0, total_mass = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    total_mass += std::abs(lam[i]);
+    if (lam[i] < 0.0) negative_mass += -lam[i];
+  }
+  *clamped_mass = total_mass > 0.0 ? negative_mass / total_mass : 0.0;
+  *clamped_count = 0;
+  for (int c = 0; c < q; ++c) {
+    const double lambda = lam[n - 1 - c];
+    eigvals[c] = lambda;
+    double* v = V.data() + static_cast<size_t>(c) * n;
+    int64_t arg = 0;
+    double best = std::abs(v[0]);
+    for (int64_t i = 1; i < n; ++i)
+      if (std::abs(v[i]) > best) {
+        best = std::abs(v[i]);
+        arg = i;
+      }
+    const double sgn = (v[arg] < 0.0) ? -1.0 : 1.0;
+    if (lambda < 0.0) ++*clamped_count;
+    const double sc = std::sqrt(std::max(lambda, 0.0));
+    for (int64_t i = 0; i < n; ++i) coords[static_cast<size_t>(c) * n + i] = (sgn * v[i]) * sc;
+  }
+  if (stress) {
+    if (D->sum_sq > 0.0) {
+      Engine E(D, q, st);
+      E.upload(coords, E.Y.get());
+      const double* y = E.Y.get();
+      *stress = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
+    } else {
+      *stress = 0.0;
+    }
+  }
+}
+
+namespace {
+
+DevBuf<double> weights_pinv(const double* weights, int64_t n, cudaStream_t st) {
+  std::vector<double> V(static_cast<size_t>(n * n), 0.0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      if (i == j) continue;
+      const double w = weights[j * n + i];  // column-major (i, j)
+      V[j * n + i] = -w;
+      V[i * n + i] += w;
+    }
+  DevBuf<double> dV(static_cast<size_t>(n * n));
+  GMDS_CUDA(cudaMemcpyAsync(dV.get(), V.data(), V.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  cusolverDnHandle_t h = nullptr;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(GMDS_CUDA_ERROR, "cusolverDnCreate failed");
+  struct G {
+    cusolverDnHandle_t h;
+    ~G() { cusolverDnDestroy(h); }
+  } g{h};
+  cusolverDnSetStream(h, st);
+  DevBuf<double> w(static_cast<size_t>(n));
+  int lwork = 0;
+  cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), dV.get(),
+                              static_cast<int>(n), w.get(), &lwork);
+  DevBuf<double> work(static_cast<size_t>(lwork));
+  DevBuf<int> info(1);
+  if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), dV.get(),
+                       static_cast<int>(n), w.get(), work.get(), lwork, info.get()) != CUSOLVER_STATUS_SUCCESS)
+    fail(GMDS_NUMERIC_FAILURE, "smacof: eigensolver failed on V");
+  count_launch();
+  std::vector<double> lam(static_cast<size_t>(n)), U(static_cast<size_t>(n * n));
+  int hinfo = 0;
+  GMDS_CUDA(cudaMemcpyAsync(&hinfo, info.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(lam.data(), w.get(), n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(U.data(), dV.get(), U.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  if (hinfo != 0) fail(GMDS_NUMERIC_FAILURE, "smacof: eigensolver failed on V");
+  double amax = 0.0;
+  for (double l : lam) amax = std::max(amax, std::abs(l));
+  const double cutoff = 1e-12 * std::max(amax, 1.0);
+  // pinv = U diag(inv) U^T (host; weighted SMACOF is a small-n feature)
+  std::vector<double> P(static_cast<size_t>(n * n), 0.0);
+  for (int64_t k = 0; k < n; ++k) {
+    if (!(lam[k] > cutoff)) continue;
+    const double inv = 1.0 / lam[k];
+    const double* u = U.data() + k * n;
+    for (int64_t j = 0; j < n; ++j) {
+      const double uj = u[j] * inv;
+      for (int64_t i = 0; i < n; ++i) P[j * n + i] += u[i] * uj;
+    }
+  }
+  DevBuf<double> dP(static_cast<size_t>(n * n));
+  GMDS_CUDA(cudaMemcpyAsync(dP.get(), P.data(), P.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  return dP;
+}
+
+}  // namespace
+
+// minimize_stress (embed.cpp:491-532)
+void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, const double* Y0, gmds_fit_result* res,
+                         cudaStream_t st, const double* init_cache) {
+  if (cfg.max_iters < 1) fail(GMDS_INVALID_CONFIG, "minimize_stress: max_iters must be >= 1");
+  if (!(cfg.rel_tol > 0.0)) fail(GMDS_INVALID_CONFIG, "minimize_stress: rel_tol must be > 0");
+  const int64_t n = D->n;
+  std::vector<double> init(static_cast<size_t>(n) * q);
+  if (Y0) {
+    std::memcpy(init.data(), Y0, init.size() * sizeof(double));
+  } else if (init_cache) {
+    std::memcpy(init.data(), init_cache, init.size() * sizeof(double));
+  } else {
+    std::vector<double> ev(static_cast<size_t>(q));
+    int cc = 0;
+    double cm = 0.0;
+    classical_mds_dev(D, q, init.data(), ev.data(), &cc, &cm, nullptr, st);
+  }
+  if (cfg.kind == GMDS_HUBER && std::isnan(cfg.huber_delta)) {
+    const double med = packed_median(D->ptr(), D->storage, n, st);
+    const double base = med > 0.0 ? med : 1.0;
+    double best_ks = std::numeric_limits<double>::infinity();
+    std::vector<double> best_coords(static_cast<size_t>(n) * q), coords(static_cast<size_t>(n) * q);
+    std::vector<double> best_hist;
+    gmds_fit_result best{};
+    for (const double factor : {0.5, 1.0, 2.0}) {
+      gmds_stress_cfg trial = cfg;
+      trial.huber_delta = factor * base;
+      std::vector<double> hist(static_cast<size_t>(cfg.max_iters) + 2);
+      gmds_fit_result rr{};
+      rr.coords = coords.data();
+      rr.history = hist.data();
+      rr.history_cap = static_cast<int64_t>(hist.size());
+      minimize_stress_dev(D, q, trial, nullptr, &rr, st, init.data());
+      // kruskal_stress(e.coords, D) (embed.cpp:508)
+      if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
+      Engine E(D, q, st);
+      E.upload(coords.data(), E.Y.get());
+      const double* y = E.Y.get();
+      const double ks = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
+      if (ks < best_ks) {
+        best_ks = ks;
+        best = rr;
+        best_coords = coords;
+        best_hist.assign(hist.begin(), hist.begin() + std::min<int64_t>(rr.history_len, rr.history_cap));
+      }
+    }
+    std::memcpy(res->coords, best_coords.data(), best_coords.size() * sizeof(double));
+    res->history_len = best.history_len;
+    if (res->history)
+      for (int64_t t = 0; t < std::min<int64_t>(static_cast<int64_t>(best_hist.size()), res->history_cap); ++t)
+        res->history[t] = best_hist[static_cast<size_t>(t)];
+    res->iterations = best.iterations;
+    res->converged = best.converged;
+    res->stress = best.stress;
+    res->huber_delta = best.huber_delta;
+    return;
+  }
+  const Resolved rp = resolve(D, cfg.kind, cfg.huber_delta, cfg.smacof_weights, "minimize_stress");
+  Engine E(D, q, st);
+  DevBuf<unsigned char> W;
+  if (rp.weighted) {
+    W = upload_weights(D, cfg.smacof_weights, st);
+    E.W = W.get();
+  }
+  E.upload(init.data(), E.Y.get());
+  IterResult r;
+  if (cfg.kind == GMDS_SMACOF) {
+    DevBuf<double> vp;
+    cublasHandle_t blas = nullptr;
+    if (rp.weighted) {
+      vp = weights_pinv(cfg.smacof_weights, n, st);
+      if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(GMDS_CUDA_ERROR, "cublasCreate failed");
+      cublasSetStream(blas, st);
+    }
+    r = smacof_iterate(E, rp, rp.weighted ? vp.get() : nullptr, cfg.max_iters, cfg.rel_tol, blas);
+    if (blas) cublasDestroy(blas);
+  } else {
+    r = gradient_descent(E, rp, cfg.max_iters, cfg.rel_tol);
+  }
+  E.download(E.Y.get(), res->coords);
+  res->history_len = static_cast<int64_t>(r.history.size());
+  if (res->history)
+    for (int64_t t = 0; t < std::min<int64_t>(res->history_len, res->history_cap); ++t)
+      res->history[t] = r.history[static_cast<size_t>(t)];
+  res->iterations = r.iterations;
+  res->converged = r.converged ? 1 : 0;
+  res->stress = r.loss;
+  res->huber_delta = (cfg.kind == GMDS_HUBER) ? cfg.huber_delta : 0.0;
+  res->passes = E.passes;
+}
+
+// DistanceMatrix::from_matrix (metrics.cpp:169-191) on a host column-major matrix.
+std::vector<double> validate_full(const double* M, int64_t n) {
+  if (n < 1) fail(GMDS_INVALID_INPUT, "DistanceMatrix: matrix is empty");
+  double scale = 0.0;
+  bool has_nan = false;
+  for (int64_t k = 0; k < n * n; ++k) {
+    if (std::isnan(M[k])) has_nan = true;
+    scale = std::max(scale, std::abs(M[k]));
+  }
+  (void)has_nan;
+  const double tol = 1e-12 * std::max(scale, 1.0);
+  std::vector<double> out(static_cast<size_t>(n * n), 0.0);  // row-major image of the validated matrix
+  for (int64_t i = 0; i < n; ++i) {
+    if (std::abs(M[i * n + i]) > tol) fail(GMDS_INVALID_INPUT, "DistanceMatrix: nonzero diagonal");
+    for (int64_t j = i + 1; j < n; ++j) {
+      const double a = M[j * n + i];  // (i, j) column-major
+      const double b = M[i * n + j];  // (j, i)
+      if (!std::isfinite(a) || !std::isfinite(b)) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
+      if (std::abs(a - b) > tol) fail(GMDS_INVALID_INPUT, "DistanceMatrix: asymmetric entries");
+      if (a < -tol || b < -tol) fail(GMDS_INVALID_INPUT, "DistanceMatrix: negative entry");
+      const double v = std::max(0.0, a);
+      out[i * n + j] = v;
+      out[j * n + i] = v;
+    }
+  }
+  return out;
+}
+
+void dmat_finish(gmds_dmat* d, cudaStream_t st) {  // stats used by resolve_params
+  const DStats s = packed_stats(d->ptr(), d->storage, d->n, st);
+  d->sum_sq = s.sum_sq;
+  d->sum = s.sum;
+  d->min_off = d->n >= 2 ? s.min_off : 0.0;
+  d->max_val = d->n >= 2 ? std::max(0.0, s.max_off) : 0.0;
+  d->stats = true;
+}
+
+}  // namespace gmds
+
+using namespace gmds;
+
+extern "C" {
+
+gmds_status gmds_dmat_from_host(const double* D, int64_t n, gmds_dtype storage, gmds_dmat** out) {
+  return guard([&] {
+    *out = nullptr;
+    std::vector<double> full = validate_full(D, n);
+    require_device();
+    Stream st;
+    auto* d = new gmds_dmat();
+    d->n = n;
+    d->storage = storage;
+    try {
+      d->buf.alloc(static_cast<size_t>(packed_elems(n)) * dtype_size(storage));
+      DevBuf<double> dfull(full.size());
+      GMDS_CUDA(cudaMemcpyAsync(dfull.get(), full.data(), full.size() * sizeof(double), cudaMemcpyHostToDevice, st.s));
+      pack_full(dfull.get(), n, storage, d->buf.get(), st.s);
+      dmat_finish(d, st.s);
+    } catch (...) {
+      delete d;
+      throw;
+    }
+    *out = d;
+  });
+}
+
+static void dmat_gini_common(const void* dX, gmds_dtype xt, int64_t n, int64_t p, double nu, gmds_dtype storage,
+                             gmds_dmat** out, cudaStream_t st) {
+  auto* d = new gmds_dmat();
+  d->n = n;
+  d->storage = storage;
+  try {
+    const size_t bytes = static_cast<size_t>(packed_elems(n)) * dtype_size(storage);
+    d->buf.alloc(bytes);
+    GMDS_CUDA(cudaMemsetAsync(d->buf.get(), 0, bytes, st));
+    DevBuf<int> flag(1);
+    GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
+    run_gini(dX, xt, n, p, &nu, 1, storage, 1, d->buf.get(), 0, 1, st, flag.get());
+    check_flag(flag.get(), st);
+    dmat_finish(d, st);
+  } catch (...) {
+    delete d;
+    throw;
+  }
+  *out = d;
+}
+
+gmds_status gmds_dmat_gini(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, double nu,
+                           gmds_dtype storage, gmds_dmat** out) {
+  return guard([&] {
+    *out = nullptr;
+    check_nu(nu);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    require_device();
+    Stream st;
+    DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
+    dmat_gini_common(dX.get(), xt, n, p, nu, storage, out, st.s);
+  });
+}
+
+gmds_status gmds_dmat_gini_device(const void* dX, gmds_dtype xt, int64_t n, int64_t p, double nu, gmds_dtype storage,
+                                  gmds_dmat** out) {
+  return guard([&] {
+    *out = nullptr;
+    check_nu(nu);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    require_device();
+    Stream st;
+    dmat_gini_common(dX, xt, n, p, nu, storage, out, st.s);
+  });
+}
+
+gmds_status gmds_dmat_download(const gmds_dmat* d, double* D_full) {
+  return guard([&] {
+    if (!d) fail(GMDS_INVALID_INPUT, "dmat_download: null handle");
+    Stream st;
+    DevBuf<double> full(static_cast<size_t>(d->n * d->n));
+    unpack_full(d->ptr(), d->storage, d->n, full.get(), false, st.s);
+    GMDS_CUDA(cudaMemcpyAsync(D_full, full.get(), sizeof(double) * d->n * d->n, cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+  });
+}
+
+int64_t gmds_dmat_n(const gmds_dmat* d) { return d ? d->n : 0; }
+void gmds_dmat_free(gmds_dmat* d) { delete d; }
+
+gmds_status gmds_kruskal_stress(const gmds_dmat* D, const double* coords, int32_t q, double* out) {
+  return guard([&] {
+    check_coords(D, coords, q, "kruskal_stress");
+    if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
+    Stream st;
+    Engine E(D, q, st.s);
+    E.upload(coords, E.Y.get());
+    const double* y = E.Y.get();
+    *out = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
+  });
+}
+
+gmds_status gmds_stress_loss(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q, double huber_delta,
+                             const double* weights, double* out) {
+  return guard([&] {
+    check_coords(D, coords, q, "stress_loss");
+    const Resolved rp = resolve(D, kind, huber_delta, weights, "stress_loss");
+    Stream st;
+    Engine E(D, q, st.s);
+    DevBuf<unsigned char> W;
+    if (rp.weighted) {
+      W = upload_weights(D, weights, st.s);
+      E.W = W.get();
+    }
+    E.upload(coords, E.Y.get());
+    const double* y = E.Y.get();
+    *out = E.loss_of(kind, E.loss_raw(kind, rp.delta, &y, 1)[0]);
+  });
+}
+
+gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q,
+                                 double huber_delta, const double* weights, double* grad) {
+  return guard([&] {
+    check_coords(D, coords, q, "stress_gradient");
+    const Resolved rp = resolve(D, kind, huber_delta, weights, "stress_gradient");
+    Stream st;
+    Engine E(D, q, st.s);
+    DevBuf<unsigned char> W;
+    if (rp.weighted) {
+      W = upload_weights(D, weights, st.s);
+      E.W = W.get();
+    }
+    E.upload(coords, E.Y.get());
+    const double raw = E.grad_raw(kind, rp.delta, E.Y.get());
+    double scale = 1.0;
+    if (kind == kKruskal) {
+      const double ks = std::sqrt(raw / D->sum_sq);
+      scale = (ks <= 0.0) ? 0.0 : 1.0 / (ks * D->sum_sq);
+    } else if (kind == kSammon) {
+      scale = 2.0 * (1.0 / D->sum);
+    }
+    E.scale_grad(scale);
+    E.download(E.graw.get(), grad);
+  });
+}
+
+gmds_status gmds_classical_mds(const gmds_dmat* D, int32_t q, double* coords, double* eigvals, int32_t* clamped_count,
+                               double* clamped_mass, double* stress) {
+  return guard([&] {
+    if (!D) fail(GMDS_INVALID_INPUT, "classical_mds: null distance matrix");
+    Stream st;
+    int cc = 0;
+    classical_mds_dev(D, q, coords, eigvals, &cc, clamped_mass, stress, st.s);
+    *clamped_count = cc;
+  });
+}
+
+gmds_status gmds_minimize_stress(const gmds_dmat* D, int32_t q, const gmds_stress_cfg* cfg, const double* Y0,
+                                 gmds_fit_result* res) {
+  return guard([&] {
+    if (!D) fail(GMDS_INVALID_INPUT, "minimize_stress: null distance matrix");
+    if (Y0) check_coords(D, Y0, q, "minimize_stress");
+    Stream st;
+    minimize_stress_dev(D, q, *cfg, Y0, res, st.s, nullptr);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// Stress engine bound to one device DistanceMatrix (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "dmat.cuh"
+#include "stress.cuh"
+
+namespace gmds {
+
+struct Engine {
+  const gmds_dmat* D;
+  int q, Q;
+  bool rows_mode;
+  cudaStream_t st;
+  int64_t n = 0, nb = 0, nchunks = 0;
+  int64_t passes = 0;  // passes over D issued by this engine
+  const void* W = nullptr;
+  DevBuf<int64_t> chunk_I, chunk_J0, strip_first;
+  DevBuf<double> rowpart, colpart, losspart, graw, scal, Y;
+  DevBuf<double> cand[kMaxCand];
+
+  Engine(const gmds_dmat* D, int q, cudaStream_t st);
+  void upload(const double* coords_colmajor, double* dst);
+  void download(const double* src, double* coords_colmajor);
+  PassArgs args(int kind, double delta) const;
+  // raw loss sums at up to kMaxCand configurations (one pass)
+  std::vector<double> loss_raw(int kind, double delta, const double* const* Ys, int nc);
+  // raw gradient sums into graw, returns the raw loss at Yd (one pass)
+  double grad_raw(int kind, double delta, const double* Yd);
+  // graw *= scale, returns |graw|^2
+  double scale_grad(double scale);
+  double loss_of(int kind, double raw) const;
+};
+
+void dmat_finish(gmds_dmat* d, cudaStream_t st);
+void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigvals, int* clamped_count,
+                       double* clamped_mass, double* stress, cudaStream_t st);
+void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, const double* Y0, gmds_fit_result* res,
+                         cudaStream_t st, const double* init_cache);
+
+}  // namespace gmds

@@ -1,0 +1,44 @@
+// Internal kernel launch interface of libgmds (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gmds.h"
+
+namespace gmds {
+
+// Packed upper-triangle tile image used for every device-resident D:
+// kPT x kPT blocks (I <= J), each stored row-major, blocks in row-major
+// upper-triangle order.  Entries with i >= j or j >= n are zero.
+constexpr int kPT = 128;
+
+__host__ __device__ int64_t packed_offset(int64_t i, int64_t j, int64_t nb);
+int64_t packed_elems(int64_t n);
+
+struct GiniTileArgs {
+  int64_t n;           // rows
+  int d;               // features (p)
+  int tile;            // pairs tile edge (rows per panel)
+  int64_t nbt;         // tile rows = ceil(n / tile)
+  int64_t tile_begin;  // [begin, end) of this launch's tiles (pairs for p > 1024)
+  int64_t tile_end;
+  const double* lut;   // nnu x 2d, device
+  int nnu;
+  int packed;          // 0: full n x n per nu; 1: packed tile image per nu
+  int64_t nb_packed;   // ceil(n / kPT)
+  int64_t out_stride;  // elements between consecutive nu outputs
+  int* flag;           // device: bit0 = non-finite distance produced
+};
+
+void count_launch(int64_t k = 1);
+int64_t launch_count();
+
+int gini_tile_size(int d, gmds_dtype xt, int nnu);
+void launch_midrank(const double* dv, const void* dX, gmds_dtype xt, const int64_t* dpairs, int64_t nseg, int d,
+                    double* dranks, cudaStream_t st);
+void launch_gini(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, cudaStream_t st);
+void launch_euclid(const void* dX, gmds_dtype xt, int64_t n, int d, double* dout, cudaStream_t st);
+void launch_transpose(const void* din, gmds_dtype t, int64_t rows, int64_t cols, void* dout, cudaStream_t st);
+
+}  // namespace gmds

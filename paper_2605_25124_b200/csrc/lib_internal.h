@@ -1,0 +1,30 @@
+// Host helpers shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace gmds {
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  Stream();
+  ~Stream();
+  Stream(const Stream&) = delete;
+  Stream& operator=(const Stream&) = delete;
+};
+
+void require_device();
+void check_nu(double nu);
+void check_finite_host(const void* X, gmds_dtype xt, int64_t count, const char* who);
+std::vector<double> build_lut(int d, const double* nus, int nnu);
+DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                                  cudaStream_t st);
+void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag);
+void check_flag(int* dflag, cudaStream_t st);
+
+}  // namespace gmds

@@ -1,0 +1,45 @@
+// Stress-pass launch interface (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "gmds.h"
+
+namespace gmds {
+
+enum PassKind { kKruskal = 0, kHuber = 1, kSammon = 2, kSmacof = 3, kGuttman = 4 };
+constexpr int kMaxCand = 4;
+
+struct PassArgs {
+  const void* D;            // packed image (storage dtype)
+  const void* W;            // packed weights image or nullptr
+  int64_t n, nb;            // rows, ceil(n / kPT)
+  const double* Y[kMaxCand];  // n x Q row-major (padded), one per candidate
+  int ncand;
+  int kind;
+  double huber_delta;
+  const int64_t* chunk_I;   // [nchunks]
+  const int64_t* chunk_J0;  // [nchunks]
+  int64_t chunk_len;
+  int64_t nchunks;
+  double* rowpart;          // [nchunks][kPT][Q]  (rows kernel: [n][q] final)
+  double* colpart;          // [nblk][kPT][Q]
+  double* losspart;         // [nchunks][kMaxCand] (rows kernel: [n][kMaxCand])
+};
+
+struct Steps {
+  double v[kMaxCand];
+  int n;
+};
+
+void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage, cudaStream_t st);
+void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
+                        int64_t nb, int q, double* out, cudaStream_t st);
+void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
+void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, cudaStream_t st);
+void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& s, double* const* outs,
+                      cudaStream_t st);
+void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st);
+
+}  // namespace gmds

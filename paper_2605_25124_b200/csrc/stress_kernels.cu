@@ -1,0 +1,191 @@
+// Support kernels of the stress path (generic rows pass, reductions, trial
+// points) and the pass dispatcher.  The fused pass itself is in
+// stress_pass.cuh.
+#include "stress_pass.cuh"
+
+namespace gmds {
+
+// Generic (any q <= 64) loss / gradient pass: thread per row i, sequential
+// over j.  Used for q > 4 (embedding dimensions the fused pass does not
+// instantiate).  Row i's gradient is the full sum over j != i.
+template <typename TD>
+__global__ void stress_rows_kernel(PassArgs a, int q, int grad) {
+  using M = typename MathOf<TD>::type;
+  const TD* __restrict__ D = static_cast<const TD*>(a.D);
+  const TD* __restrict__ W = static_cast<const TD*>(a.W);
+  const M delta = static_cast<M>(a.huber_delta);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double loss[kMaxCand] = {0, 0, 0, 0};
+    double g[64];
+    for (int k = 0; k < (grad ? q : 0); ++k) g[k] = 0.0;
+    const int nc = grad ? 1 : a.ncand;
+    for (int64_t j = 0; j < a.n; ++j) {
+      if (j == i) continue;
+      const int64_t lo = min(i, j), hi = max(i, j);
+      const int64_t off = packed_offset(lo, hi, a.nb);
+      const M Dv = static_cast<M>(D[off]);
+      const M wv = W ? static_cast<M>(W[off]) : M(1);
+      for (int c = 0; c < nc; ++c) {
+        M d2 = 0;
+        for (int k = 0; k < q; ++k) {
+          const M dy = static_cast<M>(a.Y[c][i * q + k]) - static_cast<M>(a.Y[c][j * q + k]);
+          d2 = fma(dy, dy, d2);
+        }
+        const M dist = sqrt(d2);
+        PairTerms<M> t;
+        switch (a.kind) {
+          case kKruskal: t = pair_terms<kKruskal, M>(Dv, dist, wv, delta); break;
+          case kHuber: t = pair_terms<kHuber, M>(Dv, dist, wv, delta); break;
+          case kSammon: t = pair_terms<kSammon, M>(Dv, dist, wv, delta); break;
+          case kSmacof: t = pair_terms<kSmacof, M>(Dv, dist, wv, delta); break;
+          default: t = pair_terms<kGuttman, M>(Dv, dist, wv, delta); break;
+        }
+        if (j > i) loss[c] += static_cast<double>(t.term);  // each pair once
+        if (grad)
+          for (int k = 0; k < q; ++k)
+            g[k] += static_cast<double>(t.c * (static_cast<M>(a.Y[0][i * q + k]) - static_cast<M>(a.Y[0][j * q + k])));
+      }
+    }
+    if (grad)
+      for (int k = 0; k < q; ++k) a.rowpart[i * q + k] = g[k];
+    for (int c = 0; c < nc; ++c) a.losspart[i * kMaxCand + c] = loss[c];
+  }
+}
+
+// Stage 2: out[r][k] = sum over strip-R chunks of rowpart + sum over I <= R of colpart(I, R).
+__global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                                   const int64_t* __restrict__ strip_first, int64_t n, int64_t nb, int Q,
+                                   double* __restrict__ out) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * Q) return;
+  const int64_t r = e / Q;
+  const int k = static_cast<int>(e % Q);
+  const int64_t R = r / kPT, rr = r % kPT;
+  double s = 0.0;
+  for (int64_t c = strip_first[R]; c < strip_first[R + 1]; ++c) s += rowpart[(c * kPT + rr) * Q + k];
+  for (int64_t I = 0; I <= R; ++I) s += colpart[(blk_index(I, R, nb) * kPT + rr) * Q + k];
+  out[e] = s;
+}
+
+// Deterministic single-CTA sums: out[c] = sum_k part[k*stride + c] for c < m.
+__global__ void sum_parts_kernel(const double* __restrict__ part, int64_t count, int stride, int m,
+                                 double* __restrict__ out) {
+  __shared__ double red[1024];
+  for (int c = 0; c < m; ++c) {
+    double s = 0.0;
+    for (int64_t k = threadIdx.x; k < count; k += blockDim.x) s += part[k * stride + c];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = red[0];
+    __syncthreads();
+  }
+}
+
+// g *= scale (in place); out = sum g^2 (deterministic single CTA).
+__global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double scale, double* __restrict__ out) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    const double v = g[k] * scale;
+    g[k] = v;
+    s += v * v;
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// out_c = Y - step_c * G for each candidate (trial = coords - step * grad, embed.cpp:243).
+__global__ void axpy_cand_kernel(const double* __restrict__ Y, const double* __restrict__ G, int64_t m, Steps s,
+                                 double* __restrict__ out0, double* __restrict__ out1, double* __restrict__ out2,
+                                 double* __restrict__ out3) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double y = Y[k], g = G[k];
+    out0[k] = y - s.v[0] * g;
+    if (s.n > 1) out1[k] = y - s.v[1] * g;
+    if (s.n > 2) out2[k] = y - s.v[2] * g;
+    if (s.n > 3) out3[k] = y - s.v[3] * g;
+  }
+}
+
+// X+ = g / n (guttman_transform's uniform branch, embed.cpp:293).
+__global__ void scale_kernel(const double* __restrict__ in, int64_t m, double inv, double* __restrict__ out) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[k] = in[k] / inv;
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+
+template <typename TD, bool GRAD>
+static void launch_pass_t(const PassArgs& a, int Q, cudaStream_t st) {
+  launch_pass_td<TD, GRAD>(a, Q, st);
+  count_launch();
+  check_launch("stress_pass_kernel");
+}
+
+void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage, cudaStream_t st) {
+  if (q <= 4) {
+    if (storage == GMDS_F32)
+      grad ? launch_pass_t<float, true>(a, q, st) : launch_pass_t<float, false>(a, q, st);
+    else
+      grad ? launch_pass_t<double, true>(a, q, st) : launch_pass_t<double, false>(a, q, st);
+    return;
+  }
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(a.n, 128)));
+  if (storage == GMDS_F32)
+    stress_rows_kernel<float><<<blocks, 128, 0, st>>>(a, q, grad ? 1 : 0);
+  else
+    stress_rows_kernel<double><<<blocks, 128, 0, st>>>(a, q, grad ? 1 : 0);
+  count_launch();
+  check_launch("stress_rows_kernel");
+}
+
+void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
+                        int64_t nb, int q, double* out, cudaStream_t st) {
+  const int64_t m = n * q;
+  reduce_rows_kernel<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, st>>>(rowpart, colpart, strip_first, n, nb,
+                                                                             q, out);
+  count_launch();
+  check_launch("reduce_rows_kernel");
+}
+
+void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st) {
+  sum_parts_kernel<<<1, 1024, 0, st>>>(part, count, stride, m, out);
+  count_launch();
+  check_launch("sum_parts_kernel");
+}
+
+void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, cudaStream_t st) {
+  scale_sqnorm_kernel<<<1, 1024, 0, st>>>(g, m, scale, out);
+  count_launch();
+  check_launch("scale_sqnorm_kernel");
+}
+
+void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& s, double* const* outs,
+                      cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 1024)));
+  axpy_cand_kernel<<<blocks, 256, 0, st>>>(Y, G, m, s, outs[0], outs[1], outs[2], outs[3]);
+  count_launch();
+  check_launch("axpy_cand_kernel");
+}
+
+void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 1024)));
+  scale_kernel<<<blocks, 256, 0, st>>>(in, m, divisor, out);
+  count_launch();
+  check_launch("scale_kernel");
+}
+
+}  // namespace gmds

@@ -1,0 +1,6 @@
+// Instantiation: stress_pass_kernel<Q, float, false, KIND> for Q in 1..4, every kind.
+#include "stress_pass.cuh"
+
+namespace gmds {
+GMDS_INSTANTIATE_PASS(float, false)
+}  // namespace gmds

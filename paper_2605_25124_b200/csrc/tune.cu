@@ -1,0 +1,243 @@
+// tune_nu / alternating_tune (tune.cpp:85-167) over the device engine.
+//
+// The reference builds one n x n matrix per (nu, fold) cell.  Here every
+// fold's distance matrices for ALL grid values come out of one launch (one
+// sort per pair serves every nu), stay on the device in packed form, and
+// are embedded and scored there; only scalars and the final embedding come
+// back to the host.  Host control flow (folds, argmin with ties to the
+// smaller nu, refit) follows the reference line by line.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dmat.cuh"
+#include "dmat_kernels.cuh"
+#include "fit.h"
+#include "kernels.cuh"
+#include "lib_internal.h"
+
+namespace gmds {
+
+namespace {
+
+// Rng::uniform_below + shuffle_indices (rng.cpp:29-37, 65-70) on std::mt19937_64.
+uint64_t uniform_below(std::mt19937_64& g, uint64_t bound) {
+  if (bound <= 1) return 0;
+  const uint64_t limit = bound * ((~uint64_t{0}) / bound);
+  for (;;) {
+    const uint64_t x = g();
+    if (x < limit) return x % bound;
+  }
+}
+
+// make_folds (tune.cpp:39-56)
+std::vector<std::vector<int>> make_folds(int n, int k, uint64_t seed) {
+  std::vector<int> idx(static_cast<size_t>(n));
+  std::iota(idx.begin(), idx.end(), 0);
+  std::mt19937_64 g(seed);
+  for (size_t i = idx.size(); i > 1; --i) std::swap(idx[i - 1], idx[static_cast<size_t>(uniform_below(g, i))]);
+  std::vector<std::vector<int>> folds(static_cast<size_t>(k));
+  const int base = n / k, extra = n % k;
+  int off = 0;
+  for (int f = 0; f < k; ++f) {
+    const int size = base + (f < extra ? 1 : 0);
+    folds[f].assign(idx.begin() + off, idx.begin() + off + size);
+    std::sort(folds[f].begin(), folds[f].end());
+    off += size;
+  }
+  return folds;
+}
+
+// NuGrid::from_values (tune.cpp:74-83)
+void check_grid(const double* g, int m) {
+  if (m < 1) fail(GMDS_INVALID_CONFIG, "NuGrid: empty grid");
+  for (int i = 0; i < m; ++i) {
+    if (!(g[i] > 1.0)) fail(GMDS_INVALID_CONFIG, "NuGrid: every value must be > 1");
+    if (i > 0 && !(g[i] > g[i - 1]))
+      fail(GMDS_INVALID_CONFIG, "NuGrid: values must be strictly increasing (no duplicates)");
+  }
+}
+
+// Distance matrices of X (device, row-major) for several nu from one launch.
+std::vector<std::unique_ptr<gmds_dmat>> gini_multi(const void* dX, gmds_dtype xt, int64_t n, int64_t p,
+                                                   const double* nus, int nnu, cudaStream_t st) {
+  const int64_t per = packed_elems(n);
+  auto buf = std::make_shared<DevBuf<unsigned char>>(static_cast<size_t>(per) * nnu * sizeof(double));
+  GMDS_CUDA(cudaMemsetAsync(buf->get(), 0, static_cast<size_t>(per) * nnu * sizeof(double), st));
+  DevBuf<int> flag(1);
+  GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
+  run_gini(dX, xt, n, p, nus, nnu, GMDS_F64, 1, buf->get(), 0, 1, st, flag.get());
+  check_flag(flag.get(), st);
+  std::vector<std::unique_ptr<gmds_dmat>> out;
+  for (int v = 0; v < nnu; ++v) {
+    auto d = std::make_unique<gmds_dmat>();
+    d->n = n;
+    d->storage = GMDS_F64;
+    d->shared = buf;
+    d->offset = static_cast<size_t>(per) * v * sizeof(double);
+    dmat_finish(d.get(), st);
+    out.push_back(std::move(d));
+  }
+  return out;
+}
+
+struct Emb {
+  std::vector<double> coords;
+  double stress = 0.0;
+};
+
+// embed_distances (tune.cpp:20-33): classical, or minimize_stress with a default StressConfig.
+Emb embed(const gmds_dmat* D, int q, int method, uint64_t seed, cudaStream_t st) {
+  Emb e;
+  e.coords.assign(static_cast<size_t>(D->n) * q, 0.0);
+  if (method == GMDS_M_CLASSICAL) {
+    std::vector<double> ev(static_cast<size_t>(q));
+    int cc = 0;
+    double cm = 0.0;
+    classical_mds_dev(D, q, e.coords.data(), ev.data(), &cc, &cm, &e.stress, st);
+    return e;
+  }
+  gmds_stress_cfg cfg{};
+  cfg.kind = method - 1;  // EmbeddingMethod -> StressKind
+  cfg.huber_delta = std::nan("");
+  cfg.smacof_weights = nullptr;
+  cfg.max_iters = 300;
+  cfg.rel_tol = 1e-6;
+  cfg.seed = seed;
+  gmds_fit_result r{};
+  r.coords = e.coords.data();
+  minimize_stress_dev(D, q, cfg, nullptr, &r, st, nullptr);
+  e.stress = r.stress;
+  return e;
+}
+
+double kruskal_of(const gmds_dmat* D, const double* coords, int q, cudaStream_t st) {
+  // kruskal_stress (embed.cpp:462-475)
+  if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
+  Engine E(D, q, st);
+  E.upload(coords, E.Y.get());
+  const double* y = E.Y.get();
+  return E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
+}
+
+std::vector<double> rows_of(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                            const std::vector<int>& rows) {
+  // select_rows (tune.cpp:14-18) into a row-major fp64 block (fp32 widens exactly)
+  std::vector<double> out(rows.size() * static_cast<size_t>(p));
+  for (size_t r = 0; r < rows.size(); ++r)
+    for (int64_t c = 0; c < p; ++c) {
+      const int64_t idx = (lx == GMDS_ROW_MAJOR) ? rows[r] * p + c : c * n + rows[r];
+      out[r * p + c] = (xt == GMDS_F32) ? static_cast<double>(static_cast<const float*>(X)[idx])
+                                        : static_cast<const double*>(X)[idx];
+    }
+  return out;
+}
+
+DevBuf<double> upload_f64(const std::vector<double>& h, cudaStream_t st) {
+  DevBuf<double> d(h.size());
+  GMDS_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  return d;
+}
+
+}  // namespace
+
+}  // namespace gmds
+
+using namespace gmds;
+
+extern "C" {
+
+gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                         const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
+                         double* mean_stress, double* nu_star, double* coords, double* stress) {
+  return guard([&] {
+    check_grid(grid, m);
+    if (k_folds < 1) fail(GMDS_INVALID_CONFIG, "tune_nu: k_folds must be >= 1");
+    if (n < k_folds) fail(GMDS_INVALID_CONFIG, "tune_nu: more folds than rows");
+    const auto folds = make_folds(static_cast<int>(n), k_folds, seed);
+    for (const auto& f : folds)
+      if (static_cast<int>(f.size()) < q + 1)
+        fail(GMDS_INVALID_CONFIG, "tune_nu: a fold has " + std::to_string(f.size()) +
+                                      " points, need at least p + 1 = " + std::to_string(q + 1));
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    require_device();
+    Stream st;
+    std::vector<double> cell(static_cast<size_t>(m) * k_folds, 0.0);
+    for (int f = 0; f < k_folds; ++f) {
+      const std::vector<double> Xf = rows_of(X, xt, lx, n, p, folds[f]);
+      const int64_t nf = static_cast<int64_t>(folds[f].size());
+      if (nf < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+      DevBuf<double> dX = upload_f64(Xf, st.s);
+      const auto Ds = gini_multi(dX.get(), GMDS_F64, nf, p, grid, m, st.s);
+      for (int g = 0; g < m; ++g) {
+        const gmds_dmat* D = Ds[g].get();
+        if (D->max_val <= 0.0) {  // all points coincide (tune.cpp:106-110)
+          cell[static_cast<size_t>(g) * k_folds + f] = 0.0;
+          continue;
+        }
+        const Emb e = embed(D, q, method, seed, st.s);
+        cell[static_cast<size_t>(g) * k_folds + f] = kruskal_of(D, e.coords.data(), q, st.s);
+      }
+    }
+    for (int g = 0; g < m; ++g) {
+      double acc = 0.0;
+      for (int f = 0; f < k_folds; ++f) acc += cell[static_cast<size_t>(g) * k_folds + f];
+      mean_stress[g] = acc / static_cast<double>(k_folds);
+    }
+    int best = 0;
+    for (int g = 1; g < m; ++g)
+      if (mean_stress[g] < mean_stress[best]) best = g;  // ties keep the smaller nu
+    *nu_star = grid[best];
+    std::vector<int> all(static_cast<size_t>(n));
+    std::iota(all.begin(), all.end(), 0);
+    DevBuf<double> dX = upload_f64(rows_of(X, xt, lx, n, p, all), st.s);
+    const auto Dfull = gini_multi(dX.get(), GMDS_F64, n, p, nu_star, 1, st.s);
+    const Emb e = embed(Dfull[0].get(), q, method, seed, st.s);
+    std::memcpy(coords, e.coords.data(), e.coords.size() * sizeof(double));
+    *stress = e.stress;
+  });
+}
+
+gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                                  int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
+                                  double* nu_star, double* coords, double* stress) {
+  return guard([&] {
+    if (outer_iters < 1) fail(GMDS_INVALID_CONFIG, "alternating_tune: need at least one outer iteration");
+    check_grid(grid, m);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    require_device();
+    Stream st;
+    std::vector<int> all(static_cast<size_t>(n));
+    std::iota(all.begin(), all.end(), 0);
+    DevBuf<double> dX = upload_f64(rows_of(X, xt, lx, n, p, all), st.s);
+    // every grid value's D from one sort per pair, reused by all outer iterations
+    const auto Dgrid = gini_multi(dX.get(), GMDS_F64, n, p, grid, m, st.s);
+    double nu = 2.0;
+    Emb emb;
+    for (int t = 0; t < outer_iters; ++t) {
+      const auto D = gini_multi(dX.get(), GMDS_F64, n, p, &nu, 1, st.s);
+      emb = embed(D[0].get(), q, GMDS_M_SAMMON, seed, st.s);
+      int best = 0;
+      std::vector<double> sweep(static_cast<size_t>(m));
+      for (int g = 0; g < m; ++g) sweep[g] = kruskal_of(Dgrid[g].get(), emb.coords.data(), q, st.s);
+      for (int g = 1; g < m; ++g)
+        if (sweep[g] < sweep[best]) best = g;
+      nu = grid[best];
+      nu_path[t] = nu;
+    }
+    *nu_star = nu;
+    std::memcpy(coords, emb.coords.data(), emb.coords.size() * sizeof(double));
+    *stress = emb.stress;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+"""GPU parity: rank + distance kernels (through the C-ABI) vs the oracle and
+the reference's golden vectors.  Ranks bit-exact; distances within the
+north-star 1e-6 max-normalised tolerance (observed ~1e-15)."""
+import numpy as np
+import pytest
+
+from oracle import gini_oracle as O
+from _util import unpad
+
+pytestmark = pytest.mark.gpu
+
+G = pytest.importorskip("paper_2605_25124_b200.gmds")
+
+TOL = 1e-6  # north_star: distance matrix within 1e-6 relative, max-normalised
+
+
+def maxnorm_err(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    scale = max(np.max(np.abs(b)), 1e-300)
+    return float(np.max(np.abs(a - b)) / scale) if a.size else 0.0
+
+
+def test_device_visible():
+    assert G.device_count() >= 1
+
+
+def test_midrank_golden_bitexact(golden):
+    g = golden("midrank")
+    for v, r, m in zip(g["values"], g["ranks"], g["lengths"]):
+        assert np.array_equal(G.midrank(unpad(v, m)), unpad(r, m))
+
+
+@pytest.mark.parametrize("d", [1, 2, 31, 32, 33, 100, 511, 1024, 1025, 3000, 20000])
+def test_midrank_batch_vs_oracle(d):
+    rng = np.random.default_rng(d)
+    V = rng.integers(-5, 6, size=(7, d)).astype(np.float64) * 0.25
+    V[:, ::3] = rng.standard_normal(V[:, ::3].shape)
+    V[V == 0.0] = -0.0
+    got = G.midrank_batch(V)
+    for k in range(V.shape[0]):
+        assert np.array_equal(got[k], O.midrank(V[k]))
+
+
+def test_midrank_errors():
+    with pytest.raises(G.InvalidInput):
+        G.midrank([1.0, np.nan])
+    with pytest.raises(G.InvalidInput):
+        G.midrank([np.inf])
+
+
+@pytest.mark.parametrize("p,dtype", [(8, np.float64), (20, np.float64), (128, np.float32), (784, np.float32),
+                                     (784, np.float64), (1025, np.float32)])
+def test_pair_midranks_bitexact(p, dtype):
+    rng = np.random.default_rng(p)
+    n = 40
+    X = rng.random((n, p))
+    X[rng.random((n, p)) < 0.8] = 0.0  # heavy exact-zero ties (config 3 shape)
+    X[3] = X[5]                        # duplicated row: all-tied z
+    X = X.astype(dtype)
+    I = np.array([0, 3, 1, 7, 39, 12])
+    J = np.array([1, 5, 2, 8, 0, 30])
+    got = G.pair_midranks(X, I, J)
+    ref = O.pair_midranks(X.astype(np.float64), I, J)
+    assert np.array_equal(got, ref)
+
+
+def test_known_answers():
+    x, y = [10.0, 1200.0], [10.0, 12.0]
+    assert G.gen_gini_distance(x, y, 2.0) == 594.0
+    assert G.gen_gini_distance(x, y, 3.0) == 594.0
+    assert G.gen_gini_distance(x, x, 3.5) == 0.0
+    ones = np.ones(5)
+    for nu in (1.5, 2.0, 3.0, 5.0):
+        assert G.gen_gini_distance(2.0 * ones, -6.0 * ones, nu) == 0.0  # egalitarian null
+    D = G.pairwise_matrix(np.array([[10.0, 1200.0], [10.0, 12.0]]), 2.0)
+    assert D[0, 1] == 594.0 and D[1, 0] == 594.0 and D[0, 0] == 0.0
+    D = G.pairwise_matrix(np.array([[1.0, 2.0, 3.0], [1.0, 2.0, 3.0]]), 2.5)
+    assert D[0, 1] == 0.0
+
+
+def test_distance_golden(golden):
+    g = golden("distance")
+    for x, y, m, nu, dist in zip(g["x"], g["y"], g["lengths"], g["nu"], g["distance"]):
+        got = G.gen_gini_distance(unpad(x, m), unpad(y, m), float(nu))
+        assert abs(got - dist) <= 1e-12 * max(1.0, abs(dist))
+
+
+def test_pairwise_golden(golden):
+    g = golden("pairwise")
+    for name in ("t888", "t321", "c1", "ties"):
+        X = g[f"{name}_X"]
+        iu = np.triu_indices(X.shape[0], 1)
+        nus = list(g[f"{name}_nus"])
+        Ds = G.pairwise_gini(X, nus)
+        for k in range(len(nus)):
+            assert maxnorm_err(Ds[k][iu], g[f"{name}_D{k}"]) <= 1e-13
+            assert np.array_equal(Ds[k], Ds[k].T) and np.all(np.diag(Ds[k]) == 0.0)
+        E = G.pairwise_matrix(X, None)
+        assert np.array_equal(E[iu], g[f"{name}_E"])  # Euclidean branch is bit-exact
+
+
+@pytest.mark.parametrize("n,p,dtype,nus", [(64, 1, np.float64, [2.0]), (50, 33, np.float64, [1.1, 2.0, 8.0]),
+                                           (97, 128, np.float32, [1.5, 2.0, 3.0, 5.0]),
+                                           (40, 784, np.float32, [2.0]), (33, 784, np.float64, [1.3, 4.0]),
+                                           (20, 1100, np.float32, [2.0, 3.0])])
+def test_pairwise_vs_oracle(n, p, dtype, nus):
+    rng = np.random.default_rng(n * p)
+    X = rng.lognormal(0.0, 1.0, (n, p))
+    X[rng.random((n, p)) < 0.5] = 0.0
+    X[4] = X[9]
+    X = X.astype(dtype)
+    Ds = G.pairwise_gini(X, nus)
+    for k, nu in enumerate(nus):
+        ref = O.pairwise_matrix(X.astype(np.float64), nu)
+        assert maxnorm_err(Ds[k], ref) <= TOL
+        assert Ds[k][4, 9] == 0.0
+
+
+def test_pairwise_fp32_output():
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((70, 20))
+    D32 = G.pairwise_gini(X, [2.0], out_dtype=np.float32)[0]
+    ref = O.pairwise_matrix(X, 2.0)
+    assert D32.dtype == np.float32 and maxnorm_err(D32, ref) <= 1e-6
+
+
+def test_pairwise_colmajor_input():
+    rng = np.random.default_rng(8)
+    X = np.asfortranarray(rng.standard_normal((45, 12)))
+    assert maxnorm_err(G.pairwise_matrix(X, 1.7), O.pairwise_matrix(np.ascontiguousarray(X), 1.7)) <= 1e-13
+
+
+def test_pairwise_errors():
+    with pytest.raises(G.InvalidConfig):
+        G.pairwise_matrix(np.zeros((3, 2)), 1.0)
+    with pytest.raises(G.InvalidConfig):
+        G.pairwise_matrix(np.zeros((3, 2)), 0.5)
+    with pytest.raises(G.InvalidInput):
+        G.pairwise_matrix(np.zeros((1, 2)), 2.0)
+    with pytest.raises(G.InvalidInput):
+        G.pairwise_matrix(np.zeros((3, 0)), 2.0)
+    X = np.zeros((3, 2))
+    X[1, 1] = np.nan
+    with pytest.raises(G.InvalidInput):
+        G.pairwise_matrix(X, 2.0)
+    with pytest.raises(G.InvalidInput):
+        G.gen_gini_distance([1.0, 2.0], [1.0], 2.0)
+
+
+def test_device_entry_sharded_matches_full():
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(9)
+    X = rng.random((300, 64)).astype(np.float32)
+    dX = torch.from_numpy(X).cuda()
+    full = torch.zeros((2, 300, 300), dtype=torch.float64, device="cuda")
+    G.pairwise_gini_device(dX.data_ptr(), G.F32, 300, 64, [2.0, 3.0], G.F64, False, full.data_ptr())
+    sh = torch.zeros_like(full)
+    for s in range(3):
+        G.pairwise_gini_device(dX.data_ptr(), G.F32, 300, 64, [2.0, 3.0], G.F64, False, sh.data_ptr(), s, 3)
+    torch.cuda.synchronize()
+    assert torch.equal(full, sh)
+    ref = O.pairwise_matrix(X.astype(np.float64), 3.0)
+    assert maxnorm_err(full[1].cpu().numpy(), ref) <= 1e-12

@@ -1,0 +1,250 @@
+"""GPU parity: stress losses / gradients, classical MDS, minimize_stress
+trajectories and the nu-tuning callers vs the oracle and the reference's
+golden outputs.  Contract (north_star): stress trajectory within 1e-4
+relative for the first 50 iterations, final stress within 1%."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import gini_oracle as O
+
+pytestmark = pytest.mark.gpu
+G = pytest.importorskip("paper_2605_25124_b200.gmds")
+
+TRAJ = 1e-4
+FINAL = 1e-2
+
+
+def c1(golden):
+    g = golden("stress")
+    n = 200
+    D = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    D[iu] = g["c1_D"]
+    return g, D + D.T
+
+
+def rand_dissim(seed, n, dim=5):
+    rng = np.random.default_rng(seed)
+    P = rng.uniform(-2, 2, (n, dim))
+    D = np.sqrt(np.linalg.norm(P[:, None] - P[None], axis=2)) + 0.1
+    np.fill_diagonal(D, 0.0)
+    return D
+
+
+@pytest.mark.parametrize("kind", ["kruskal", "huber", "sammon", "smacof"])
+@pytest.mark.parametrize("q", [1, 2, 3, 5])
+def test_loss_and_gradient(kind, q):
+    D = rand_dissim(q, 150)
+    rng = np.random.default_rng(10 + q)
+    Y = rng.standard_normal((150, q))
+    hd = 0.7 if kind == "huber" else None
+    Dm = G.dmat_from_host(D)
+    assert G.stress_loss(kind, Y, Dm, hd) == pytest.approx(O.stress_loss(kind, Y, D, hd), rel=1e-12)
+    g = G.stress_gradient(kind, Y, Dm, hd)
+    gr = O.stress_gradient(kind, Y, D, hd)
+    assert np.max(np.abs(g - gr)) <= 1e-11 * np.max(np.abs(gr))
+
+
+def test_kruskal_and_golden_gradients(golden):
+    g, D = c1(golden)
+    Y = g["cmds_coords"]
+    assert G.kruskal_stress(Y, D) == pytest.approx(float(g["cmds_stress"]), rel=1e-12)
+    for kind in ("kruskal", "sammon", "huber"):
+        hd = float(g["huber_history"][0] * 0 + g["huber_huber_delta"]) if kind == "huber" else None
+        assert G.stress_loss(kind, Y, D, hd) == pytest.approx(float(g[f"{kind}_loss0"]), rel=1e-12)
+        gg = G.stress_gradient(kind, Y, D, hd)
+        assert np.max(np.abs(gg - g[f"{kind}_grad0"])) <= 1e-10 * np.max(np.abs(g[f"{kind}_grad0"]))
+
+
+def test_fp32_storage_loss():
+    D = rand_dissim(3, 300)
+    Y = np.random.default_rng(1).standard_normal((300, 2))
+    assert G.kruskal_stress(Y, G.dmat_from_host(D, G.F32)) == pytest.approx(O.kruskal_stress(Y, D), rel=1e-6)
+
+
+def test_classical_mds_golden(golden):
+    g, D = c1(golden)
+    r = G.classical_mds(D, 2)
+    assert np.allclose(r["coords"], g["cmds_coords"], atol=1e-9)
+    assert np.allclose(r["eigenvalues"], g["cmds_eig"], rtol=1e-11)
+    assert r["clamped_mass"] == pytest.approx(float(g["cmds_clamped_mass"]), rel=1e-9)
+    assert r["stress"] == pytest.approx(float(g["cmds_stress"]), rel=1e-10)
+
+
+def test_classical_known_answers():
+    # test_embed.cpp:90-98: two points at distance 2 -> +1 / -1, eigenvalue 2
+    r = G.classical_mds(np.array([[0.0, 2.0], [2.0, 0.0]]), 1)
+    assert r["coords"][0, 0] == pytest.approx(1.0, rel=1e-12) and r["coords"][1, 0] == pytest.approx(-1.0, rel=1e-12)
+    assert r["eigenvalues"][0] == pytest.approx(2.0, rel=1e-12)
+    sq = G.pairwise_matrix(np.array([[0, 0], [1, 0], [1, 1], [0, 1.0]]), None)
+    assert G.classical_mds(sq, 2)["stress"] < 1e-8
+    with pytest.raises(G.InvalidInput):
+        G.classical_mds(sq, 4)
+    with pytest.raises(G.InvalidInput):
+        G.classical_mds(sq, 0)
+
+
+def test_classical_clamped_indefinite():
+    # test_embed.cpp:100-122: a Gini metric whose Gram matrix is indefinite
+    for seed in range(64):
+        rng = O.Rng(seed)
+        X = O.random_matrix(rng, 8, 3, 5.0)
+        D = O.pairwise_matrix(X, 3.0)
+        lam = np.linalg.eigvalsh(O.double_center(D * D))
+        if lam[0] < -1e-9 * np.max(np.abs(lam)):
+            r = G.classical_mds(D, 7)
+            ref = O.classical_mds(D, 7)
+            assert r["clamped_count"] == ref.clamped_count > 0
+            assert r["clamped_mass"] == pytest.approx(ref.clamped_mass, rel=1e-9)
+            assert r["eigenvalues"][6] < 0 and np.max(np.abs(r["coords"][:, 6])) == 0.0
+            assert r["stress"] == pytest.approx(ref.stress, rel=1e-9)
+            return
+    pytest.fail("no indefinite instance found")
+
+
+@pytest.mark.parametrize("kind", ["kruskal", "sammon", "smacof", "huber"])
+def test_minimize_stress_c1_golden(golden, kind):
+    # config 1 (n=200, p=8, nu=2, q=2), classical init, 500 iterations, vs the reference run
+    g, D = c1(golden)
+    hd = float(g["huber_huber_delta"]) if kind == "huber" else None
+    e = G.minimize_stress(D, 2, kind, huber_delta=hd, max_iters=500, rel_tol=1e-300)
+    ref = g[f"{kind}_history"]
+    h = np.array(e["stress_history"])
+    k = min(51, len(ref))
+    assert len(h) >= k
+    assert np.max(np.abs(h[:k] - ref[:k]) / ref[:k]) <= TRAJ
+    assert abs(e["stress"] - ref[-1]) <= FINAL * ref[-1]
+    assert e["iterations"] == int(g[f"{kind}_iterations"])
+
+
+@pytest.mark.parametrize("kind", ["kruskal", "sammon", "smacof"])
+def test_minimize_stress_fp32_storage(golden, kind):
+    g, D = c1(golden)
+    e = G.minimize_stress(D, 2, kind, max_iters=200, rel_tol=1e-300, storage=G.F32)
+    ref = g[f"{kind}_history"]
+    h = np.array(e["stress_history"])
+    assert np.max(np.abs(h[:51] - ref[:51]) / ref[:51]) <= TRAJ
+    assert abs(e["stress"] - ref[200]) <= FINAL * ref[200]
+
+
+@pytest.mark.parametrize("kind", ["kruskal", "sammon", "smacof"])
+def test_minimize_stress_seeded_init(kind):
+    # config 1's seeded N(0, 1e-2) init vs the oracle fed the same Y0
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((120, 8))
+    D = O.pairwise_matrix(X, 2.0)
+    Y0 = rng.normal(0.0, 0.1, (120, 2))
+    e = G.minimize_stress(D, 2, kind, max_iters=60, rel_tol=1e-300, Y0=Y0)
+    r = O.minimize_stress(D, 2, kind, max_iters=60, rel_tol=1e-300, Y0=Y0)
+    h, hr = np.array(e["stress_history"]), np.array(r.stress_history)
+    assert len(h) == len(hr)
+    assert np.max(np.abs(h[:51] - hr[:51]) / hr[:51]) <= TRAJ
+
+
+@pytest.mark.parametrize("kind", ["kruskal", "huber", "sammon", "smacof"])
+def test_default_config_fits_golden(golden, kind):
+    g = golden("stress")
+    D = g[f"rd_{kind}_D"]
+    e = G.minimize_stress(D, 2, kind, huber_delta=(0.5 if kind == "huber" else None))
+    assert e["iterations"] == int(g[f"rd_{kind}_iterations"])
+    assert e["converged"] == bool(g[f"rd_{kind}_converged"])
+    assert e["stress"] == pytest.approx(float(g[f"rd_{kind}_stress"]), rel=1e-6)
+
+
+def test_huber_auto_delta(golden):
+    g = golden("stress")
+    e = G.minimize_stress(g["auto_D"], 2, "huber")
+    assert e["huber_delta"] == pytest.approx(float(g["auto_huber_delta"]), rel=1e-15)
+    assert e["stress"] == pytest.approx(float(g["auto_stress"]), rel=1e-6)
+
+
+def test_unit_square_all_kinds():
+    # test_embed.cpp:272-284
+    sq = G.pairwise_matrix(np.array([[0, 0], [1, 0], [1, 1], [0, 1.0]]), None)
+    for kind in ("kruskal", "huber", "sammon", "smacof"):
+        e = G.minimize_stress(sq, 2, kind, huber_delta=(1.0 if kind == "huber" else None))
+        assert e["stress"] < 1e-6 and e["converged"]
+
+
+def test_smacof_monotone_and_weighted():
+    for seed in range(5):
+        D = rand_dissim(100 + seed, 20)
+        h = G.minimize_stress(D, 2, "smacof")["stress_history"]
+        assert all(h[t] <= h[t - 1] * (1 + 1e-12) + 1e-15 for t in range(1, len(h)))
+    D = rand_dissim(7, 25)
+    W = np.random.default_rng(3).uniform(0.5, 2.0, (25, 25))
+    W = (W + W.T) / 2
+    e = G.minimize_stress(D, 2, "smacof", weights=W, max_iters=40, rel_tol=1e-300)
+    r = O.minimize_stress(D, 2, "smacof", weights=W, max_iters=40, rel_tol=1e-300)
+    assert np.max(np.abs(np.array(e["stress_history"]) - r.stress_history) / r.stress_history[0]) <= 1e-8
+
+
+def test_stress_error_contract():
+    D = np.array([[0, 0, 1], [0, 0, 1], [1, 1, 0.0]])
+    with pytest.raises(G.DegenerateInput):
+        G.stress_loss("sammon", np.zeros((3, 2)), D)
+    with pytest.raises(G.InvalidConfig):
+        G.stress_loss("huber", np.zeros((3, 2)), D)
+    with pytest.raises(G.InvalidConfig):
+        G.stress_loss("huber", np.zeros((3, 2)), D, huber_delta=-1.0)
+    with pytest.raises(G.DegenerateInput):
+        G.kruskal_stress(np.zeros((2, 1)), np.zeros((2, 2)))
+    with pytest.raises(G.InvalidConfig):
+        G.minimize_stress(D, 2, "kruskal", max_iters=0)
+    with pytest.raises(G.InvalidConfig):
+        G.minimize_stress(D, 2, "kruskal", rel_tol=0.0)
+    with pytest.raises(G.InvalidInput):
+        G.dmat_from_host(np.array([[0.0, 1.0], [2.0, 0.0]]))
+    Y = np.zeros((3, 2))
+    Y[0, 0] = np.nan
+    with pytest.raises(G.InvalidInput):
+        G.kruskal_stress(Y, D)
+
+
+def test_nonconvergence_flag():
+    # test_embed.cpp:343-358
+    D = rand_dissim(21, 14)
+    a = G.minimize_stress(D, 2, "sammon")
+    b = G.minimize_stress(D, 2, "sammon")
+    assert np.array_equal(a["coords"], b["coords"]) and a["stress"] == b["stress"]  # deterministic
+    t = G.minimize_stress(D, 2, "sammon", max_iters=1, rel_tol=1e-14)
+    assert not t["converged"] and t["iterations"] == 1
+
+
+def test_tune_golden(golden):
+    g = golden("tune")
+    r = G.tune_nu(g["u_X"], 2, g["u_grid"], 3, "classical", 4)
+    assert np.allclose(r["mean_stress"], g["u_mean"], rtol=1e-9)
+    assert r["nu_star"] == float(g["u_nu_star"])
+    assert np.allclose(r["coords"], g["u_coords"], atol=1e-8)
+    r = G.tune_nu(g["s_X"], 2, g["s_grid"], 2, "smacof", 11)
+    assert np.allclose(r["mean_stress"], g["s_mean"], rtol=1e-6)
+    a = G.alternating_tune(g["a_X"], 2, 3, g["a_grid"], 17)
+    assert a["nu_path"] == list(g["a_path"]) and a["nu_star"] == float(g["a_nu_star"])
+    assert a["stress"] == pytest.approx(float(g["a_stress"]), rel=1e-6)
+
+
+def test_tune_contract():
+    X = np.full((12, 3), 4.2)
+    r = G.tune_nu(X, 1, O.nugrid_linspace(1.5, 3.5, 4), 3, "classical", 5)
+    assert r["nu_star"] == 1.5 and all(s == 0.0 for s in r["mean_stress"])
+    X = np.random.default_rng(5).uniform(-1, 1, (9, 3))
+    with pytest.raises(G.InvalidConfig):
+        G.tune_nu(X, 3, [2.0], 3)
+    with pytest.raises(G.InvalidConfig):
+        G.tune_nu(X, 2, [2.0], 0)
+    with pytest.raises(G.InvalidConfig):
+        G.tune_nu(X, 2, [2.0], 10)
+    with pytest.raises(G.InvalidConfig):
+        G.tune_nu(X, 2, [2.0, 2.0], 2)
+    with pytest.raises(G.InvalidConfig):
+        G.alternating_tune(X, 2, 0, [2.0])
+    # one fold + singleton grid == direct pipeline (test_tune.cpp:36-46)
+    X = O.random_matrix(O.Rng(2), 15, 4, 2.0)
+    r = G.tune_nu(X, 2, [2.4], 1, "classical", 9)
+    D = G.pairwise_matrix(X, 2.4)
+    direct = G.classical_mds(D, 2)
+    assert r["mean_stress"][0] == pytest.approx(G.kruskal_stress(direct["coords"], D), rel=1e-12)
+    assert np.allclose(r["coords"], direct["coords"], atol=1e-12)
