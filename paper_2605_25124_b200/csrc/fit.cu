@@ -242,7 +242,6 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
   IterResult r;
   const int kind = rp.kind;
   double* Yc[kMaxCand];
-  for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();
   const double* y0 = E.Y.get();
   double f = E.loss_of(kind, E.loss_raw(kind, rp.delta, &y0, 1)[0]);
   r.history.push_back(f);
@@ -275,6 +274,7 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
         s.v[c] = sv;
         sv *= 0.5;
       }
+      for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();  // buffers rotate on acceptance
       launch_axpy_cand(E.Y.get(), E.graw.get(), E.n * E.Q, s, Yc, E.st);
       const std::vector<double> raws = E.loss_raw(kind, rp.delta, Yc, s.n);
       for (int c = 0; c < s.n; ++c) {
