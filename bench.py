@@ -1,0 +1,410 @@
+#!/usr/bin/env python3
+"""bench.py -- BASELINE.json's metric on the B200 engine (and the reference arm).
+
+Metric: "Gini distance-matrix pairs/sec; stress iters/sec at n=20k,p=784,q=2
+vs roofline".  Workload (BASELINE metric config = SURVEY 8(d) "metric" row):
+n = 20000 rows, p = 784 features, fp32, image-like synthetic data (80% exact
+zeros per row, the rest uniform over the 256 levels k/255 plus N(0, 0.1^2)
+noise, clipped to [0, 1]; seeded numpy PCG64), nu = 2, q = 2.
+
+One step = one full Gini distance matrix (n(n-1)/2 = 199,990,000 pairs, one
+sort per pair) written as the packed fp32 triangle the fit consumes, followed
+by S Kruskal stress iterations (Armijo gradient descent, seeded N(0, 0.1^2)
+init, rel_tol 1e-300) on that matrix.
+  value  = distance pairs/s (device-resident X, CUDA events on the launch stream)
+  stress = stress iterations/s of the same step (reported beside value)
+  e2e    = pairs/s through the drop-in C-ABI pairwise_matrix call
+           (gmds_pairwise_gini: pinned host X in, host n x n fp64 D out;
+           host<->device copies inside the timed region)
+
+``--impl reference`` times the reference's own CPU implementation (the
+UNMODIFIED reference core compiled by oracle/Makefile, all host threads) on a
+bounded sample of the same workload.  Multi-GPU (torchrun): the pair tiles are
+split across ranks (strong scaling, no collective on the data path); the
+timed region is bracketed by a barrier and the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N, P, Q, NU = 20000, 784, 2, 2.0
+STRESS_ITERS = 10
+SEED = 2605
+
+
+def make_image_like(n, p, seed=SEED):
+    """SURVEY 8(d) C3 generator: 80% exact zeros, 256 levels + N(0, 0.1^2) noise, clipped."""
+    g = np.random.default_rng(seed)
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < 0.8] = 0.0
+    return X.astype(np.float32)
+
+
+def ops_per_pair(p, nnu):
+    """p*ceil(log2 p) comparisons + p differences + 2*p*Nnu LUT FMAs."""
+    return p * int(np.ceil(np.log2(p))) + p + 2 * p * nnu
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.dev = device_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------------
+# reference arm / cpu baseline
+
+
+def reference_rate(X, seconds_target=12.0, threads=0):
+    """Reference pairs/s on host cores: the UNMODIFIED reference per-pair code
+    (gen_gini_distance under its own parallel_for) over a bounded block of rows.
+    Falls back to the oracle restatement when oracle/_ref was not built."""
+    from oracle import ref_lib
+
+    L = ref_lib.load()
+    n = X.shape[0]
+    Xd = np.ascontiguousarray(X, dtype=np.float64)
+    if L is not None:
+        ref_lib.set_max_threads(threads)
+        cores = ref_lib.max_threads()
+        kind = "reference"
+        # calibrate on one row per thread, then size the sample to ~seconds_target
+        rows = max(1, cores)
+        t0 = time.perf_counter()
+        ref_lib.gini_rows(Xd, NU, 0, rows)
+        dt = time.perf_counter() - t0
+        per_pair = dt / sum(n - 1 - i for i in range(rows))
+        want = int(seconds_target / per_pair)
+        rows = max(cores, int(np.ceil(want / max(1, n - 1) / cores)) * cores)
+        rows = min(rows, n - 1)
+        pairs = sum(n - 1 - i for i in range(rows))
+        t0 = time.perf_counter()
+        ref_lib.gini_rows(Xd, NU, 0, rows)
+        dt = time.perf_counter() - t0
+        sample = f"rows 0..{rows - 1} of the n={n}, p={X.shape[1]} matrix ({pairs} pairs), reference gen_gini_distance"
+        return pairs / dt, cores, kind, sample, dt
+    from oracle import gini_oracle as O
+
+    rows = 8
+    I, J = [], []
+    for i in range(rows):
+        I.extend([i] * (n - 1 - i))
+        J.extend(range(i + 1, n))
+    I, J = np.array(I), np.array(J)
+    t0 = time.perf_counter()
+    O.gini_pairs(Xd, I, J, NU)
+    dt = time.perf_counter() - t0
+    return I.size / dt, 1, "port", f"rows 0..{rows - 1} ({I.size} pairs), numpy restatement", dt
+
+
+def reference_stress_rate(seconds_cap=8.0):
+    """Reference serial Kruskal iterate loop (embed.cpp:222-272): per-iteration
+    time at n=2500 (on the reference's Euclidean distances of the same data --
+    the iterate loop's cost does not depend on the metric that built D, and a
+    Gini D at n=2500 would itself take ~40 s on the host), scaled to n=20000 by
+    the pair count (each iteration is >= 3 O(n^2) passes); an extrapolation."""
+    from oracle import ref_lib
+
+    if ref_lib.load() is None:
+        return None
+    n_s = 2500
+    Xs = make_image_like(n_s, P, seed=SEED + 1).astype(np.float64)
+    D = ref_lib.pairwise_matrix(Xs, None)
+    t0 = time.perf_counter()
+    r = ref_lib.minimize_stress(D, Q, "kruskal", max_iters=3, rel_tol=1e-300)
+    dt_with_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ref_lib.classical_mds(D, Q)
+    dt_init = time.perf_counter() - t0
+    per_iter = max(1e-9, (dt_with_init - dt_init) / max(1, r["iterations"]))
+    scale = (N * (N - 1)) / (n_s * (n_s - 1))
+    return {"iters_per_sec": 1.0 / (per_iter * scale), "sample": f"3 Kruskal iterations at n={n_s} "
+            f"({per_iter * 1e3:.1f} ms/iter), x{scale:.0f} pair-count extrapolation to n={N}", "cores": 1}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    X = make_image_like(N, P)
+    rate, cores, kind, sample, dt = reference_rate(X)
+    srate = reference_stress_rate()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "pairs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "metric: n=20000 p=784 image-like fp32 (widened exactly to f64), nu=2, q=2",
+                   "n": N, "p": P, "q": Q, "nu": NU},
+        "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": rate, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    if srate:
+        line["stress_iters_per_sec"] = srate["iters_per_sec"]
+        line["stress_sample"] = srate["sample"]
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "Gini distance-matrix pairs/sec; stress iters/sec at n=20k,p=784,q=2 vs roofline"
+
+
+# ---------------------------------------------------------------------------------------------------
+# B200 arm
+
+
+def run_engine(args, rank, world, dist):
+    import torch
+
+    from paper_2605_25124_b200 import gmds as G
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    G.lib().gmds_set_device(dev)
+    stream = torch.cuda.current_stream()
+    G.lib().gmds_set_stream(ctypes_void(stream.cuda_stream))
+
+    X = make_image_like(N, P)
+    dX = torch.from_numpy(X).cuda()
+    npairs = N * (N - 1) // 2
+    pe = G.packed_elems(N)
+    dD = torch.zeros(pe, dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def distance_step():
+        G.pairwise_gini_device(dX.data_ptr(), G.F32, N, P, [NU], G.F32, True, dD.data_ptr(), rank, world,
+                               stream.cuda_stream)
+
+    # ---- distance: warm-up, then K timed steps (L2 flushed between steps)
+    for _ in range(args.warmup):
+        distance_step()
+    barrier()
+    launches0 = G.launch_count()
+    times = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            distance_step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    barrier()
+    dist_launches = G.launch_count() - launches0
+    t_dist = max_over_ranks(dist, float(np.mean(times)))
+
+    # ---- stress: S Kruskal iterations on the packed matrix of this step (single-GPU fit;
+    # with several ranks every rank fits its own replica of the full matrix)
+    Dm = G.dmat_gini_device(dX.data_ptr(), G.F32, N, P, NU, G.F32)
+    Y0 = np.random.default_rng(SEED).normal(0.0, 0.1, (N, Q))
+    G.minimize_stress(Dm, Q, "kruskal", max_iters=2, rel_tol=1e-300, Y0=Y0)  # warm-up
+    barrier()
+    launches1 = G.launch_count()
+    stimes, siters, spasses = [], 0, 0
+    with ClockSampler(dev) as clk2:
+        for _ in range(max(1, args.steps)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = G.minimize_stress(Dm, Q, "kruskal", max_iters=STRESS_ITERS, rel_tol=1e-300, Y0=Y0)
+            e1.record(stream)
+            e1.synchronize()
+            stimes.append(e0.elapsed_time(e1) / 1e3)
+            siters += r["iterations"]
+            spasses += r["passes"]
+    stress_launches = G.launch_count() - launches1
+    t_stress = max_over_ranks(dist, float(np.sum(stimes)))
+    iters_per_sec = siters / t_stress
+    Dm.free()
+
+    # ---- e2e: the drop-in pairwise_matrix call, pinned host X -> host fp64 n x n D
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        Xh = torch.from_numpy(X).pin_memory().numpy()
+        Dh = torch.empty((1, N, N), dtype=torch.float64).pin_memory().numpy()
+        etimes = []
+        G.lib().gmds_set_stream(ctypes_void(0))
+        for k in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            G.lib().gmds_pairwise_gini(G._vp(Xh), G._i32(G.F32), G._i32(G.ROW_MAJOR), G._i64(N), G._i64(P),
+                                       G._p(np.array([NU])), G._i32(1), G._i32(G.F64), G._vp(Dh))
+            etimes.append(time.perf_counter() - t0)
+        G.lib().gmds_set_stream(ctypes_void(stream.cuda_stream))
+        e2e = {"value": npairs / float(np.mean(etimes)), "unit": "pairs/s", "h2d_bytes_per_step": int(X.nbytes),
+               "d2h_bytes_per_step": int(Dh.nbytes), "ms_per_step": float(np.mean(etimes)) * 1e3,
+               "call": "gmds_pairwise_gini (pairwise_matrix drop-in, fp64 n x n out)"}
+
+    # ---- roofline of the dominant kernel (gini_tile_kernel: the whole distance step is this kernel
+    # plus a 12 KB LUT upload and two 4-byte flag copies)
+    alu = ctypes_double()
+    G.lib().gmds_probe_alu(ctypes_ref(alu))
+    ops_pair = ops_per_pair(P, 1)
+    my_pairs = npairs  # all ranks together
+    achieved = my_pairs * ops_pair / t_dist
+    peaks = load_peaks()
+    stress_bytes = npairs * 4  # one read of the packed fp32 triangle per pass
+    pass_time = t_stress / max(1, spasses / max(1, world))
+    value = npairs / t_dist
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": (t_dist + t_stress / max(1, args.steps)) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded numpy PCG64, SURVEY 8(d) image-like generator)",
+        "config": {"workload": "metric: n=20000 p=784 q=2 nu=2 (BASELINE metric config; C3 generator at n=20k)",
+                   "n": N, "p": P, "q": Q, "nu": NU, "input_dtype": "f32", "D_storage": "f32 packed triangle",
+                   "stress_iters_per_step": STRESS_ITERS, "stress_kind": "kruskal (Armijo GD)",
+                   "init": "seeded N(0, 0.1^2) (SURVEY F4)", "l2": "flushed (256 MB write) before every "
+                   "distance step; the packed D (800 MB) exceeds L2 for the stress passes",
+                   "parallelism": f"pair tiles sharded over {world} GPU(s)"},
+        "distance_ms": t_dist * 1e3,
+        "stress_iters_per_sec": iters_per_sec,
+        "stress_ms_per_iter": 1e3 / iters_per_sec,
+        "stress_passes_per_iter": spasses / max(1, siters),
+        "gpu_launches": int(dist_launches + stress_launches),
+        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu.value / 1e12, "unit": "Tops/s",
+                     "frac": achieved / alu.value, "traffic": None,
+                     "kernel": "gini_tile_kernel", "ops_per_pair": ops_pair,
+                     "peak_source": "measured on this GPU by gmds_probe_alu (FFMA + IADD3/LOP3 lane-op rate)"},
+        "stress_roofline": {"bound": "hbm", "achieved": stress_bytes / pass_time / 1e9, "peak": peaks.get("hbm_gbs"),
+                            "unit": "GB/s", "frac": stress_bytes / pass_time / 1e9 / peaks.get("hbm_gbs", 6446.6),
+                            "traffic": None, "kernel": "stress_pass_kernel (+ reductions, per pass)",
+                            "bytes_per_pass": stress_bytes},
+        "clocks": clk.summary(),
+        "clocks_stress": clk2.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, kind, sample, _ = reference_rate(X, seconds_target=10.0)
+        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind, "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def ctypes_void(v):
+    import ctypes
+
+    return ctypes.c_void_p(v)
+
+
+def ctypes_double():
+    import ctypes
+
+    return ctypes.c_double()
+
+
+def ctypes_ref(x):
+    import ctypes
+
+    return ctypes.byref(x)
+
+
+def max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["engine", "reference"], default="engine")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    try:
+        run_engine(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

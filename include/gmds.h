@@ -53,6 +53,11 @@ int gmds_device_count(void);
 gmds_status gmds_set_device(int device);
 /* Number of libgmds kernel launches issued by this process so far (bench.py's gpu_launches). */
 int64_t gmds_launch_count(void);
+/* Make this thread's subsequent calls run on `stream` (a cudaStream_t; NULL
+ * restores private per-call streams).  Calls remain blocking. */
+gmds_status gmds_set_stream(void* stream);
+/* Roofline probe: measured FP32-FMA + INT lane-op rate of this GPU (ops/s). */
+gmds_status gmds_probe_alu(double* lane_ops_per_sec);
 
 /* ---- rank: midrank (metrics.hpp:71-72, metrics.cpp:101-110 -> midrank_into 42-56) ----
  * m vectors of length d, row-major (vector k at v + k*d).  ranks: m*d. */

@@ -87,36 +87,6 @@ DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, 
   return out;
 }
 
-void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
-              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag) {
-  const std::vector<double> lut = build_lut(static_cast<int>(p), nus, nnu);
-  DevBuf<double> dlut(lut.size());
-  GMDS_CUDA(cudaMemcpyAsync(dlut.get(), lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-  GiniTileArgs a{};
-  a.n = n;
-  a.d = static_cast<int>(p);
-  a.lut = dlut.get();
-  a.nnu = nnu;
-  a.packed = packed;
-  a.nb_packed = ceil_div(n, kPT);
-  a.out_stride = packed ? packed_elems(n) : n * n;
-  a.flag = dflag;
-  int64_t units;
-  if (p <= 1024) {
-    a.tile = gini_tile_size(static_cast<int>(p), xt, nnu);
-    a.nbt = ceil_div(n, a.tile);
-    units = a.nbt * (a.nbt + 1) / 2;
-  } else {
-    a.tile = 1;
-    a.nbt = n;
-    units = n * (n - 1) / 2;
-  }
-  a.tile_begin = units * shard / nshards;
-  a.tile_end = units * (shard + 1) / nshards;
-  launch_gini(a, dX, xt, dD, ot, st);
-  GMDS_CUDA(cudaStreamSynchronize(st));  // keeps dlut alive until the kernel is done
-}
-
 void check_flag(int* dflag, cudaStream_t st) {
   int flag = 0;
   GMDS_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -124,9 +94,44 @@ void check_flag(int* dflag, cudaStream_t st) {
   if (flag & 1) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
 }
 
-Stream::Stream() { GMDS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+namespace {
+thread_local cudaStream_t g_user_stream = nullptr;
+thread_local bool g_user_stream_set = false;
+}  // namespace
+
+// Calls use the caller's stream when one was set with gmds_set_stream (bench
+// timing with CUDA events on that stream); otherwise a private stream.
+Stream::Stream() {
+  if (g_user_stream_set) {
+    s = g_user_stream;
+    owned = false;
+  } else {
+    GMDS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+}
 Stream::~Stream() {
-  if (s) cudaStreamDestroy(s);
+  if (s && owned) cudaStreamDestroy(s);
+}
+
+// ALU roofline probe: independent FFMA (fma pipe) and IADD3/LOP3 (alu pipe)
+// chains, interleaved so both pipes issue every cycle.  Counts lane-ops.
+__global__ void alu_probe_kernel(float* out, int iters) {
+  float a0 = threadIdx.x * 1e-3f, a1 = a0 + 1.f, a2 = a0 + 2.f, a3 = a0 + 3.f;
+  unsigned b0 = threadIdx.x, b1 = b0 * 3u, b2 = b0 * 5u, b3 = b0 * 7u;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fmaf(a0, 0.999f, 1e-4f);
+      b0 = (b0 + 0x9e3779b9u) ^ b1;
+      a1 = fmaf(a1, 0.999f, 1e-4f);
+      b1 = (b1 + 0x7f4a7c15u) ^ b2;
+      a2 = fmaf(a2, 0.999f, 1e-4f);
+      b2 = (b2 + 0x94d049bbu) ^ b3;
+      a3 = fmaf(a3, 0.999f, 1e-4f);
+      b3 = (b3 + 0xbf58476du) ^ b0;
+    }
+  }
+  if (a0 + a1 + a2 + a3 == 1234.5f && (b0 ^ b1 ^ b2 ^ b3) == 77u) out[0] = 1.f;
 }
 
 }  // namespace gmds
@@ -152,6 +157,38 @@ gmds_status gmds_set_device(int device) {
 }
 
 int64_t gmds_launch_count(void) { return launch_count(); }
+
+gmds_status gmds_set_stream(void* stream) {
+  g_user_stream = static_cast<cudaStream_t>(stream);
+  g_user_stream_set = (stream != nullptr);
+  return GMDS_OK;
+}
+
+gmds_status gmds_probe_alu(double* lane_ops_per_sec) {
+  return guard([&] {
+    require_device();
+    int dev = 0, sms = 0;
+    GMDS_CUDA(cudaGetDevice(&dev));
+    GMDS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    DevBuf<float> out(1);
+    const int iters = 4096, blocks = sms * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    GMDS_CUDA(cudaEventCreate(&e0));
+    GMDS_CUDA(cudaEventCreate(&e1));
+    alu_probe_kernel<<<blocks, threads>>>(out.get(), 64);  // warm-up
+    GMDS_CUDA(cudaEventRecord(e0));
+    alu_probe_kernel<<<blocks, threads>>>(out.get(), iters);
+    GMDS_CUDA(cudaEventRecord(e1));
+    GMDS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    GMDS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    // per inner unroll: 4 FFMA + 4 x (IADD3 + LOP3) = 12 lane-ops
+    const double ops = static_cast<double>(blocks) * threads * iters * 16.0 * 12.0;
+    *lane_ops_per_sec = ops / (ms * 1e-3);
+  });
+}
 
 int64_t gmds_packed_elems(int64_t n) { return packed_elems(n); }
 

@@ -268,7 +268,9 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     int acc_c = -1;
     for (int halvings = 0; halvings < 60 && !accepted;) {
       Steps s{};
-      s.n = std::min(kMaxCand, 60 - halvings);
+      // first batch: step and step/2 (the common accept pattern after a doubling);
+      // further batches: four halvings per pass
+      s.n = std::min(halvings == 0 ? 2 : kMaxCand, 60 - halvings);
       double sv = step;
       for (int c = 0; c < s.n; ++c) {
         s.v[c] = sv;

@@ -1,0 +1,221 @@
+// Host orchestration of the Gini distance kernels (run_gini): row-store
+// preparation (bitmask-sparse rows when X is sparse), kernel and tile-size
+// selection, and the overflow pass.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "gini_split.cuh"
+#include "kernels.cuh"
+#include "lib_internal.h"
+
+namespace gmds {
+
+template <int KMAX>
+void launch_gini_split(const SplitArgs& sa, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, size_t smem,
+                       unsigned blocks, cudaStream_t st);
+template <int K>
+void launch_gini_list(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64_t* pairs, int64_t npairs, void* dout,
+                      gmds_dtype ot, cudaStream_t st);
+
+namespace {
+
+// warp per row: presence masks, running popcounts, per-row nonzero counts
+template <typename T>
+__global__ void row_mask_kernel(const T* __restrict__ X, int64_t n, int p, int W, uint32_t* __restrict__ masks,
+                                uint16_t* __restrict__ prefix, int* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n;
+       row += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    int run = 0;
+    for (int w = 0; w < W; ++w) {
+      const int e = w * 32 + lane;
+      const bool nz = (e < p) && (X[row * p + e] != T(0));
+      const unsigned m = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0) {
+        masks[row * W + w] = m;
+        prefix[row * W + w] = static_cast<uint16_t>(run);
+      }
+      run += __popc(m);
+    }
+    if (lane == 0) counts[row] = run;
+  }
+}
+
+template <typename T>
+__global__ void row_fill_kernel(const T* __restrict__ X, int64_t n, int p, int W, const uint32_t* __restrict__ masks,
+                                const uint16_t* __restrict__ prefix, const int64_t* __restrict__ rowptr,
+                                T* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n;
+       row += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    for (int w = 0; w < W; ++w) {
+      const int e = w * 32 + lane;
+      const unsigned m = masks[row * W + w];
+      if ((m >> lane) & 1u) vals[rowptr[row] + prefix[row * W + w] + __popc(m & lt)] = X[row * p + e];
+    }
+  }
+}
+
+struct RowStore {
+  DevBuf<uint32_t> masks;
+  DevBuf<uint16_t> prefix;
+  DevBuf<int64_t> rowptr;
+  DevBuf<unsigned char> vals;
+  int W = 0;
+  int maxnnz = 0;
+  double density = 1.0;
+};
+
+RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_t st, bool fill_if_sparse) {
+  RowStore rs;
+  rs.W = (p + 31) / 32;
+  rs.masks.alloc(static_cast<size_t>(n) * rs.W);
+  rs.prefix.alloc(static_cast<size_t>(n) * rs.W);
+  DevBuf<int> counts(static_cast<size_t>(n));
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), 148 * 16)));
+  if (xt == GMDS_F32)
+    row_mask_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dX), n, p, rs.W, rs.masks.get(),
+                                                   rs.prefix.get(), counts.get());
+  else
+    row_mask_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dX), n, p, rs.W, rs.masks.get(),
+                                                    rs.prefix.get(), counts.get());
+  count_launch();
+  check_launch("row_mask_kernel");
+  std::vector<int> hc(static_cast<size_t>(n));
+  GMDS_CUDA(cudaMemcpyAsync(hc.data(), counts.get(), n * sizeof(int), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> rp(static_cast<size_t>(n) + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    rp[i + 1] = rp[i] + hc[i];
+    rs.maxnnz = std::max(rs.maxnnz, hc[i]);
+  }
+  rs.density = static_cast<double>(rp[n]) / (static_cast<double>(n) * p);
+  if (!fill_if_sparse || rs.density >= 0.5) return rs;
+  rs.rowptr.alloc(rp.size());
+  GMDS_CUDA(cudaMemcpyAsync(rs.rowptr.get(), rp.data(), rp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  rs.vals.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])) * dtype_size(xt));
+  if (xt == GMDS_F32)
+    row_fill_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dX), n, p, rs.W, rs.masks.get(),
+                                                   rs.prefix.get(), rs.rowptr.get(), reinterpret_cast<float*>(rs.vals.get()));
+  else
+    row_fill_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dX), n, p, rs.W, rs.masks.get(),
+                                                    rs.prefix.get(), rs.rowptr.get(),
+                                                    reinterpret_cast<double*>(rs.vals.get()));
+  count_launch();
+  check_launch("row_fill_kernel");
+  return rs;
+}
+
+size_t split_smem(int tile, int p, int W, int maxnnz, size_t sz, int nnu, bool sparse) {
+  size_t s = static_cast<size_t>(8) * kSplitCap * 8 + static_cast<size_t>(nnu) * tile * (tile + 1) * 8;
+  if (sparse)
+    s += ((2 * static_cast<size_t>(tile) * W * 6 + 15) & ~static_cast<size_t>(15)) +
+         2 * static_cast<size_t>(tile) * maxnnz * sz;
+  else
+    s += 2 * static_cast<size_t>(tile) * p * sz;
+  return s;
+}
+
+}  // namespace
+
+void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag) {
+  const std::vector<double> lut = build_lut(static_cast<int>(p), nus, nnu);
+  DevBuf<double> dlut(lut.size());
+  GMDS_CUDA(cudaMemcpyAsync(dlut.get(), lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  GiniTileArgs a{};
+  a.n = n;
+  a.d = static_cast<int>(p);
+  a.lut = dlut.get();
+  a.nnu = nnu;
+  a.packed = packed;
+  a.nb_packed = ceil_div(n, kPT);
+  a.out_stride = packed ? packed_elems(n) : n * n;
+  a.flag = dflag;
+  if (p > 1024) {  // CTA-per-pair block sort
+    a.tile = 1;
+    a.nbt = n;
+    const int64_t units = n * (n - 1) / 2;
+    a.tile_begin = units * shard / nshards;
+    a.tile_end = units * (shard + 1) / nshards;
+    launch_gini(a, dX, xt, dD, ot, st);
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  const size_t sz = dtype_size(xt);
+  RowStore rs = build_rows(dX, xt, n, static_cast<int>(p), st, true);
+  const bool sparse = rs.density < 0.5;
+  auto full_kernel = [&]() {  // the all-keys warp kernel (dense data with large p)
+    a.tile = gini_tile_size(static_cast<int>(p), xt, nnu);
+    a.nbt = ceil_div(n, a.tile);
+    const int64_t units = a.nbt * (a.nbt + 1) / 2;
+    a.tile_begin = units * shard / nshards;
+    a.tile_end = units * (shard + 1) / nshards;
+    launch_gini(a, dX, xt, dD, ot, st);
+  };
+  if (!sparse && p > 512) {
+    full_kernel();
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  int tile = 32;
+  const size_t two_per_sm = 113 * 1024, one_per_sm = 220 * 1024;
+  while (tile > 4 && split_smem(tile, static_cast<int>(p), rs.W, rs.maxnnz, sz, nnu, sparse) > two_per_sm) tile >>= 1;
+  if (split_smem(tile, static_cast<int>(p), rs.W, rs.maxnnz, sz, nnu, sparse) > two_per_sm) {
+    tile = 32;
+    while (tile > 1 && split_smem(tile, static_cast<int>(p), rs.W, rs.maxnnz, sz, nnu, sparse) > one_per_sm) tile >>= 1;
+  }
+  const size_t smem = split_smem(tile, static_cast<int>(p), rs.W, rs.maxnnz, sz, nnu, sparse);
+  if (smem > one_per_sm) {
+    full_kernel();
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  a.tile = tile;
+  a.nbt = ceil_div(n, tile);
+  const int64_t units = a.nbt * (a.nbt + 1) / 2;
+  a.tile_begin = units * shard / nshards;
+  a.tile_end = units * (shard + 1) / nshards;
+  if (a.tile_end <= a.tile_begin) return;
+  SplitArgs sa{};
+  sa.g = a;
+  sa.masks = rs.masks.get();
+  sa.prefix = rs.prefix.get();
+  sa.rowptr = rs.rowptr.get();
+  sa.vals = rs.vals.get();
+  sa.W = rs.W;
+  sa.maxnnz = std::max(1, rs.maxnnz);
+  sa.sparse = sparse ? 1 : 0;
+  const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(tile) * tile;
+  sa.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 24) : 0;
+  DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * sa.ovf_cap)));
+  DevBuf<unsigned long long> ovf_count(1);
+  GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));
+  sa.ovf_pairs = ovf.get();
+  sa.ovf_count = ovf_count.get();
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30));
+  if (p <= 256)
+    launch_gini_split<8>(sa, dX, xt, dD, ot, smem, blocks, st);
+  else
+    launch_gini_split<16>(sa, dX, xt, dD, ot, smem, blocks, st);
+  count_launch();
+  check_launch("gini_split_kernel");
+  unsigned long long novf = 0;
+  GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  if (novf == 0) return;
+  if (static_cast<int64_t>(novf) > sa.ovf_cap) {  // list too long: redo these tiles with the all-keys kernel
+    full_kernel();
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  // p > 512 here, so the full sort needs 1024 keys (K = 32)
+  launch_gini_list<32>(a, dX, xt, ovf.get(), static_cast<int64_t>(novf), dD, ot, st);
+  count_launch();
+  check_launch("gini_list_kernel");
+  GMDS_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace gmds

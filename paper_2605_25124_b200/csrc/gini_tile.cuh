@@ -5,6 +5,8 @@
 
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "warp_rank.cuh"
@@ -103,12 +105,19 @@ __global__ void __launch_bounds__(256) gini_tile_kernel(GiniTileArgs a, const T*
     __syncthreads();
     const T* pj = diag ? rowsI : rowsJ;
 
-    for (int k = warp; k < tile * tile; k += nwarps) {
-      const int r = k / tile, c = k % tile;
+    // Every warp runs the same trip count with no data-dependent branch
+    // around the shuffles (a divergent-looking region makes ptxas wrap each
+    // shuffle in WARPSYNC/collective fallback code); invalid pairs (i >= j,
+    // j >= n) are computed on the zero row pair and simply not stored.
+    const int per_warp = (tile * tile + nwarps - 1) / nwarps;
+    for (int it = 0; it < per_warp; ++it) {
+      const int k = warp + it * nwarps;
+      const int kk = (k < tile * tile) ? k : 0;
+      const int r = kk / tile, c = kk % tile;
       const int64_t i = i0 + r, j = j0 + c;
-      if (!(j < a.n && i < j)) continue;  // warp-uniform
+      const bool valid = (k < tile * tile) && (j < a.n) && (i < j);
       const T* xi = rowsI + static_cast<size_t>(r) * d;
-      const T* xj = pj + static_cast<size_t>(c) * d;
+      const T* xj = valid ? pj + static_cast<size_t>(c) * d : xi;
       double key[K];
 #pragma unroll
       for (int q = 0; q < K; ++q) {
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(256) gini_tile_kernel(GiniTileArgs a, const T*
           if (lane * K + q < d) acc = fma(key[q], __ldg(L + h[q]), acc);
         acc = warp_sum(acc);
         const double val = clamp_nonneg(half_p * acc);
-        if (lane == 0) {
+        if (lane == 0 && valid) {
           otile[(static_cast<size_t>(v) * tile + r) * tstride + c] = val;
           if (isinf(val)) atomicOr(a.flag, 1);
         }
@@ -165,6 +174,55 @@ __global__ void __launch_bounds__(256) gini_tile_kernel(GiniTileArgs a, const T*
 }
 
 
+// Overflow pairs of the split kernel (more than 512 nonzeros): warp per
+// listed pair, full N = 32K sort straight from the row-major X in HBM/L2.
+template <int K, typename T, typename TO>
+__global__ void __launch_bounds__(256) gini_list_kernel(GiniTileArgs a, const T* __restrict__ X,
+                                                        const int64_t* __restrict__ pairs, int64_t npairs,
+                                                        TO* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int d = a.d;
+  const double half_p = 0.5 * static_cast<double>(d);
+  const int64_t w0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t q = w0; q < npairs; q += nw) {
+    const int64_t i = pairs[2 * q], j = pairs[2 * q + 1];
+    double key[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int e = r * 32 + lane;
+      key[r] = (e < d) ? static_cast<double>(X[i * d + e]) - static_cast<double>(X[j * d + e]) : INFINITY;
+    }
+    Payload<false>::Arr<K> nop;
+    warp_bitonic_sort<K, false>(key, nop, lane);
+    int h[K];
+    warp_tie_groups<K>(key, h, lane);
+    for (int v = 0; v < a.nnu; ++v) {
+      const double* L = a.lut + static_cast<size_t>(v) * 2 * d;
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (lane * K + r < d) acc = fma(key[r], __ldg(L + h[r]), acc);
+      acc = warp_sum(acc);
+      const double val = clamp_nonneg(half_p * acc);
+      if (lane == 0) {
+        TO* o = out + static_cast<size_t>(v) * a.out_stride;
+        if (a.packed) {
+          o[packed_offset(i, j, a.nb_packed)] = static_cast<TO>(val);
+        } else {
+          o[i * a.n + j] = static_cast<TO>(val);
+          o[j * a.n + i] = static_cast<TO>(val);
+        }
+        if (isinf(val)) atomicOr(a.flag, 1);
+      }
+    }
+  }
+}
+
+template <int K>
+void launch_gini_list(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64_t* pairs, int64_t npairs, void* dout,
+                      gmds_dtype ot, cudaStream_t st);
+
 template <int K>
 void launch_midrank_warp(const double* dv, const void* dX, gmds_dtype xt, const int64_t* dpairs, int64_t nseg, int d,
                          double* dranks, dim3 g, int threads, cudaStream_t st);
@@ -189,6 +247,21 @@ void launch_gini_tile(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout,
     GMDS_CUDA(cudaFuncSetAttribute(gini_tile_kernel<KK, T, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                    static_cast<int>(smem)));                                                      \
     gini_tile_kernel<KK, T, TO><<<blocks, 256, smem, st>>>(a, static_cast<const T*>(dX), static_cast<TO*>(dout)); \
+  }                                                                                                               \
+  template <typename T, typename TO>                                                                              \
+  static void gini_list_##KK(GiniTileArgs a, const void* dX, const int64_t* pairs, int64_t np, void* dout,        \
+                             cudaStream_t st) {                                                                   \
+    const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((np + 7) / 8, 148 * 8))); \
+    gini_list_kernel<KK, T, TO><<<blocks, 256, 0, st>>>(a, static_cast<const T*>(dX), pairs, np,                 \
+                                                       static_cast<TO*>(dout));                                  \
+  }                                                                                                               \
+  template <>                                                                                                     \
+  void launch_gini_list<KK>(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64_t* pairs, int64_t np,     \
+                            void* dout, gmds_dtype ot, cudaStream_t st) {                                         \
+    if (xt == GMDS_F32 && ot == GMDS_F32) gini_list_##KK<float, float>(a, dX, pairs, np, dout, st);               \
+    else if (xt == GMDS_F32) gini_list_##KK<float, double>(a, dX, pairs, np, dout, st);                           \
+    else if (ot == GMDS_F32) gini_list_##KK<double, float>(a, dX, pairs, np, dout, st);                           \
+    else gini_list_##KK<double, double>(a, dX, pairs, np, dout, st);                                              \
   }                                                                                                               \
   template <>                                                                                                     \
   void launch_gini_tile<KK>(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, size_t smem, \

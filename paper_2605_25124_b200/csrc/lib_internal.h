@@ -11,6 +11,7 @@ namespace gmds {
 
 struct Stream {
   cudaStream_t s = nullptr;
+  bool owned = true;
   Stream();
   ~Stream();
   Stream(const Stream&) = delete;

@@ -32,14 +32,16 @@ __global__ void stress_rows_kernel(PassArgs a, int q, int grad) {
           const M dy = static_cast<M>(a.Y[c][i * q + k]) - static_cast<M>(a.Y[c][j * q + k]);
           d2 = fma(dy, dy, d2);
         }
-        const M dist = sqrt(d2);
+        M dist, inv;
+        dist_inv(d2, dist, inv);
+        const M invD = (a.kind == kSammon) ? M(1) / Dv : M(0);
         PairTerms<M> t;
         switch (a.kind) {
-          case kKruskal: t = pair_terms<kKruskal, M>(Dv, dist, wv, delta); break;
-          case kHuber: t = pair_terms<kHuber, M>(Dv, dist, wv, delta); break;
-          case kSammon: t = pair_terms<kSammon, M>(Dv, dist, wv, delta); break;
-          case kSmacof: t = pair_terms<kSmacof, M>(Dv, dist, wv, delta); break;
-          default: t = pair_terms<kGuttman, M>(Dv, dist, wv, delta); break;
+          case kKruskal: t = pair_terms<kKruskal, M>(Dv, invD, dist, inv, wv, delta); break;
+          case kHuber: t = pair_terms<kHuber, M>(Dv, invD, dist, inv, wv, delta); break;
+          case kSammon: t = pair_terms<kSammon, M>(Dv, invD, dist, inv, wv, delta); break;
+          case kSmacof: t = pair_terms<kSmacof, M>(Dv, invD, dist, inv, wv, delta); break;
+          default: t = pair_terms<kGuttman, M>(Dv, invD, dist, inv, wv, delta); break;
         }
         if (j > i) loss[c] += static_cast<double>(t.term);  // each pair once
         if (grad)

@@ -51,40 +51,57 @@ __device__ __forceinline__ int64_t blk_index(int64_t I, int64_t J, int64_t nb) {
 template <typename M>
 struct PairTerms {
   M term;  // loss contribution
-  M c;     // gradient weight
+  M c;     // gradient weight c_ij (already divided by dist; 0 when dist == 0)
 };
 
+// dist and 1/dist of a squared distance.  fp64 path: IEEE sqrt and division
+// (parity mode).  fp32 path: one MUFU.RSQ (rsqrtf, <= 2 ulp) gives both, so a
+// pair costs one XU op per configuration and no division.
+__device__ __forceinline__ void dist_inv(double d2, double& dist, double& inv) {
+  dist = sqrt(d2);
+  inv = (dist > 0.0) ? 1.0 / dist : 0.0;
+}
+__device__ __forceinline__ void dist_inv(float d2, float& dist, float& inv) {
+  const float r = rsqrtf(d2);
+  inv = (d2 > 0.f) ? r : 0.f;
+  dist = d2 * inv;
+}
+
+// invD = 1/D (Sammon only; computed once per pair, shared by all candidates).
 template <int KIND, typename M>
-__device__ __forceinline__ PairTerms<M> pair_terms(M Dv, M dist, M w, M delta) {
+__device__ __forceinline__ PairTerms<M> pair_terms(M Dv, M invD, M dist, M inv, M w, M delta) {
   const M e = Dv - dist;
   PairTerms<M> r;
   switch (KIND) {
     case kKruskal:
       r.term = e * e;
-      r.c = -e;
+      r.c = -e * inv;
       break;
     case kHuber: {
       const M ae = fabs(e);
       r.term = (ae <= delta) ? M(0.5) * e * e : delta * (ae - M(0.5) * delta);
-      r.c = -fmin(fmax(e, -delta), delta);
+      r.c = -fmin(fmax(e, -delta), delta) * inv;
       break;
     }
     case kSammon:
-      r.term = e * e / Dv;
-      r.c = -e / Dv;
+      r.term = e * e * invD;
+      r.c = -e * invD * inv;
       break;
     case kSmacof:
       r.term = w * e * e;
-      r.c = M(-2) * w * e;
+      r.c = M(-2) * w * e * inv;
       break;
     default:  // kGuttman: loss is the smacof loss at the same Z
       r.term = w * e * e;
-      r.c = w * Dv;
+      r.c = w * Dv * inv;
       break;
   }
-  r.c = (dist > M(0)) ? r.c / dist : M(0);
   return r;
 }
+
+// Shared-memory slot of block row r (0..127): rows are stored [y][tj] so the
+// 16 tj-threads of a half-warp read 16 different banks (r = tj * 8 + y).
+__device__ __forceinline__ int yslot(int r) { return (r % kMT) * kTG + r / kMT; }
 
 }  // namespace stress_detail
 using namespace stress_detail;
@@ -95,10 +112,10 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
   using M = typename MathOf<TD>::type;
   constexpr int NCM = GRAD ? 1 : kMaxCand;
   __shared__ M sYi[NCM][kPT][Q];
-  __shared__ M sYj[NCM][kPT][Q];
+  __shared__ M sYj[NCM][kPT][Q];  // [yslot(r)]
   __shared__ double sRed[GRAD ? kTG * kPT : 1];
   __shared__ double sLoss[kThreads / 32][kMaxCand];
-  // row sums of the chunk (fixed-order: x rows reduced across the half-warp, then += per block)
+  // row sums of the chunk (fixed order: x rows reduced across the half-warp, then += per block)
   __shared__ double sRowTot[GRAD ? kPT * Q : 1];
 
   const int tid = threadIdx.x;
@@ -112,17 +129,15 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
   const TD* __restrict__ W = static_cast<const TD*>(a.W);
   const M delta = static_cast<M>(a.huber_delta);
 
-  // stage Y rows of block-row I (every candidate)
   for (int e = tid; e < nc * kPT * Q; e += kThreads) {
     const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
     const int64_t i = I * kPT + r;
     sYi[c][r][k] = (i < a.n) ? static_cast<M>(a.Y[c][i * Q + k]) : M(0);
   }
-
-  double lossacc[NCM];
   if constexpr (GRAD) {
     for (int e = tid; e < kPT * Q; e += kThreads) sRowTot[e] = 0.0;
   }
+  double lossacc[NCM];
 #pragma unroll
   for (int c = 0; c < NCM; ++c) lossacc[c] = 0.0;
 
@@ -131,37 +146,40 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
     for (int e = tid; e < nc * kPT * Q; e += kThreads) {
       const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
       const int64_t j = J * kPT + r;
-      sYj[c][r][k] = (j < a.n) ? static_cast<M>(a.Y[c][j * Q + k]) : M(0);
+      sYj[c][yslot(r)][k] = (j < a.n) ? static_cast<M>(a.Y[c][j * Q + k]) : M(0);
     }
     __syncthreads();
     const int64_t blk = blk_index(I, J, a.nb);
     const TD* Db = D + blk * (kPT * kPT);
     const TD* Wb = W ? W + blk * (kPT * kPT) : nullptr;
-    double colacc[GRAD ? kMT : 1][Q];
-    if (GRAD) {
+    M colacc[GRAD ? kMT : 1][Q];
+    if constexpr (GRAD) {
 #pragma unroll
-      for (int x = 0; x < (GRAD ? kMT : 1); ++x)
+      for (int y = 0; y < kMT; ++y)
 #pragma unroll
-        for (int k = 0; k < Q; ++k) colacc[x][k] = 0.0;
+        for (int k = 0; k < Q; ++k) colacc[y][k] = M(0);
     }
     const bool diag = (I == J);
 #pragma unroll 1
     for (int x = 0; x < kMT; ++x) {
       const int ri = ti * kMT + x;
-      double rowacc[Q];
+      M rowacc[Q];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) rowacc[k] = 0.0;
+      for (int k = 0; k < Q; ++k) rowacc[k] = M(0);
+      M lossrow[NCM];
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) lossrow[c] = M(0);
       TD dv[kMT];
       const TD* drow = Db + ri * kPT + tj * kMT;
       if constexpr (sizeof(TD) == 4) {
-        const float4 v0 = *reinterpret_cast<const float4*>(drow);
-        const float4 v1 = *reinterpret_cast<const float4*>(drow + 4);
+        const float4 v0 = __ldcs(reinterpret_cast<const float4*>(drow));
+        const float4 v1 = __ldcs(reinterpret_cast<const float4*>(drow + 4));
         dv[0] = v0.x, dv[1] = v0.y, dv[2] = v0.z, dv[3] = v0.w;
         dv[4] = v1.x, dv[5] = v1.y, dv[6] = v1.z, dv[7] = v1.w;
       } else {
 #pragma unroll
         for (int y = 0; y < kMT; y += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(drow + y);
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(drow + y));
           dv[y] = v.x, dv[y + 1] = v.y;
         }
       }
@@ -173,7 +191,8 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
         const int rj = tj * kMT + y;
         const int64_t j = J * kPT + rj;
         const bool valid = (j < a.n) && (!diag || ri < rj);
-        if (!valid) continue;
+        const M Dv = static_cast<M>(dv[y]);
+        const M invD = (KIND == kSammon && valid) ? M(1) / Dv : M(0);
 #pragma unroll
         for (int c = 0; c < NCM; ++c) {
           if (c >= nc) break;
@@ -181,27 +200,31 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
           M d2 = M(0);
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
-            dy[k] = sYi[c][ri][k] - sYj[c][rj][k];
+            dy[k] = sYi[c][ri][k] - sYj[c][y * kTG + tj][k];
             d2 = fma(dy[k], dy[k], d2);
           }
-          const M dist = sqrt(d2);
-          const PairTerms<M> t = pair_terms<KIND, M>(static_cast<M>(dv[y]), dist, static_cast<M>(wv[y]), delta);
-          lossacc[c] += static_cast<double>(t.term);
+          M dist, inv;
+          dist_inv(d2, dist, inv);
+          const PairTerms<M> t = pair_terms<KIND, M>(Dv, invD, dist, inv, static_cast<M>(wv[y]), delta);
+          lossrow[c] += valid ? t.term : M(0);
           if constexpr (GRAD) {
+            const M cc = valid ? t.c : M(0);
 #pragma unroll
             for (int k = 0; k < Q; ++k) {
-              const double g = static_cast<double>(t.c * dy[k]);
+              const M g = cc * dy[k];
               rowacc[k] += g;
               colacc[y][k] -= g;
             }
           }
         }
       }
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
       if constexpr (GRAD) {
         // the 16 tj-threads of row ri share a half-warp: xor-tree in a fixed order
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
-          double v = rowacc[k];
+          double v = static_cast<double>(rowacc[k]);
 #pragma unroll
           for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
           if (tj == 0) sRowTot[ri * Q + k] += v;
@@ -214,7 +237,7 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
       for (int k = 0; k < Q; ++k) {
         if (k > 0) __syncthreads();
 #pragma unroll
-        for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = colacc[y][k];
+        for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = static_cast<double>(colacc[y][k]);
         __syncthreads();
         if (tid < kPT) {
           double s = 0.0;
@@ -243,7 +266,6 @@ __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
     a.losspart[chunk * kMaxCand + tid] = s;
   }
 }
-
 
 template <typename TD, bool GRAD>
 void launch_pass_td(const PassArgs& a, int Q, cudaStream_t st);

@@ -161,3 +161,51 @@ def test_device_entry_sharded_matches_full():
     assert torch.equal(full, sh)
     ref = O.pairwise_matrix(X.astype(np.float64), 3.0)
     assert maxnorm_err(full[1].cpu().numpy(), ref) <= 1e-12
+
+
+def image_like(n, p, seed, zero_frac=0.8):
+    g = np.random.default_rng(seed)
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < zero_frac] = 0.0
+    return X.astype(np.float32)
+
+
+@pytest.mark.parametrize("p", [200, 300, 784, 1000])
+def test_sparse_split_path_vs_oracle(p):
+    # config-3 shaped data: bitmask-sparse panels, zero compaction, sign-split sorts
+    X = image_like(90, p, p)
+    X[11] = X[12]  # duplicate row -> D == 0
+    nus = [1.1, 2.0, 3.0, 5.0, 8.0]
+    Ds = G.pairwise_gini(X, nus)
+    Xd = X.astype(np.float64)
+    for k, nu in enumerate(nus):
+        assert maxnorm_err(Ds[k], O.pairwise_matrix(Xd, nu)) <= TOL
+    assert Ds[0][11, 12] == 0.0
+
+
+def test_overflow_list_path():
+    # p = 784 with a few dense rows: dense-dense pairs have > 512 nonzeros and
+    # take the overflow list; everything else the split kernel
+    X = image_like(70, 784, 5)
+    X[:6] = np.random.default_rng(6).lognormal(0.0, 1.0, (6, 784)).astype(np.float32)
+    D = G.pairwise_gini(X, [2.0, 4.0])
+    Xd = X.astype(np.float64)
+    assert maxnorm_err(D[0], O.pairwise_matrix(Xd, 2.0)) <= TOL
+    assert maxnorm_err(D[1], O.pairwise_matrix(Xd, 4.0)) <= TOL
+
+
+@pytest.mark.parametrize("p", [300, 600])
+def test_dense_mid_p(p):
+    X = np.random.default_rng(p).lognormal(0.0, 1.0, (50, p)).astype(np.float32)
+    assert maxnorm_err(G.pairwise_matrix(X, 2.5), O.pairwise_matrix(X.astype(np.float64), 2.5)) <= TOL
+
+
+def test_all_zero_rows_and_constant_shift():
+    X = np.zeros((20, 784), dtype=np.float32)
+    X[5, 3] = 1.0
+    X[7] = 0.25  # constant row: z = const - 0 on most features
+    D = G.pairwise_matrix(X, 2.0)
+    assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= TOL
+    assert D[0, 1] == 0.0
