@@ -39,7 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N, P, Q, NU = 20000, 784, 2, 2.0
-STRESS_ITERS = 10
+STRESS_ITERS = 50
 SEED = 2605
 
 

@@ -3,9 +3,16 @@
 #pragma once
 
 #include <memory>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
+
+namespace gmds {
+struct Engine;
+}
 
 struct gmds_dmat {
   int64_t n = 0;
@@ -20,5 +27,10 @@ struct gmds_dmat {
   double min_off = 0.0;  // min_{i<j} D_ij
   double max_val = 0.0;  // max over the full matrix (0 on the diagonal)
   bool stats = false;
+  // stress-pass workspaces cached per embedding dimension (reused across
+  // calls; a second concurrent user of the same handle gets a fresh one)
+  mutable std::mutex mu;
+  mutable std::vector<std::pair<int, std::shared_ptr<gmds::Engine>>> engines;
+  mutable std::vector<bool> busy;
   const void* ptr() const { return shared ? static_cast<const void*>(shared->get() + offset) : buf.get(); }
 };

@@ -161,6 +161,40 @@ double Engine::loss_of(int kind, double raw) const {
   }
 }
 
+EngineLease acquire_engine(const gmds_dmat* D, int q, cudaStream_t st) {
+  EngineLease L;
+  L.D = D;
+  {
+    std::lock_guard<std::mutex> g(D->mu);
+    for (size_t k = 0; k < D->engines.size(); ++k)
+      if (D->engines[k].first == q && !D->busy[k]) {
+        D->busy[k] = true;
+        L.e = D->engines[k].second;
+        L.slot = static_cast<int>(k);
+        break;
+      }
+  }
+  if (!L.e) {
+    auto e = std::make_shared<Engine>(D, q, st);
+    std::lock_guard<std::mutex> g(D->mu);
+    D->engines.emplace_back(q, e);
+    D->busy.push_back(true);
+    L.e = e;
+    L.slot = static_cast<int>(D->engines.size()) - 1;
+  }
+  L.e->st = st;
+  L.e->W = nullptr;
+  L.e->passes = 0;
+  return L;
+}
+
+EngineLease::~EngineLease() {
+  if (D && slot >= 0) {
+    std::lock_guard<std::mutex> g(D->mu);
+    D->busy[static_cast<size_t>(slot)] = false;
+  }
+}
+
 // ---------------------------------------------------------------------------
 namespace {
 
@@ -270,7 +304,7 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
       Steps s{};
       // first batch: step and step/2 (the common accept pattern after a doubling);
       // further batches: four halvings per pass
-      s.n = std::min(halvings == 0 ? 2 : kMaxCand, 60 - halvings);
+      s.n = std::min((halvings == 0 || E.D->storage == GMDS_F32) ? 2 : kMaxCand, 60 - halvings);
       double sv = step;
       for (int c = 0; c < s.n; ++c) {
         s.v[c] = sv;
@@ -426,7 +460,8 @@ void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigval
   }
   if (stress) {
     if (D->sum_sq > 0.0) {
-      Engine E(D, q, st);
+      EngineLease L = acquire_engine(D, q, st);
+      Engine& E = *L;
       E.upload(coords, E.Y.get());
       const double* y = E.Y.get();
       *stress = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
@@ -530,7 +565,8 @@ void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, 
       minimize_stress_dev(D, q, trial, nullptr, &rr, st, init.data());
       // kruskal_stress(e.coords, D) (embed.cpp:508)
       if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
-      Engine E(D, q, st);
+      EngineLease L = acquire_engine(D, q, st);
+      Engine& E = *L;
       E.upload(coords.data(), E.Y.get());
       const double* y = E.Y.get();
       const double ks = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
@@ -553,7 +589,8 @@ void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, 
     return;
   }
   const Resolved rp = resolve(D, cfg.kind, cfg.huber_delta, cfg.smacof_weights, "minimize_stress");
-  Engine E(D, q, st);
+  EngineLease L = acquire_engine(D, q, st);
+  Engine& E = *L;
   DevBuf<unsigned char> W;
   if (rp.weighted) {
     W = upload_weights(D, cfg.smacof_weights, st);
@@ -720,7 +757,8 @@ gmds_status gmds_kruskal_stress(const gmds_dmat* D, const double* coords, int32_
     check_coords(D, coords, q, "kruskal_stress");
     if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
     Stream st;
-    Engine E(D, q, st.s);
+    EngineLease L = acquire_engine(D, q, st.s);
+    Engine& E = *L;
     E.upload(coords, E.Y.get());
     const double* y = E.Y.get();
     *out = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
@@ -733,7 +771,8 @@ gmds_status gmds_stress_loss(int32_t kind, const gmds_dmat* D, const double* coo
     check_coords(D, coords, q, "stress_loss");
     const Resolved rp = resolve(D, kind, huber_delta, weights, "stress_loss");
     Stream st;
-    Engine E(D, q, st.s);
+    EngineLease L = acquire_engine(D, q, st.s);
+    Engine& E = *L;
     DevBuf<unsigned char> W;
     if (rp.weighted) {
       W = upload_weights(D, weights, st.s);
@@ -751,7 +790,8 @@ gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double*
     check_coords(D, coords, q, "stress_gradient");
     const Resolved rp = resolve(D, kind, huber_delta, weights, "stress_gradient");
     Stream st;
-    Engine E(D, q, st.s);
+    EngineLease L = acquire_engine(D, q, st.s);
+    Engine& E = *L;
     DevBuf<unsigned char> W;
     if (rp.weighted) {
       W = upload_weights(D, weights, st.s);

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -35,6 +36,24 @@ struct Engine {
   double scale_grad(double scale);
   double loss_of(int kind, double raw) const;
 };
+
+// Engine for (D, q) on stream st: a cached workspace when free, else a fresh one.
+struct EngineLease {
+  std::shared_ptr<Engine> e;
+  const gmds_dmat* D = nullptr;
+  int slot = -1;
+  Engine* operator->() const { return e.get(); }
+  Engine& operator*() const { return *e; }
+  EngineLease() = default;
+  EngineLease(const EngineLease&) = delete;
+  EngineLease(EngineLease&& o) noexcept : e(std::move(o.e)), D(o.D), slot(o.slot) {
+    o.D = nullptr;
+    o.slot = -1;
+  }
+  EngineLease& operator=(const EngineLease&) = delete;
+  ~EngineLease();
+};
+EngineLease acquire_engine(const gmds_dmat* D, int q, cudaStream_t st);
 
 void dmat_finish(gmds_dmat* d, cudaStream_t st);
 void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigvals, int* clamped_count,

@@ -1,6 +1,6 @@
-// Instantiation: stress_pass_kernel<Q, float, true, KIND> for Q in 1..4, every kind.
-#include "stress_pass.cuh"
+// Instantiation: fp32-storage stress pass (TMA-streamed, stress_tma.cuh), GRAD=true.
+#include "stress_tma.cuh"
 
 namespace gmds {
-GMDS_INSTANTIATE_PASS(float, true)
+GMDS_INSTANTIATE_TMA(true)
 }  // namespace gmds

@@ -1,6 +1,6 @@
-// Instantiation: stress_pass_kernel<Q, float, false, KIND> for Q in 1..4, every kind.
-#include "stress_pass.cuh"
+// Instantiation: fp32-storage stress pass (TMA-streamed, stress_tma.cuh), GRAD=false.
+#include "stress_tma.cuh"
 
 namespace gmds {
-GMDS_INSTANTIATE_PASS(float, false)
+GMDS_INSTANTIATE_TMA(false)
 }  // namespace gmds

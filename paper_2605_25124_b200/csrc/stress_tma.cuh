@@ -1,0 +1,314 @@
+// K3 (fp32 storage): the stress pass with D streamed by TMA bulk copies.
+//
+// Same contract as stress_pass_kernel (stress_pass.cuh): one pass over the
+// packed upper triangle, loss partials at up to kMaxCand configurations, and
+// (GRAD) per-row sums of c_ij (y_i - y_j), reduced in a fixed order.
+//
+// Data movement: every 128x128 block of the packed fp32 image is two
+// contiguous 32 KB half-blocks (rows 0-63, 64-127).  One elected thread
+// streams them with cp.async.bulk (1-D TMA) into a 2-stage shared-memory
+// ring guarded by mbarriers (two CTAs per SM: up to 128 KB in flight) while the
+// 256 threads consume the previous stage from shared memory.
+//
+// Arithmetic diet per pair (kruskal, q = 2): y_j held in registers, 2 FADD,
+// FMUL+FFMA, FMNMX, MUFU.RSQ, FMUL, FADD, FFMA (loss), FMUL, 4 FFMA
+// (row/column sums).  d2 is clamped to FLT_MIN before rsqrtf so coincident
+// points (d2 = 0, hence dy = 0) add exactly 0 without a select; interior
+// blocks skip all validity masks.
+#pragma once
+
+#include <float.h>
+
+#include <type_traits>
+
+#include "stress_pass.cuh"
+
+namespace gmds {
+
+namespace tma_detail {
+
+constexpr int kStages = 2;
+constexpr int kHalfRows = 64;
+constexpr int kHalfFloats = kHalfRows * kPT;  // 8192 floats = 32 KB
+constexpr int kMR = 4;                        // micro-tile rows per half (ti*4 + x)
+constexpr int kTmaCand = 2;                   // trial points per loss pass (y_j kept in registers)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int KIND>
+__device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, float inv, float w, float delta,
+                                           float& term, float& c) {
+  const float e = Dv - dist;
+  if constexpr (KIND == kKruskal) {
+    term = e * e;
+    c = -e * inv;
+  } else if constexpr (KIND == kHuber) {
+    const float ae = fabsf(e);
+    term = (ae <= delta) ? 0.5f * e * e : delta * (ae - 0.5f * delta);
+    c = -fminf(fmaxf(e, -delta), delta) * inv;
+  } else if constexpr (KIND == kSammon) {
+    term = e * e * invD;
+    c = -e * invD * inv;
+  } else if constexpr (KIND == kSmacof) {
+    term = w * e * e;
+    c = -2.f * w * e * inv;
+  } else {  // kGuttman
+    term = w * e * e;
+    c = w * Dv * inv;
+  }
+}
+
+}  // namespace tma_detail
+
+template <int Q, bool GRAD, int KIND>
+__global__ void __launch_bounds__(kThreads) stress_tma_kernel(PassArgs a) {
+  using namespace tma_detail;
+  constexpr int NCM = GRAD ? 1 : kTmaCand;
+  extern __shared__ __align__(128) unsigned char dyn[];
+  float* ring = reinterpret_cast<float*>(dyn);  // [kStages][kHalfFloats]
+  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ float sYi[NCM][kPT][Q];
+  __shared__ float sYj[NCM][kPT][Q];  // [yslot(r)]
+  __shared__ double sRed[GRAD ? kTG * kPT : 1];
+  __shared__ double sLoss[kThreads / 32][kMaxCand];
+  __shared__ double sRowTot[GRAD ? kPT * Q : 1];
+
+  const int tid = threadIdx.x;
+  const int ti = tid / kTG, tj = tid % kTG;
+  const int64_t chunk = blockIdx.x;
+  const int64_t I = a.chunk_I[chunk];
+  const int64_t J0 = a.chunk_J0[chunk];
+  const int64_t J1 = min(J0 + a.chunk_len, a.nb);
+  const int nblocks = static_cast<int>(J1 - J0);
+  const int nhalves = 2 * nblocks;
+  const int nc = GRAD ? 1 : a.ncand;
+  const float* __restrict__ D = static_cast<const float*>(a.D);
+  const float* __restrict__ W = static_cast<const float*>(a.W);
+  const float delta = static_cast<float>(a.huber_delta);
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int h) {
+    const int64_t J = J0 + h / 2;
+    const float* src = D + blk_index(I, J, a.nb) * (kPT * kPT) + (h & 1) * kHalfFloats;
+    uint64_t* bar = &bars[h % kStages];
+    mbar_expect_tx(bar, kHalfFloats * 4);
+    bulk_g2s(ring + (h % kStages) * kHalfFloats, src, kHalfFloats * 4, bar);
+  };
+  if (tid == 0)
+    for (int h = 0; h < min(kStages, nhalves); ++h) issue(h);
+
+  for (int e = tid; e < nc * kPT * Q; e += kThreads) {
+    const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
+    const int64_t i = I * kPT + r;
+    sYi[c][r][k] = (i < a.n) ? static_cast<float>(a.Y[c][i * Q + k]) : 0.f;
+  }
+  if constexpr (GRAD) {
+    for (int e = tid; e < kPT * Q; e += kThreads) sRowTot[e] = 0.0;
+  }
+  double lossacc[NCM];
+#pragma unroll
+  for (int c = 0; c < NCM; ++c) lossacc[c] = 0.0;
+  float colacc[GRAD ? kMT : 1][Q];
+  float yj[NCM][kMT][Q];  // this thread's 8 columns, loaded once per block
+
+  for (int h = 0; h < nhalves; ++h) {
+    const int64_t J = J0 + h / 2;
+    const int half = h & 1;
+    if (half == 0) {
+      __syncthreads();  // sYj / sRed of the previous block are consumed
+      for (int e = tid; e < nc * kPT * Q; e += kThreads) {
+        const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
+        const int64_t j = J * kPT + r;
+        sYj[c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+      }
+      if constexpr (GRAD) {
+#pragma unroll
+        for (int y = 0; y < kMT; ++y)
+#pragma unroll
+          for (int k = 0; k < Q; ++k) colacc[y][k] = 0.f;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < NCM; ++c)
+#pragma unroll
+        for (int y = 0; y < kMT; ++y)
+#pragma unroll
+          for (int k = 0; k < Q; ++k) yj[c][y][k] = (c < nc) ? sYj[c][y * kTG + tj][k] : 0.f;
+    }
+    mbar_wait(&bars[h % kStages], static_cast<uint32_t>((h / kStages) & 1));
+    const float* Ds = ring + (h % kStages) * kHalfFloats;
+    const int64_t blk = blk_index(I, J, a.nb);
+    const float* Wb = W ? W + blk * (kPT * kPT) + half * kHalfFloats : nullptr;
+    const bool edge = (I == J) || (J * kPT + kPT > a.n);
+#pragma unroll 1
+    for (int x = 0; x < kMR; ++x) {
+      const int rloc = ti * kMR + x;           // row within the half
+      const int ri = half * kHalfRows + rloc;  // row within the block
+      const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT);
+      const float4 v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT + 4);
+      const float dv[kMT] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      float wv[kMT];
+#pragma unroll
+      for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tj * kMT + y] : 1.f;
+      float rowacc[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) rowacc[k] = 0.f;
+      float lossrow[NCM];
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) lossrow[c] = 0.f;
+      float yi[NCM][Q];
+#pragma unroll
+      for (int c = 0; c < NCM; ++c)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) yi[c][k] = (c < nc) ? sYi[c][ri][k] : 0.f;
+      // interior blocks: no masks at all; edge blocks (diagonal / last column block) mask per pair
+      auto pairs = [&](auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
+#pragma unroll
+        for (int y = 0; y < kMT; ++y) {
+          const int rj = tj * kMT + y;
+          bool keep = true;
+          if constexpr (EDGE) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
+          const float Dv = dv[y];
+          const float invD = (KIND == kSammon) ? 1.f / fmaxf(Dv, FLT_MIN) : 0.f;
+#pragma unroll
+          for (int c = 0; c < NCM; ++c) {
+            if (c >= nc) break;
+            float dy[Q];
+            float d2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              dy[k] = yi[c][k] - yj[c][y][k];
+              d2 = fmaf(dy[k], dy[k], d2);
+            }
+            const float inv = rsqrtf(fmaxf(d2, FLT_MIN));
+            const float dist = d2 * inv;
+            float term, cc;
+            kind_terms<KIND>(Dv, invD, dist, inv, wv[y], delta, term, cc);
+            if constexpr (EDGE) {
+              term = keep ? term : 0.f;
+              cc = keep ? cc : 0.f;
+            }
+            lossrow[c] += term;
+            if constexpr (GRAD) {
+#pragma unroll
+              for (int k = 0; k < Q; ++k) {
+                rowacc[k] = fmaf(cc, dy[k], rowacc[k]);
+                colacc[y][k] = fmaf(-cc, dy[k], colacc[y][k]);
+              }
+            }
+          }
+        }
+      };
+      if (edge)
+        pairs(std::true_type{});
+      else
+        pairs(std::false_type{});
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
+      if constexpr (GRAD) {
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          double v = static_cast<double>(rowacc[k]);
+#pragma unroll
+          for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+          if (tj == 0) sRowTot[ri * Q + k] += v;
+        }
+      }
+    }
+    if constexpr (GRAD) {
+      if (half == 1) {  // column partials of block J (rows ti*4.. of both halves)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          __syncthreads();
+#pragma unroll
+          for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = static_cast<double>(colacc[y][k]);
+          __syncthreads();
+          if (tid < kPT) {
+            double s = 0.0;
+            for (int t = 0; t < kTG; ++t) s += sRed[t * kPT + tid];
+            a.colpart[(blk * kPT + tid) * Q + k] = s;
+          }
+        }
+      }
+    }
+    __syncthreads();  // stage h % kStages is free
+    if (tid == 0 && h + kStages < nhalves) issue(h + kStages);
+  }
+  if constexpr (GRAD) {
+    __syncthreads();
+    for (int e = tid; e < kPT * Q; e += kThreads) a.rowpart[chunk * (kPT * Q) + e] = sRowTot[e];
+  }
+#pragma unroll
+  for (int c = 0; c < NCM; ++c) {
+    double v = lossacc[c];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if ((tid & 31) == 0) sLoss[tid >> 5][c] = v;
+  }
+  __syncthreads();
+  if (tid < nc) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += sLoss[w][tid];
+    a.losspart[chunk * kMaxCand + tid] = s;
+  }
+}
+
+constexpr size_t kTmaSmem = static_cast<size_t>(tma_detail::kStages) * tma_detail::kHalfFloats * 4;
+
+#define GMDS_TMA_KIND(QQ, KK)                                                                              \
+  case KK:                                                                                                 \
+    GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, GRAD, KK>,                                        \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem))); \
+    stress_tma_kernel<QQ, GRAD, KK><<<g, kThreads, kTmaSmem, st>>>(a);                                      \
+    break;
+#define GMDS_TMA_Q(QQ)                                                                                    \
+  case QQ:                                                                                                \
+    switch (a.kind) {                                                                                     \
+      GMDS_TMA_KIND(QQ, kKruskal) GMDS_TMA_KIND(QQ, kHuber) GMDS_TMA_KIND(QQ, kSammon)                    \
+      GMDS_TMA_KIND(QQ, kSmacof) GMDS_TMA_KIND(QQ, kGuttman)                                              \
+      default: fail(GMDS_ERROR, "stress pass: bad kind");                                                 \
+    }                                                                                                     \
+    break;
+#define GMDS_INSTANTIATE_TMA(GR)                                                                          \
+  template <>                                                                                             \
+  void launch_pass_td<float, GR>(const PassArgs& a, int Q, cudaStream_t st) {                              \
+    constexpr bool GRAD = GR;                                                                             \
+    const unsigned g = static_cast<unsigned>(a.nchunks);                                                  \
+    switch (Q) {                                                                                          \
+      GMDS_TMA_Q(1) GMDS_TMA_Q(2) GMDS_TMA_Q(3) GMDS_TMA_Q(4)                                             \
+      default: fail(GMDS_ERROR, "stress pass: unsupported padded dimension");                             \
+    }                                                                                                     \
+  }
+
+}  // namespace gmds

@@ -120,7 +120,8 @@ Emb embed(const gmds_dmat* D, int q, int method, uint64_t seed, cudaStream_t st)
 double kruskal_of(const gmds_dmat* D, const double* coords, int q, cudaStream_t st) {
   // kruskal_stress (embed.cpp:462-475)
   if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
-  Engine E(D, q, st);
+  EngineLease L = acquire_engine(D, q, st);
+  Engine& E = *L;
   E.upload(coords, E.Y.get());
   const double* y = E.Y.get();
   return E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
