@@ -5,7 +5,7 @@
 #include <vector>
 
 #include "common.cuh"
-#include "gini_split.cuh"
+#include "gini_merge.cuh"
 #include "kernels.cuh"
 #include "lib_internal.h"
 
@@ -18,19 +18,24 @@ template <int K>
 void launch_gini_list(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64_t* pairs, int64_t npairs, void* dout,
                       gmds_dtype ot, cudaStream_t st);
 
+void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, const int64_t* rowptr, const int* rows,
+                     int nrows, int K, uint16_t* sidx, cudaStream_t st);
+
 namespace {
 
 // warp per row: presence masks, running popcounts, per-row nonzero counts
 template <typename T>
 __global__ void row_mask_kernel(const T* __restrict__ X, int64_t n, int p, int W, uint32_t* __restrict__ masks,
-                                uint16_t* __restrict__ prefix, int* __restrict__ counts) {
+                                uint16_t* __restrict__ prefix, int* __restrict__ counts, int* __restrict__ negflag) {
   const int lane = threadIdx.x & 31;
   for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n;
        row += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
     int run = 0;
     for (int w = 0; w < W; ++w) {
       const int e = w * 32 + lane;
-      const bool nz = (e < p) && (X[row * p + e] != T(0));
+      const T xv = (e < p) ? X[row * p + e] : T(0);
+      const bool nz = xv != T(0);
+      if (xv < T(0)) atomicOr(negflag, 1);
       const unsigned m = __ballot_sync(0xffffffffu, nz);
       if (lane == 0) {
         masks[row * W + w] = m;
@@ -45,7 +50,7 @@ __global__ void row_mask_kernel(const T* __restrict__ X, int64_t n, int p, int W
 template <typename T>
 __global__ void row_fill_kernel(const T* __restrict__ X, int64_t n, int p, int W, const uint32_t* __restrict__ masks,
                                 const uint16_t* __restrict__ prefix, const int64_t* __restrict__ rowptr,
-                                T* __restrict__ vals) {
+                                T* __restrict__ vals, uint16_t* __restrict__ fidx) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < n;
@@ -53,12 +58,18 @@ __global__ void row_fill_kernel(const T* __restrict__ X, int64_t n, int p, int W
     for (int w = 0; w < W; ++w) {
       const int e = w * 32 + lane;
       const unsigned m = masks[row * W + w];
-      if ((m >> lane) & 1u) vals[rowptr[row] + prefix[row * W + w] + __popc(m & lt)] = X[row * p + e];
+      if ((m >> lane) & 1u) {
+        const int64_t o = rowptr[row] + prefix[row * W + w] + __popc(m & lt);
+        vals[o] = X[row * p + e];
+        fidx[o] = static_cast<uint16_t>(e);
+      }
     }
   }
 }
 
 struct RowStore {
+  DevBuf<uint16_t> fidx, sidx;
+  bool nonneg = false;
   DevBuf<uint32_t> masks;
   DevBuf<uint16_t> prefix;
   DevBuf<int64_t> rowptr;
@@ -74,18 +85,23 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
   rs.masks.alloc(static_cast<size_t>(n) * rs.W);
   rs.prefix.alloc(static_cast<size_t>(n) * rs.W);
   DevBuf<int> counts(static_cast<size_t>(n));
+  DevBuf<int> negflag(1);
+  GMDS_CUDA(cudaMemsetAsync(negflag.get(), 0, sizeof(int), st));
   const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 8), 148 * 16)));
   if (xt == GMDS_F32)
     row_mask_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dX), n, p, rs.W, rs.masks.get(),
-                                                   rs.prefix.get(), counts.get());
+                                                   rs.prefix.get(), counts.get(), negflag.get());
   else
     row_mask_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dX), n, p, rs.W, rs.masks.get(),
-                                                    rs.prefix.get(), counts.get());
+                                                    rs.prefix.get(), counts.get(), negflag.get());
   count_launch();
   check_launch("row_mask_kernel");
   std::vector<int> hc(static_cast<size_t>(n));
+  int hneg = 0;
   GMDS_CUDA(cudaMemcpyAsync(hc.data(), counts.get(), n * sizeof(int), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(&hneg, negflag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
+  rs.nonneg = (hneg == 0);
   std::vector<int64_t> rp(static_cast<size_t>(n) + 1, 0);
   for (int64_t i = 0; i < n; ++i) {
     rp[i + 1] = rp[i] + hc[i];
@@ -96,15 +112,37 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
   rs.rowptr.alloc(rp.size());
   GMDS_CUDA(cudaMemcpyAsync(rs.rowptr.get(), rp.data(), rp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   rs.vals.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])) * dtype_size(xt));
+  rs.fidx.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
   if (xt == GMDS_F32)
     row_fill_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dX), n, p, rs.W, rs.masks.get(),
-                                                   rs.prefix.get(), rs.rowptr.get(), reinterpret_cast<float*>(rs.vals.get()));
+                                                   rs.prefix.get(), rs.rowptr.get(), reinterpret_cast<float*>(rs.vals.get()), rs.fidx.get());
   else
     row_fill_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dX), n, p, rs.W, rs.masks.get(),
                                                     rs.prefix.get(), rs.rowptr.get(),
-                                                    reinterpret_cast<double*>(rs.vals.get()));
+                                                    reinterpret_cast<double*>(rs.vals.get()), rs.fidx.get());
   count_launch();
   check_launch("row_fill_kernel");
+  if (rs.nonneg) {
+    // value-sorted feature order per row (the merge kernel's runs); rows bucketed by sort width
+    rs.sidx.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
+    std::vector<std::vector<int>> buckets(6);
+    for (int64_t i = 0; i < n; ++i) {
+      int K = 1;
+      while (32 * K < hc[i]) K <<= 1;
+      int bk = 0;
+      while ((1 << bk) < K) ++bk;
+      buckets[bk].push_back(static_cast<int>(i));
+    }
+    for (int bk = 0; bk < 6; ++bk) {
+      if (buckets[bk].empty()) continue;
+      DevBuf<int> rows(buckets[bk].size());
+      GMDS_CUDA(cudaMemcpyAsync(rows.get(), buckets[bk].data(), buckets[bk].size() * sizeof(int),
+                                cudaMemcpyHostToDevice, st));
+      launch_row_sort(rs.vals.get(), xt, rs.fidx.get(), rs.rowptr.get(), rows.get(),
+                      static_cast<int>(buckets[bk].size()), 1 << bk, rs.sidx.get(), st);
+      GMDS_CUDA(cudaStreamSynchronize(st));
+    }
+  }
   return rs;
 }
 
@@ -160,8 +198,55 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     GMDS_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  int tile = 32;
   const size_t two_per_sm = 113 * 1024, one_per_sm = 220 * 1024;
+  if (sparse && rs.nonneg && p > 32) {  // merge path: pre-sorted row runs + one bitonic merge per sign half
+    int mt = 32;
+    while (mt > 4 && merge_smem(mt, rs.W, std::max(1, rs.maxnnz), sz, nnu) > one_per_sm) mt >>= 1;
+    const size_t msm = merge_smem(mt, rs.W, std::max(1, rs.maxnnz), sz, nnu);
+    if (msm <= one_per_sm) {
+      a.tile = mt;
+      a.nbt = ceil_div(n, mt);
+      const int64_t munits = a.nbt * (a.nbt + 1) / 2;
+      a.tile_begin = munits * shard / nshards;
+      a.tile_end = munits * (shard + 1) / nshards;
+      if (a.tile_end <= a.tile_begin) return;
+      MergeArgs ma{};
+      ma.s.g = a;
+      ma.s.masks = rs.masks.get();
+      ma.s.prefix = rs.prefix.get();
+      ma.s.rowptr = rs.rowptr.get();
+      ma.s.vals = rs.vals.get();
+      ma.s.W = rs.W;
+      ma.s.maxnnz = std::max(1, rs.maxnnz);
+      ma.s.sparse = 1;
+      ma.sidx = rs.sidx.get();
+      const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(mt) * mt;
+      ma.s.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 24) : 0;
+      DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * ma.s.ovf_cap)));
+      DevBuf<unsigned long long> ovf_count(1);
+      GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));
+      ma.s.ovf_pairs = ovf.get();
+      ma.s.ovf_count = ovf_count.get();
+      const unsigned mblocks = static_cast<unsigned>(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30));
+      launch_gini_merge(ma, dX, xt, dD, ot, msm, mblocks, st);
+      count_launch();
+      check_launch("gini_merge_kernel");
+      unsigned long long novf = 0;
+      GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
+      GMDS_CUDA(cudaStreamSynchronize(st));
+      if (novf == 0) return;
+      if (static_cast<int64_t>(novf) > ma.s.ovf_cap) {
+        full_kernel();
+      } else {
+        launch_gini_list<32>(a, dX, xt, ovf.get(), static_cast<int64_t>(novf), dD, ot, st);
+        count_launch();
+        check_launch("gini_list_kernel");
+      }
+      GMDS_CUDA(cudaStreamSynchronize(st));
+      return;
+    }
+  }
+  int tile = 32;
   while (tile > 4 && split_smem(tile, static_cast<int>(p), rs.W, rs.maxnnz, sz, nnu, sparse) > two_per_sm) tile >>= 1;
   if (split_smem(tile, static_cast<int>(p), rs.W, rs.maxnnz, sz, nnu, sparse) > two_per_sm) {
     tile = 32;

@@ -110,6 +110,64 @@ __device__ __forceinline__ void warp_bitonic_upto(double (&v)[K], int lane, int 
   }
 }
 
+// Bitonic merge of 2H = 32K blocked keys whose halves are each a bitonic
+// sequence (ascending run, +inf padding, descending run): the half-cleaner
+// cascade t = H/2 .. 1 (partners stay inside their half).
+template <int K>
+__device__ __forceinline__ void warp_bitonic_merge(double (&v)[K], int lane) {
+  constexpr int H = 16 * K;
+#pragma unroll
+  for (int t = H / 2; t > 0; t >>= 1) {
+    if (t < K) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (!(r & t)) ce_asc(v[r], v[r + t]);
+    } else {
+      const int m = t / K;
+      const bool keep_lo = !(lane & m);
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const double o = __shfl_xor_sync(kFull, v[r], m);
+        const bool tk = keep_lo ? (o < v[r]) : (v[r] < o);
+        v[r] = tk ? o : v[r];
+      }
+    }
+  }
+}
+
+// Tie groups of the sorted split array (negatives in half A, positives in
+// half B), shifted to real positions, and the LUT sum for every nu.
+template <int K>
+__device__ __forceinline__ void finish_split(double (&key)[K], int n_neg, int n_pos, int zeros, int lane,
+                                             const double* __restrict__ lut, int d, int nnu, double half_p, bool store,
+                                             double* out, size_t ostride, int* flag) {
+  constexpr int H = 16 * K;
+  int h[K];
+  warp_tie_groups<K>(key, h, lane);
+  const int shiftB = 2 * (n_neg + zeros) - 2 * H;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int g = lane * K + r;
+    int hh = -1;
+    if (g < n_neg) hh = h[r];
+    else if (g >= H && g < H + n_pos) hh = h[r] + shiftB;
+    h[r] = hh;
+  }
+  for (int v = 0; v < nnu; ++v) {
+    const double* L = lut + static_cast<size_t>(v) * 2 * d;
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      if (h[r] >= 0) acc = fma(key[r], __ldg(L + h[r]), acc);
+    acc = warp_sum(acc);
+    const double val = clamp_nonneg(half_p * acc);
+    if (lane == 0 && store) {
+      out[v * ostride] = val;
+      if (isinf(val)) atomicOr(flag, 1);
+    }
+  }
+}
+
 // Load the compacted nonzeros into blocked registers, sort, find tie groups,
 // and for every nu reduce (p/2) * sum_k z_k L[h_k] across the warp; lane 0
 // writes the clamped distance to *out (stride ostride between nu values).
