@@ -72,6 +72,15 @@ gmds_status gmds_pair_midranks(const void* X, gmds_dtype xt, gmds_layout lx, int
 /* ---- distance: gen_gini_distance (metrics.hpp:105-107, metrics.cpp:157-163) for one pair. */
 gmds_status gmds_gen_gini_distance(const double* x, int64_t dx, const double* y, int64_t dy, double nu, double* out);
 
+/* Directed generalized Gini dissimilarity (metrics.hpp:95-97, metrics.cpp:69-93, 148-151). */
+gmds_status gmds_gen_gini_directed(const double* x, int64_t dx, const double* y, int64_t dy, double nu, double* out);
+/* gini_norm (metrics.hpp:79-80, metrics.cpp:58-66, 112-115). */
+gmds_status gmds_gini_norm(const double* x, int64_t d, double* out);
+/* gini_pseudo_distance (metrics.hpp:85-86, metrics.cpp:119-127). */
+gmds_status gmds_gini_pseudo_distance(const double* x, int64_t dx, const double* y, int64_t dy, double* out);
+/* empirical_survival (metrics.hpp:89-90, metrics.cpp:133-144): out[d]. */
+gmds_status gmds_empirical_survival(const double* z, int64_t d, double* out);
+
 /* ---- pairwise_matrix, Gini branch (metrics.hpp:112, metrics.cpp:193-219 + from_matrix 169-191).
  * nnu values of nu at once (one sort per pair serves them all).  D: host,
  * nnu consecutive n x n matrices of out_t.  Each nu must be > 1
@@ -118,6 +127,9 @@ gmds_status gmds_stress_loss(int32_t kind, const gmds_dmat* D, const double* coo
                              const double* weights, double* out);
 gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q,
                                  double huber_delta, const double* weights, double* grad);
+
+/* double_center (embed.hpp:51, embed.cpp:382-413): S, B host n x n column-major. */
+gmds_status gmds_double_center(const double* S, int64_t n, double* B);
 
 /* classical_mds (embed.cpp:415-460): coords n x q column-major, eigvals q. */
 gmds_status gmds_classical_mds(const gmds_dmat* D, int32_t q, double* coords, double* eigvals, int32_t* clamped_count,

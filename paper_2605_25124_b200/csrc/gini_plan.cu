@@ -221,7 +221,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       ma.s.sparse = 1;
       ma.sidx = rs.sidx.get();
       const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(mt) * mt;
-      ma.s.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 24) : 0;
+      ma.s.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 20) : 0;
       DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * ma.s.ovf_cap)));
       DevBuf<unsigned long long> ovf_count(1);
       GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));
@@ -274,7 +274,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   sa.maxnnz = std::max(1, rs.maxnnz);
   sa.sparse = sparse ? 1 : 0;
   const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(tile) * tile;
-  sa.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 24) : 0;
+  sa.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 20) : 0;
   DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * sa.ovf_cap)));
   DevBuf<unsigned long long> ovf_count(1);
   GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));

@@ -392,3 +392,46 @@ def alternating_tune(X, q: int, outer_iters: int, grid, seed: int = 0) -> dict:
                                        _p(coords), ctypes.byref(st)))
     return dict(nu_path=list(path[:outer_iters]), nu_star=ns.value, coords=np.ascontiguousarray(coords),
                 stress=st.value)
+
+
+# ---- remaining metrics / embed entry points -------------------------------------------------------
+
+
+def gen_gini_directed(x, y, nu: float) -> float:
+    """metrics.hpp:95-97."""
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    y = np.ascontiguousarray(y, dtype=np.float64).ravel()
+    out = np.zeros(1)
+    _check(lib().gmds_gen_gini_directed(_p(x), _i64(x.size), _p(y), _i64(y.size), ctypes.c_double(nu), _p(out)))
+    return float(out[0])
+
+
+def gini_norm(x) -> float:
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    out = np.zeros(1)
+    _check(lib().gmds_gini_norm(_p(x), _i64(x.size), _p(out)))
+    return float(out[0])
+
+
+def gini_pseudo_distance(x, y) -> float:
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    y = np.ascontiguousarray(y, dtype=np.float64).ravel()
+    out = np.zeros(1)
+    _check(lib().gmds_gini_pseudo_distance(_p(x), _i64(x.size), _p(y), _i64(y.size), _p(out)))
+    return float(out[0])
+
+
+def empirical_survival(z) -> np.ndarray:
+    z = np.ascontiguousarray(z, dtype=np.float64).ravel()
+    out = np.zeros(z.size)
+    _check(lib().gmds_empirical_survival(_p(z), _i64(z.size), _p(out)))
+    return out
+
+
+def double_center(S) -> np.ndarray:
+    S = np.asfortranarray(np.asarray(S, dtype=np.float64))
+    if S.ndim != 2 or S.shape[0] != S.shape[1] or S.shape[0] < 1:
+        raise InvalidInput("double_center: matrix is not square")
+    out = np.zeros_like(S, order="F")
+    _check(lib().gmds_double_center(_p(S), _i64(S.shape[0]), _p(out)))
+    return np.ascontiguousarray(out)

@@ -209,3 +209,36 @@ def test_all_zero_rows_and_constant_shift():
     D = G.pairwise_matrix(X, 2.0)
     assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= TOL
     assert D[0, 1] == 0.0
+
+
+def test_directed_norm_survival_golden(golden):
+    g = golden("distance")
+    for x, y, m, nu, fwd in zip(g["x"], g["y"], g["lengths"], g["nu"], g["directed"]):
+        x, y = unpad(x, m), unpad(y, m)
+        assert abs(G.gen_gini_directed(x, y, float(nu)) - fwd) <= 1e-12 * max(1.0, abs(fwd))
+    assert G.gen_gini_directed([10.0, 1200.0], [10.0, 12.0], 3.0) == pytest.approx(445.5, rel=1e-12)
+    assert G.gen_gini_directed([10.0, 12.0], [10.0, 1200.0], 3.0) == pytest.approx(742.5, rel=1e-12)
+    assert G.gini_pseudo_distance([10.0, 1200.0], [10.0, 12.0]) == 594.0
+    assert G.gini_norm([1.0, 2.0, 3.0]) == pytest.approx(2.0, rel=1e-14)
+    assert G.gini_norm([5.0, 5.0, 5.0]) == 0.0
+    assert list(G.empirical_survival([0.0, 1188.0])) == [0.75, 0.25]
+    rng = np.random.default_rng(3)
+    for d in (1, 7, 40, 300):
+        v = np.round(rng.standard_normal(d), 1)
+        assert np.array_equal(G.empirical_survival(v), O.empirical_survival(v))
+        assert G.gini_norm(v) == pytest.approx(O.gini_norm(v), rel=1e-12, abs=1e-12)
+    with pytest.raises(G.InvalidConfig):
+        G.gen_gini_directed([1.0], [2.0], 1.0)
+
+
+def test_double_center():
+    S = np.array([[0.0, 4.0], [4.0, 0.0]])
+    assert np.allclose(G.double_center(S), [[1.0, -1.0], [-1.0, 1.0]], rtol=1e-14)
+    rng = np.random.default_rng(1)
+    P = rng.standard_normal((30, 3))
+    D = O.pairwise_matrix(P, None)
+    B = G.double_center(D * D)
+    assert np.allclose(B, O.double_center(D * D), rtol=1e-10, atol=1e-12)
+    assert np.array_equal(B, B.T)
+    with pytest.raises(G.InvalidInput):
+        G.double_center(np.array([[0.0, 1.0], [3.0, 0.0]]))
