@@ -263,19 +263,36 @@ def run_engine(args, rank, world, dist):
     dist_launches = G.launch_count() - launches0
     t_dist = max_over_ranks(dist, float(np.mean(times)))
 
-    # ---- stress: S Kruskal iterations on the packed matrix of this step (single-GPU fit;
-    # with several ranks every rank fits its own replica of the full matrix)
+    # ---- stress: S Kruskal iterations on the packed matrix of this step.  One GPU: the
+    # device-controlled fit.  Several ranks: the tile-sharded fit, one NCCL all-reduce of
+    # [loss | gradient] per pass (paper_2605_25124_b200/distributed.py).
     Dm = G.dmat_gini_device(dX.data_ptr(), G.F32, N, P, NU, G.F32)
     Y0 = np.random.default_rng(SEED).normal(0.0, 0.1, (N, Q))
-    G.minimize_stress(Dm, Q, "kruskal", max_iters=2, rel_tol=1e-300, Y0=Y0)  # warm-up
+    if world > 1:
+        from paper_2605_25124_b200 import distributed as MD
+
+        allreduce_sum, _ = MD.torch_collectives()
+        part = MD.gpu_partial(Dm, rank, world)
+        stats = MD.dmat_stats(Dm)
+
+        def fit(iters):
+            r = MD.minimize_stress_sharded(part, allreduce_sum, Y0, "kruskal", stats, N, max_iters=iters,
+                                           rel_tol=1e-300)
+            r["passes"] = len(r["stress_history"]) * 2
+            return r
+    else:
+        def fit(iters):
+            return G.minimize_stress(Dm, Q, "kruskal", max_iters=iters, rel_tol=1e-300, Y0=Y0)
+    fit(2)  # warm-up
     barrier()
     launches1 = G.launch_count()
     stimes, siters, spasses = [], 0, 0
     with ClockSampler(dev) as clk2:
         for _ in range(max(1, args.steps)):
+            barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = G.minimize_stress(Dm, Q, "kruskal", max_iters=STRESS_ITERS, rel_tol=1e-300, Y0=Y0)
+            r = fit(STRESS_ITERS)
             e1.record(stream)
             e1.synchronize()
             stimes.append(e0.elapsed_time(e1) / 1e3)
@@ -332,7 +349,7 @@ def run_engine(args, rank, world, dist):
         "gpu_launches": int(dist_launches + stress_launches),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu.value / 1e12, "unit": "Tops/s",
                      "frac": achieved / alu.value, "traffic": None,
-                     "kernel": "gini_tile_kernel", "ops_per_pair": ops_pair,
+                     "kernel": "gini_merge_kernel", "ops_per_pair": ops_pair,
                      "peak_source": "measured on this GPU by gmds_probe_alu (FFMA + IADD3/LOP3 lane-op rate)"},
         "stress_roofline": {"bound": "hbm", "achieved": stress_bytes / pass_time / 1e9, "peak": peaks.get("hbm_gbs"),
                             "unit": "GB/s", "frac": stress_bytes / pass_time / 1e9 / peaks.get("hbm_gbs", 6446.6),

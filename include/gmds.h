@@ -128,6 +128,17 @@ gmds_status gmds_stress_loss(int32_t kind, const gmds_dmat* D, const double* coo
 gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q,
                                  double huber_delta, const double* weights, double* grad);
 
+/* One rank's share of a sharded stress pass: raw loss and raw
+ * per-row gradient sums of `kind` at coords over this shard's tiles of D
+ * (chunks split evenly by block count).  Summing raw_loss / raw_grad over
+ * shards 0..nshards-1 (an all-reduce) gives the full pass; the kind's global
+ * scale (1/(KS*den) for kruskal, 2/sum(D) for sammon) is applied after the
+ * reduction.  q <= 4.  kind GMDS_SMACOF+1 (= 4) is the Guttman transform sum. */
+gmds_status gmds_stress_partial(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q, double huber_delta,
+                                int32_t shard, int32_t nshards, double* raw_loss, double* raw_grad);
+/* Per-fit constants of a device DistanceMatrix: sum D^2, sum D, min and max off-diagonal entry (4 doubles). */
+gmds_status gmds_dmat_stats(const gmds_dmat* d, double* stats4);
+
 /* double_center (embed.hpp:51, embed.cpp:382-413): S, B host n x n column-major. */
 gmds_status gmds_double_center(const double* S, int64_t n, double* B);
 

@@ -97,6 +97,7 @@ void Engine::download(const double* src, double* coords_colmajor) {
 
 PassArgs Engine::args(int kind, double delta) const {
   PassArgs a{};
+  a.chunk_I = nullptr;
   a.D = D->ptr();
   a.W = W;
   a.n = n;
@@ -136,6 +137,46 @@ double Engine::grad_raw(int kind, double delta, const double* Yd) {
     launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
   else
     GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
+  double out = 0.0;
+  GMDS_CUDA(cudaMemcpyAsync(&out, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  ++passes;
+  return out;
+}
+
+// Raw sums over the chunks of shard `shard` of `nshards` (rows of the other
+// shards' chunks contribute nothing): the per-rank pass of a sharded fit,
+// summed across ranks by an all-reduce.
+double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shard, int nshards) {
+  if (rows_mode) fail(GMDS_INVALID_INPUT, "stress_partial: sharded passes support q <= 4");
+  // chunk c covers (blocks) kChunk... weight = number of blocks; split the prefix sum evenly
+  std::vector<int64_t> cI(static_cast<size_t>(nchunks)), cJ(static_cast<size_t>(nchunks));
+  GMDS_CUDA(cudaMemcpyAsync(cI.data(), chunk_I.get(), nchunks * 8, cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(cJ.data(), chunk_J0.get(), nchunks * 8, cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  const int64_t nblk = nb * (nb + 1) / 2;
+  int64_t acc = 0, c0 = nchunks, c1 = nchunks;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t before = acc;
+    acc += std::min<int64_t>(kChunk, nb - cJ[c]);
+    if (c0 == nchunks && before * nshards >= nblk * shard) c0 = c;
+    if (c1 == nchunks && before * nshards >= nblk * (shard + 1)) c1 = c;
+  }
+  // zero the partial buffers of foreign chunks/blocks, then run the pass on the sub-range
+  GMDS_CUDA(cudaMemsetAsync(rowpart.get(), 0, rowpart.n * sizeof(double), st));
+  GMDS_CUDA(cudaMemsetAsync(colpart.get(), 0, colpart.n * sizeof(double), st));
+  GMDS_CUDA(cudaMemsetAsync(losspart.get(), 0, losspart.n * sizeof(double), st));
+  PassArgs a = args(kind, delta);
+  a.Y[0] = Yd;
+  a.ncand = 1;
+  a.chunk_I = chunk_I.get() + c0;
+  a.chunk_J0 = chunk_J0.get() + c0;
+  a.nchunks = c1 - c0;
+  a.rowpart = rowpart.get() + c0 * kPT * Q;
+  a.losspart = losspart.get() + c0 * kMaxCand;
+  if (a.nchunks > 0) launch_stress_pass(a, Q, true, D->storage, st);
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
   double out = 0.0;
   GMDS_CUDA(cudaMemcpyAsync(&out, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -750,6 +791,16 @@ gmds_status gmds_dmat_download(const gmds_dmat* d, double* D_full) {
 }
 
 int64_t gmds_dmat_n(const gmds_dmat* d) { return d ? d->n : 0; }
+
+gmds_status gmds_dmat_stats(const gmds_dmat* d, double* stats4) {
+  return guard([&] {
+    if (!d) fail(GMDS_INVALID_INPUT, "dmat_stats: null handle");
+    stats4[0] = d->sum_sq;
+    stats4[1] = d->sum;
+    stats4[2] = d->min_off;
+    stats4[3] = d->max_val;
+  });
+}
 void gmds_dmat_free(gmds_dmat* d) { delete d; }
 
 gmds_status gmds_kruskal_stress(const gmds_dmat* D, const double* coords, int32_t q, double* out) {
@@ -808,6 +859,22 @@ gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double*
     }
     E.scale_grad(scale);
     E.download(E.graw.get(), grad);
+  });
+}
+
+gmds_status gmds_stress_partial(int32_t kind, const gmds_dmat* D, const double* coords, int32_t q, double huber_delta,
+                                int32_t shard, int32_t nshards, double* raw_loss, double* raw_grad) {
+  return guard([&] {
+    check_coords(D, coords, q, "stress_partial");
+    if (nshards < 1 || shard < 0 || shard >= nshards) fail(GMDS_INVALID_CONFIG, "stress_partial: bad shard");
+    if (q > 4) fail(GMDS_INVALID_INPUT, "stress_partial: sharded passes support q <= 4");
+    Stream st;
+    EngineLease L = acquire_engine(D, q, st.s);
+    Engine& E = *L;
+    E.upload(coords, E.Y.get());
+    // this shard's chunks: a contiguous, pair-balanced slice of the chunk list
+    *raw_loss = E.grad_raw_shard(kind, huber_delta, E.Y.get(), shard, nshards);
+    E.download(E.graw.get(), raw_grad);
   });
 }
 

@@ -32,6 +32,8 @@ struct Engine {
   std::vector<double> loss_raw(int kind, double delta, const double* const* Ys, int nc);
   // raw gradient sums into graw, returns the raw loss at Yd (one pass)
   double grad_raw(int kind, double delta, const double* Yd);
+  // raw sums over one shard's chunks (sharded fits; summed across ranks)
+  double grad_raw_shard(int kind, double delta, const double* Yd, int shard, int nshards);
   // graw *= scale, returns |graw|^2
   double scale_grad(double scale);
   double loss_of(int kind, double raw) const;
