@@ -13,10 +13,10 @@ namespace gmds {
 
 void launch_gini_merge(const MergeArgs& ma, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, size_t smem,
                        unsigned blocks, cudaStream_t st) {
-  if (xt == GMDS_F32 && ot == GMDS_F32) GMDS_MERGE_ONE(float, float);
-  else if (xt == GMDS_F32) GMDS_MERGE_ONE(float, double);
-  else if (ot == GMDS_F32) GMDS_MERGE_ONE(double, float);
-  else GMDS_MERGE_ONE(double, double);
+  // the 32-bit key construction is exact for fp32 inputs only
+  if (xt != GMDS_F32) fail(GMDS_ERROR, "gini_merge_kernel: fp32 inputs only");
+  if (ot == GMDS_F32) GMDS_MERGE_ONE(float, float);
+  else GMDS_MERGE_ONE(float, double);
 }
 
 // warp per row: sort the row's nonzeros (feature order in vals/fidx) by value,

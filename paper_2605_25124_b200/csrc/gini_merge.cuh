@@ -30,13 +30,26 @@ namespace merge_detail {
 
 constexpr int kHalfCap = 256;  // max keys per sign half on the merge path
 constexpr int kMCap = 128;     // max |S_ab| on the merge path
-constexpr int kAB = kHalfCap + kHalfCap / 16;  // skewed half buffer (doubles)
+constexpr int kAB32 = 272;     // skewed u32 half buffer (256 + 256/32, rounded)
 constexpr int kMB = kMCap + kMCap / 16;
-constexpr int kWarpScratch = 2 * kAB + kMB;  // doubles per warp (>= kSplitCap for the fallback)
+// per-warp scratch in doubles: A32 | B32 (u32 keys) | M (fp64 S_ab) | RA | RB (residuals)
+constexpr int kOffB = kAB32 / 2, kOffM = kAB32, kOffRA = kOffM + kMB, kOffRB = kOffRA + kMCap;
+constexpr int kWarpScratch = kOffRB + kMCap;
 static_assert(kWarpScratch >= kSplitCap, "fallback scratch");
 
-// skewed index: blocked reads of K consecutive doubles per lane hit distinct banks
-__device__ __forceinline__ int sk(int e) { return e + (e >> 4); }
+// skewed indices: blocked reads of K consecutive elements per lane hit distinct banks
+__device__ __forceinline__ int sk(int e) { return e + (e >> 4); }    // 8-byte elements
+__device__ __forceinline__ int sk32(int e) { return e + (e >> 5); }  // 4-byte elements
+
+// Exact 32-bit keys of one sign half.  With f = z rounded toward zero to fp32
+// and x = 1 when that rounding was inexact, the magnitude code 2*bits(f) + x
+// orders |z| exactly (an inexact |z| lies strictly between f and the next
+// float, i.e. between the codes 2*bits(f) and 2*bits(f) + 2).  Positives use
+// the code, negatives its complement, so ascending keys = ascending z within
+// the half.  Two DIFFERENT inexact values in the same float interval would
+// share a key: sort_mids detects that and the pair takes the fp64 path.
+__device__ __forceinline__ uint32_t pos_key(float f, bool inexact) { return 2u * __float_as_uint(f) + (inexact ? 1u : 0u); }
+__device__ __forceinline__ uint32_t neg_key(float f, bool inexact) { return 0xFFFFFFFFu - pos_key(f, inexact); }
 
 template <typename T>
 __device__ __forceinline__ T feat_val(const T* vals, const uint32_t* mask, const uint16_t* pre, int f) {
@@ -45,9 +58,13 @@ __device__ __forceinline__ T feat_val(const T* vals, const uint32_t* mask, const
 }
 
 // Sort the unsorted S_ab values (negatives M[0..mneg), positives M[kMCap-1-q])
-// with the split network and write them descending into the tails of A / B.
+// exactly in fp64 with the split network, turn them into 32-bit keys written
+// descending into the tails of A32 / B32, and store the residual z - (+-f) of
+// each inexact one, in ascending-z order, in RA / RB.  Returns true when two
+// different values share a key (the pair then takes the fp64 path).
 template <int KM>
-__device__ __forceinline__ void sort_mids(double* M, int mneg, int mpos, int H, double* A, double* B, int lane) {
+__device__ __forceinline__ bool sort_mids(const double* M, int mneg, int mpos, int H, uint32_t* A32, uint32_t* B32,
+                                          double* RA, double* RB, int lane) {
   constexpr int Hm = 16 * KM;
   double key[KM];
   const bool hiB = lane >= 16;
@@ -64,34 +81,145 @@ __device__ __forceinline__ void sort_mids(double* M, int mneg, int mpos, int H, 
     key[r] = v;
   }
   split_detail::warp_bitonic_upto<KM>(key, lane, Hm);
+  const int cnt = hiB ? mpos : mneg;
+  uint32_t k32[KM];
+  bool inex[KM];
+  int ninex = 0;
 #pragma unroll
   for (int r = 0; r < KM; ++r) {
-    const int g = lane * KM + r;
-    if (g < mneg) A[sk(H - 1 - g)] = key[r];
-    else if (g >= Hm && g - Hm < mpos) B[sk(H - 1 - (g - Hm))] = key[r];
+    const int q = l16 * KM + r;  // slot within the half (ascending z)
+    const double z = key[r];
+    const double mag = fabs(z);
+    const float f = __double2float_rz(mag);
+    inex[r] = (q < cnt) && (static_cast<double>(f) != mag);
+    k32[r] = hiB ? pos_key(f, inex[r]) : neg_key(f, inex[r]);
+    ninex += inex[r] ? 1 : 0;
+  }
+  // collisions: equal key, different value, between adjacent real slots of the half
+  bool coll = false;
+  const double znext0 = __shfl_down_sync(kFull, key[0], 1);
+  const uint32_t knext0 = __shfl_down_sync(kFull, k32[0], 1);
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int q = l16 * KM + r;
+    const double zn = (r + 1 < KM) ? key[r + 1 < KM ? r + 1 : 0] : znext0;
+    const uint32_t kn = (r + 1 < KM) ? k32[r + 1 < KM ? r + 1 : 0] : knext0;
+    if (q + 1 < cnt && kn == k32[r] && zn != key[r]) coll = true;
+  }
+  if (__any_sync(kFull, coll)) return true;
+  // exclusive prefix of inexact counts within each 16-lane half
+  int incl = ninex;
+#pragma unroll
+  for (int d = 1; d < 16; d <<= 1) {
+    const int o = __shfl_up_sync(kFull, incl, d, 16);
+    if (l16 >= d) incl += o;
+  }
+  int t = incl - ninex;
+  double* R = hiB ? RB : RA;
+  uint32_t* T32 = hiB ? B32 : A32;
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int q = l16 * KM + r;
+    if (q < cnt) {
+      T32[sk32(H - 1 - q)] = k32[r];
+      if (inex[r]) {
+        const double z = key[r];
+        const double f = static_cast<double>(__double2float_rz(fabs(z)));
+        R[t++] = hiB ? z - f : z + f;  // exact (Sterbenz)
+      }
+    }
+  }
+  return false;
+}
+
+// Bitonic merge of 2H = 32K blocked u32 keys (two independent bitonic halves).
+template <int K>
+__device__ __forceinline__ void warp_merge_u32(uint32_t (&v)[K], int lane) {
+  constexpr int H = 16 * K;
+#pragma unroll
+  for (int t = H / 2; t > 0; t >>= 1) {
+    if (t < K) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (!(r & t)) {
+          const uint32_t a = v[r], b = v[r + t];
+          v[r] = min(a, b);
+          v[r + t] = max(a, b);
+        }
+    } else {
+      const int m = t / K;
+      const bool keep_lo = !(lane & m);
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const uint32_t o = __shfl_xor_sync(kFull, v[r], m);
+        v[r] = keep_lo ? min(v[r], o) : max(v[r], o);
+      }
+    }
   }
 }
 
 template <int K>
-__device__ __forceinline__ void merge_and_finish(const double* A, const double* B, int cn, int mneg, int cp, int mpos,
-                                                 int zeros, int lane, const double* __restrict__ lut, int d, int nnu,
+__device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint32_t* B32, const double* RA,
+                                                 const double* RB, int cn, int mneg, int cp, int mpos, int zeros,
+                                                 int lane, const double* __restrict__ lut, int d, int nnu,
                                                  double half_p, bool store, double* out, size_t ostride, int* flag) {
   constexpr int H = 16 * K;
-  double key[K];
+  uint32_t key[K];
   const bool hiB = lane >= 16;
   const int l16 = lane & 15;
-  const double* src = hiB ? B : A;
+  const uint32_t* src = hiB ? B32 : A32;
   const int head = hiB ? cp : cn;
   const int tail = H - (hiB ? mpos : mneg);
 #pragma unroll
   for (int r = 0; r < K; ++r) {
     const int g = l16 * K + r;  // slot within the half
-    key[r] = (g < head || g >= tail) ? src[sk(g)] : INFINITY;
+    key[r] = (g < head || g >= tail) ? src[sk32(g)] : 0xFFFFFFFFu;
   }
   __syncwarp();
-  split_detail::warp_bitonic_merge<K>(key, lane);
-  split_detail::finish_split<K>(key, cn + mneg, cp + mpos, zeros, lane, lut, d, nnu, half_p, store, out, ostride,
-                                flag);
+  warp_merge_u32<K>(key, lane);
+  int h[K];
+  warp_tie_groups<K>(key, h, lane);
+  const int n_neg = cn + mneg, n_pos = cp + mpos;
+  const int shiftB = 2 * (n_neg + zeros) - 2 * H;
+  // values: +-f from the key, plus the residual of inexact (odd-code) S_ab keys
+  int nodd = 0;
+  double z[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int g = lane * K + r;
+    const bool real = hiB ? (g - H < n_pos) : (g < n_neg);
+    const uint32_t code = hiB ? key[r] : 0xFFFFFFFFu - key[r];
+    const double f = static_cast<double>(__uint_as_float(code >> 1));
+    z[r] = hiB ? f : -f;
+    h[r] = real ? (hiB ? h[r] + shiftB : h[r]) : -1;
+    nodd += (real && (code & 1u)) ? 1 : 0;
+  }
+  int incl = nodd;
+#pragma unroll
+  for (int dd = 1; dd < 16; dd <<= 1) {
+    const int o = __shfl_up_sync(kFull, incl, dd, 16);
+    if (l16 >= dd) incl += o;
+  }
+  int t = incl - nodd;
+  const double* R = hiB ? RB : RA;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const uint32_t code = hiB ? key[r] : 0xFFFFFFFFu - key[r];
+    if (h[r] >= 0 && (code & 1u)) z[r] += R[t++];
+  }
+  for (int v = 0; v < nnu; ++v) {
+    const double* L = lut + static_cast<size_t>(v) * 2 * d;
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      if (h[r] >= 0) acc = fma(z[r], __ldg(L + h[r]), acc);
+    acc = warp_sum(acc);
+    const double val = clamp_nonneg(half_p * acc);
+    if (lane == 0 && store) {
+      out[v * ostride] = val;
+      if (isinf(val)) atomicOr(flag, 1);
+    }
+  }
 }
 
 }  // namespace merge_detail
@@ -112,9 +240,11 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   double* scratch = reinterpret_cast<double*>(smem_raw) + warp * kWarpScratch;
-  double* A = scratch;
-  double* B = scratch + kAB;
-  double* M = scratch + 2 * kAB;
+  uint32_t* A32 = reinterpret_cast<uint32_t*>(scratch);
+  uint32_t* B32 = reinterpret_cast<uint32_t*>(scratch + kOffB);
+  double* M = scratch + kOffM;
+  double* RA = scratch + kOffRA;
+  double* RB = scratch + kOffRB;
   double* otile = reinterpret_cast<double*>(smem_raw) + nwarps * kWarpScratch;
   const int tstride = tile + 1;
   unsigned char* pbase = reinterpret_cast<unsigned char*>(otile + static_cast<size_t>(a.nnu) * tile * tstride);
@@ -181,11 +311,12 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
         const int w = f >> 5, b = f & 31;
         const uint32_t mjw = mj[w];
         const bool inj = in && ((mjw >> b) & 1u);
-        const double av = in ? static_cast<double>(vi[pi[w] + __popc(mi[w] & ((1u << b) - 1u))]) : 0.0;
+        const T avt = in ? vi[pi[w] + __popc(mi[w] & ((1u << b) - 1u))] : T(0);
+        const double av = static_cast<double>(avt);
         const unsigned bp = __ballot_sync(kFull, in && !inj);
         if (in && !inj) {
           const int pos = cp + __popc(bp & lt);
-          if (pos < kHalfCap) B[sk(pos)] = av;
+          if (pos < kHalfCap) B32[sk32(pos)] = pos_key(static_cast<float>(avt), false);
         }
         cp += __popc(bp);
         double z = 0.0;
@@ -213,7 +344,8 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
         const unsigned bn = __ballot_sync(kFull, in && !ini);
         if (in && !ini) {
           const int pos = cn + __popc(bn & lt);
-          if (pos < kHalfCap) A[sk(pos)] = -static_cast<double>(vj[pj[w] + __popc(mj[w] & ((1u << b) - 1u))]);
+          if (pos < kHalfCap)
+            A32[sk32(pos)] = neg_key(static_cast<float>(vj[pj[w] + __popc(mj[w] & ((1u << b) - 1u))]), false);
         }
         cn += __popc(bn);
       }
@@ -221,31 +353,39 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
       const int zeros = d - n_neg - n_pos;
       const bool fits = n_neg <= kHalfCap && n_pos <= kHalfCap && mneg + mpos <= kMCap;
       __syncwarp();
+      bool done = false;
       if (fits) {
         if (n_neg + n_pos == 0) {
           if (valid && lane == 0)
             for (int v = 0; v < a.nnu; ++v) ot[v * ostride] = 0.0;
+          done = true;
         } else {
           const int H = max(16, npow2(max(n_neg, n_pos)));
+          bool coll = false;
           if (mneg + mpos > 0) {
             const int Hm = max(16, npow2(max(mneg, mpos)));
             switch (Hm / 16) {
-              case 1: sort_mids<1>(M, mneg, mpos, H, A, B, lane); break;
-              case 2: sort_mids<2>(M, mneg, mpos, H, A, B, lane); break;
-              case 4: sort_mids<4>(M, mneg, mpos, H, A, B, lane); break;
-              default: sort_mids<8>(M, mneg, mpos, H, A, B, lane); break;
+              case 1: coll = sort_mids<1>(M, mneg, mpos, H, A32, B32, RA, RB, lane); break;
+              case 2: coll = sort_mids<2>(M, mneg, mpos, H, A32, B32, RA, RB, lane); break;
+              case 4: coll = sort_mids<4>(M, mneg, mpos, H, A32, B32, RA, RB, lane); break;
+              default: coll = sort_mids<8>(M, mneg, mpos, H, A32, B32, RA, RB, lane); break;
             }
             __syncwarp();
           }
-          switch (H / 16) {
-            case 1: merge_and_finish<1>(A, B, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
-            case 2: merge_and_finish<2>(A, B, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
-            case 4: merge_and_finish<4>(A, B, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
-            case 8: merge_and_finish<8>(A, B, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
-            default: merge_and_finish<16>(A, B, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
+          if (!coll) {
+            switch (H / 16) {
+              case 1: merge_and_finish<1>(A32, B32, RA, RB, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
+              case 2: merge_and_finish<2>(A32, B32, RA, RB, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
+              case 4: merge_and_finish<4>(A32, B32, RA, RB, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
+              case 8: merge_and_finish<8>(A32, B32, RA, RB, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
+              default: merge_and_finish<16>(A32, B32, RA, RB, cn, mneg, cp, mpos, zeros, lane, a.lut, d, a.nnu, half_p, valid, ot, ostride, a.flag); break;
+            }
+            done = true;
           }
         }
-      } else {
+      }
+      if (!done) {
+        __syncwarp();
         // ---- fallback: full split path (z in feature order, compaction, network) on the same panels
         double* scr = scratch;  // kSplitCap doubles
         int nn = 0, np = 0;

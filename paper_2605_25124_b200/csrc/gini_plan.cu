@@ -199,7 +199,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     return;
   }
   const size_t two_per_sm = 113 * 1024, one_per_sm = 220 * 1024;
-  if (sparse && rs.nonneg && p > 32) {  // merge path: pre-sorted row runs + one bitonic merge per sign half
+  if (sparse && rs.nonneg && p > 32 && xt == GMDS_F32) {  // merge path (exact u32 keys need fp32 inputs): pre-sorted row runs + one bitonic merge per sign half
     int mt = 32;
     while (mt > 4 && merge_smem(mt, rs.W, std::max(1, rs.maxnnz), sz, nnu) > one_per_sm) mt >>= 1;
     const size_t msm = merge_smem(mt, rs.W, std::max(1, rs.maxnnz), sz, nnu);

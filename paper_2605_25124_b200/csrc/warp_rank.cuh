@@ -132,14 +132,14 @@ __device__ __forceinline__ void warp_bitonic_sort(double (&v)[K], typename Paylo
 
 // After a sort: for every slot, h = a + b where [a, b) is its tie group
 // (0-based, b exclusive).  Midrank R = (h + 1) / 2.
-template <int K>
-__device__ __forceinline__ void warp_tie_groups(const double (&v)[K], int (&h)[K], int lane) {
+template <int K, typename KT>
+__device__ __forceinline__ void warp_tie_groups(const KT (&v)[K], int (&h)[K], int lane) {
   // group starts: slot g starts a group iff g == 0 or v[g] != v[g-1]
-  const double prev_last = __shfl_up_sync(kFull, v[K - 1], 1);
+  const KT prev_last = __shfl_up_sync(kFull, v[K - 1], 1);
   int start_pos[K];
 #pragma unroll
   for (int r = 0; r < K; ++r) {
-    const double prev = (r == 0) ? prev_last : v[r - 1];
+    const KT prev = (r == 0) ? prev_last : v[r - 1];
     const bool st = (r == 0 && lane == 0) ? true : (v[r] != prev);
     start_pos[r] = st ? (lane * K + r) : -1;
   }

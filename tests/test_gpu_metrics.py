@@ -242,3 +242,31 @@ def test_double_center():
     assert np.array_equal(B, B.T)
     with pytest.raises(G.InvalidInput):
         G.double_center(np.array([[0.0, 1.0], [3.0, 0.0]]))
+
+
+def test_merge_path_exact_keys_adversarial():
+    # The merge path orders each sign half by 32-bit keys (fp32 magnitude rounded
+    # toward zero + an "inexact" bit).  Craft sparse non-negative fp32 rows where
+    # (a) two different differences fall in the same fp32 interval (key collision
+    # -> exact fp64 fallback), (b) a difference ties EXACTLY with a plain value of
+    # the other row, (c) magnitudes span 1e-30 .. 1e30 (inexact differences).
+    p = 96
+    rng = np.random.default_rng(17)
+    X = np.zeros((48, p), dtype=np.float32)
+    for i in range(48):
+        idx = rng.choice(p, 20, replace=False)
+        X[i, idx] = rng.choice(np.float32([1.0, 0.5, 0.25, 0.75, 2.0 ** -30, 2.0 ** -29, 1e-30, 1e30, 3.0,
+                                           1.0 + 2.0 ** -23]), 20)
+    X[0, :4] = [1.0, 1.0, 0.0, 0.25]
+    X[1, :4] = [2.0 ** -30, 2.0 ** -29, 0.25, 0.0]  # z = 1-2^-30, 1-2^-29 (same fp32 interval), -0.25, 0.25
+    X[2, :3] = [0.5, 0.25, 0.0]
+    X[3, :3] = [0.25, 0.0, 0.25]                   # z = 0.25 (S_ab) ties with 0.25 (S_a)
+    Xd = X.astype(np.float64)
+    for nu in (1.3, 2.0, 4.0):
+        D = G.pairwise_matrix(X, nu)
+        ref = O.pairwise_matrix(Xd, nu)
+        assert maxnorm_err(D, ref) <= 1e-12
+        # and pair by pair relative to the pair's own value (ties change D at ~1e-8 relative)
+        iu = np.triu_indices(48, 1)
+        big = ref[iu] > 1e-6 * ref.max()
+        assert np.max(np.abs(D[iu][big] - ref[iu][big]) / ref[iu][big]) <= 1e-9
