@@ -76,6 +76,7 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
   Y.alloc(static_cast<size_t>(n * Q));
   for (auto& b : cand) b.alloc(static_cast<size_t>(n * Q));
   scal.alloc(8);
+  sqpart.alloc(kSqBlocks);
   GMDS_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -186,7 +187,7 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
 }
 
 double Engine::scale_grad(double scale) {
-  launch_scale_sqnorm(graw.get(), n * Q, scale, scal.get() + 4, st);
+  launch_scale_sqnorm(graw.get(), n * Q, scale, scal.get() + 4, sqpart.get(), st);
   double gsq = 0.0;
   GMDS_CUDA(cudaMemcpyAsync(&gsq, scal.get() + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));

@@ -21,7 +21,7 @@ struct Engine {
   int64_t passes = 0;  // passes over D issued by this engine
   const void* W = nullptr;
   DevBuf<int64_t> chunk_I, chunk_J0, strip_first;
-  DevBuf<double> rowpart, colpart, losspart, graw, scal, Y;
+  DevBuf<double> rowpart, colpart, losspart, graw, scal, Y, sqpart;
   DevBuf<double> cand[kMaxCand];
 
   Engine(const gmds_dmat* D, int q, cudaStream_t st);

@@ -37,7 +37,8 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
                         int64_t nb, int q, double* out, cudaStream_t st);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
-void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, cudaStream_t st);
+constexpr int kSqBlocks = 148;
+void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& s, double* const* outs,
                       cudaStream_t st);
 void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st);

@@ -56,18 +56,28 @@ __global__ void stress_rows_kernel(PassArgs a, int q, int grad) {
 }
 
 // Stage 2: out[r][k] = sum over strip-R chunks of rowpart + sum over I <= R of colpart(I, R).
+// Eight lanes per output (strided over the partial list), combined by a fixed
+// xor-tree: deterministic, and eight times the loads in flight.
 __global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart,
                                    const int64_t* __restrict__ strip_first, int64_t n, int64_t nb, int Q,
                                    double* __restrict__ out) {
-  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= n * Q) return;
-  const int64_t r = e / Q;
-  const int k = static_cast<int>(e % Q);
-  const int64_t R = r / kPT, rr = r % kPT;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int sub = static_cast<int>(t & 7);
+  const int64_t e = t >> 3;
+  const bool live = e < n * Q;
   double s = 0.0;
-  for (int64_t c = strip_first[R]; c < strip_first[R + 1]; ++c) s += rowpart[(c * kPT + rr) * Q + k];
-  for (int64_t I = 0; I <= R; ++I) s += colpart[(blk_index(I, R, nb) * kPT + rr) * Q + k];
-  out[e] = s;
+  if (live) {
+    const int64_t r = e / Q;
+    const int k = static_cast<int>(e % Q);
+    const int64_t R = r / kPT, rr = r % kPT;
+    const int64_t c0 = strip_first[R], c1 = strip_first[R + 1];
+    for (int64_t c = c0 + sub; c < c1; c += 8) s += rowpart[(c * kPT + rr) * Q + k];
+    for (int64_t I = sub; I <= R; I += 8) s += colpart[(blk_index(I, R, nb) * kPT + rr) * Q + k];
+  }
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  if (live && sub == 0) out[e] = s;
 }
 
 // Deterministic single-CTA sums: out[c] = sum_k part[k*stride + c] for c < m.
@@ -88,11 +98,13 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int64_t count,
   }
 }
 
-// g *= scale (in place); out = sum g^2 (deterministic single CTA).
-__global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double scale, double* __restrict__ out) {
-  __shared__ double red[1024];
+// g *= scale (in place); per-block partial sums of g^2 (fixed order), then
+// sum_parts_kernel adds the block partials: deterministic.
+__global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double scale, double* __restrict__ part) {
+  __shared__ double red[256];
   double s = 0.0;
-  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double v = g[k] * scale;
     g[k] = v;
     s += v * v;
@@ -103,7 +115,7 @@ __global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double sc
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = red[0];
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 
 // out_c = Y - step_c * G for each candidate (trial = coords - step * grad, embed.cpp:243).
@@ -156,7 +168,7 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
 
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
                         int64_t nb, int q, double* out, cudaStream_t st) {
-  const int64_t m = n * q;
+  const int64_t m = n * q * 8;
   reduce_rows_kernel<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, st>>>(rowpart, colpart, strip_first, n, nb,
                                                                              q, out);
   count_launch();
@@ -169,9 +181,11 @@ void launch_sum_parts(const double* part, int64_t count, int stride, int m, doub
   check_launch("sum_parts_kernel");
 }
 
-void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, cudaStream_t st) {
-  scale_sqnorm_kernel<<<1, 1024, 0, st>>>(g, m, scale, out);
-  count_launch();
+void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st) {
+  const int blocks = static_cast<int>(std::min<int64_t>(kSqBlocks, std::max<int64_t>(1, ceil_div(m, 1024))));
+  scale_sqnorm_kernel<<<blocks, 256, 0, st>>>(g, m, scale, part);
+  sum_parts_kernel<<<1, 1024, 0, st>>>(part, blocks, 1, 1, out);
+  count_launch(2);
   check_launch("scale_sqnorm_kernel");
 }
 

@@ -87,7 +87,7 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 }  // namespace tma_detail
 
 template <int Q, bool GRAD, int KIND>
-__global__ void __launch_bounds__(kThreads) stress_tma_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
   constexpr int NCM = GRAD ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
