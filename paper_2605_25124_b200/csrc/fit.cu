@@ -35,6 +35,7 @@ namespace {
 
 constexpr int64_t kChunk = 4;
 constexpr double kTiny = 1e-300;  // embed.cpp:13
+constexpr bool kFusedTrials = false;
 
 int padded_q(int q) { return q <= 4 ? q : q; }
 
@@ -64,8 +65,11 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
     GMDS_CUDA(cudaMemcpyAsync(chunk_J0.get(), cJ.data(), cJ.size() * 8, cudaMemcpyHostToDevice, st));
     GMDS_CUDA(cudaMemcpyAsync(strip_first.get(), sf.data(), sf.size() * 8, cudaMemcpyHostToDevice, st));
     const int64_t nblk = nb * (nb + 1) / 2;
-    rowpart.alloc(static_cast<size_t>(nchunks * kPT * Q));
-    colpart.alloc(static_cast<size_t>(nblk * kPT * Q));
+    gcand = (D->storage == GMDS_F32) ? kTmaCands : 1;  // fp32 passes can carry two trial gradients
+    stride_row = nchunks * kPT * Q;
+    stride_col = nblk * kPT * Q;
+    rowpart.alloc(static_cast<size_t>(stride_row * gcand));
+    colpart.alloc(static_cast<size_t>(stride_col * gcand));
     losspart.alloc(static_cast<size_t>(nchunks * kMaxCand));
   } else {
     nchunks = n;
@@ -112,7 +116,29 @@ PassArgs Engine::args(int kind, double delta) const {
   a.rowpart = rowpart.get();
   a.colpart = colpart.get();
   a.losspart = losspart.get();
+  a.cand_stride_row = stride_row;
+  a.cand_stride_col = stride_col;
   return a;
+}
+
+// One pass: losses AND gradient partials at nc <= gcand trial points (fp32 D).
+std::vector<double> Engine::fused_trials(int kind, double delta, const double* const* Ys, int nc) {
+  PassArgs a = args(kind, delta);
+  for (int c = 0; c < nc; ++c) a.Y[c] = Ys[c];
+  a.ncand = nc;
+  launch_stress_pass(a, Q, true, D->storage, st);
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
+  std::vector<double> out(static_cast<size_t>(nc));
+  GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  ++passes;
+  return out;
+}
+
+// graw <- reduced gradient of trial point c of the last fused pass
+void Engine::reduce_candidate(int c) {
+  launch_reduce_rows(rowpart.get() + c * stride_row, colpart.get() + c * stride_col, strip_first.get(), n, nb, Q,
+                     graw.get(), st);
 }
 
 std::vector<double> Engine::loss_raw(int kind, double delta, const double* const* Ys, int nc) {
@@ -313,20 +339,30 @@ struct IterResult {
   std::vector<double> history;
 };
 
-// gradient_descent (embed.cpp:222-272) with batched Armijo trials.
+// gradient_descent (embed.cpp:222-272) with batched Armijo trials.  With fp32
+// storage the first trial batch also carries both trial gradients, so an
+// accepted trial hands the next iteration its gradient: one pass of D per
+// iteration in the common case (step or step/2 accepted).
 IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double rel_tol) {
   IterResult r;
   const int kind = rp.kind;
+  // Fused trial gradients are implemented (fused_trials / reduce_candidate) but
+  // measured slower on B200 than a separate gradient pass (one 2-candidate
+  // GRAD pass: 800 us vs 333 + 239 us for the two passes at n = 20000; the
+  // per-row shuffle trees double with the candidates), so they stay off.
+  const bool fused = kFusedTrials && (E.gcand >= 2) && !E.rows_mode;
   double* Yc[kMaxCand];
-  const double* y0 = E.Y.get();
-  double f = E.loss_of(kind, E.loss_raw(kind, rp.delta, &y0, 1)[0]);
+  // f = loss_value(coords) and the first gradient come from one pass
+  double raw = E.grad_raw(kind, rp.delta, E.Y.get());
+  double f = E.loss_of(kind, raw);
   r.history.push_back(f);
+  bool have_grad = true;
   double step = 1.0;
   constexpr double armijo = 1e-4;
   int it = 0;
   bool stalled = false;
   for (; it < max_iters; ++it) {
-    const double raw = E.grad_raw(kind, rp.delta, E.Y.get());
+    if (!have_grad) raw = E.grad_raw(kind, rp.delta, E.Y.get());
     double scale = 1.0;
     if (kind == kKruskal) {
       const double ks = std::sqrt(raw / E.D->sum_sq);
@@ -342,11 +378,13 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     double f_new = f;
     bool accepted = false;
     int acc_c = -1;
+    have_grad = false;
     for (int halvings = 0; halvings < 60 && !accepted;) {
       Steps s{};
       // first batch: step and step/2 (the common accept pattern after a doubling);
-      // further batches: four halvings per pass
-      s.n = std::min((halvings == 0 || E.D->storage == GMDS_F32) ? 2 : kMaxCand, 60 - halvings);
+      // further batches: loss-only passes, four (fp64) or two (fp32) halvings each
+      const bool first = (halvings == 0);
+      s.n = std::min((first || E.D->storage == GMDS_F32) ? 2 : kMaxCand, 60 - halvings);
       double sv = step;
       for (int c = 0; c < s.n; ++c) {
         s.v[c] = sv;
@@ -354,7 +392,9 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
       }
       for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();  // buffers rotate on acceptance
       launch_axpy_cand(E.Y.get(), E.graw.get(), E.n * E.Q, s, Yc, E.st);
-      const std::vector<double> raws = E.loss_raw(kind, rp.delta, Yc, s.n);
+      const bool with_grad = fused && first;
+      const std::vector<double> raws =
+          with_grad ? E.fused_trials(kind, rp.delta, Yc, s.n) : E.loss_raw(kind, rp.delta, Yc, s.n);
       for (int c = 0; c < s.n; ++c) {
         const double fc = E.loss_of(kind, raws[c]);
         if (fc <= f - armijo * s.v[c] * grad_sq) {
@@ -362,6 +402,11 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
           acc_c = c;
           f_new = fc;
           step = s.v[c];
+          if (with_grad) {
+            E.reduce_candidate(c);  // gradient at the accepted point, same pass
+            raw = raws[c];
+            have_grad = true;
+          }
           break;
         }
       }

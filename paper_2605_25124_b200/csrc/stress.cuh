@@ -10,6 +10,7 @@ namespace gmds {
 
 enum PassKind { kKruskal = 0, kHuber = 1, kSammon = 2, kSmacof = 3, kGuttman = 4 };
 constexpr int kMaxCand = 4;
+constexpr int kTmaCands = 2;  // trial points of an fp32 (TMA) pass
 
 struct PassArgs {
   const void* D;            // packed image (storage dtype)
@@ -26,6 +27,8 @@ struct PassArgs {
   double* rowpart;          // [nchunks][kPT][Q]  (rows kernel: [n][q] final)
   double* colpart;          // [nblk][kPT][Q]
   double* losspart;         // [nchunks][kMaxCand] (rows kernel: [n][kMaxCand])
+  int64_t cand_stride_row;  // elements between candidates' rowpart images (fused trial passes)
+  int64_t cand_stride_col;  // elements between candidates' colpart images
 };
 
 struct Steps {

@@ -89,7 +89,7 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 template <int Q, bool GRAD, int KIND>
 __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
-  constexpr int NCM = GRAD ? 1 : kTmaCand;
+  constexpr int NCM = kTmaCand;  // GRAD passes may carry the gradient of both Armijo trial points
   extern __shared__ __align__(128) unsigned char dyn[];
   float* ring = reinterpret_cast<float*>(dyn);  // [kStages][kHalfFloats]
   __shared__ __align__(8) uint64_t bars[kStages];
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   __shared__ float sYj[NCM][kPT][Q];  // [yslot(r)]
   __shared__ double sRed[GRAD ? kTG * kPT : 1];
   __shared__ double sLoss[kThreads / 32][kMaxCand];
-  __shared__ double sRowTot[GRAD ? kPT * Q : 1];
+  __shared__ double sRowTot[GRAD ? NCM * kPT * Q : 1];
 
   const int tid = threadIdx.x;
   const int ti = tid / kTG, tj = tid % kTG;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   const int64_t J1 = min(J0 + a.chunk_len, a.nb);
   const int nblocks = static_cast<int>(J1 - J0);
   const int nhalves = 2 * nblocks;
-  const int nc = GRAD ? 1 : a.ncand;
+  const int nc = a.ncand;
   const float* __restrict__ D = static_cast<const float*>(a.D);
   const float* __restrict__ W = static_cast<const float*>(a.W);
   const float delta = static_cast<float>(a.huber_delta);
@@ -133,12 +133,12 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
     sYi[c][r][k] = (i < a.n) ? static_cast<float>(a.Y[c][i * Q + k]) : 0.f;
   }
   if constexpr (GRAD) {
-    for (int e = tid; e < kPT * Q; e += kThreads) sRowTot[e] = 0.0;
+    for (int e = tid; e < NCM * kPT * Q; e += kThreads) sRowTot[e] = 0.0;
   }
   double lossacc[NCM];
 #pragma unroll
   for (int c = 0; c < NCM; ++c) lossacc[c] = 0.0;
-  float colacc[GRAD ? kMT : 1][Q];
+  float colacc[GRAD ? NCM : 1][GRAD ? kMT : 1][Q];
   float yj[NCM][kMT][Q];  // this thread's 8 columns, loaded once per block
 
   for (int h = 0; h < nhalves; ++h) {
@@ -153,9 +153,11 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
       }
       if constexpr (GRAD) {
 #pragma unroll
-        for (int y = 0; y < kMT; ++y)
+        for (int c = 0; c < NCM; ++c)
 #pragma unroll
-          for (int k = 0; k < Q; ++k) colacc[y][k] = 0.f;
+          for (int y = 0; y < kMT; ++y)
+#pragma unroll
+            for (int k = 0; k < Q; ++k) colacc[c][y][k] = 0.f;
       }
       __syncthreads();
 #pragma unroll
@@ -180,9 +182,11 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
       float wv[kMT];
 #pragma unroll
       for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tj * kMT + y] : 1.f;
-      float rowacc[Q];
+      float rowacc[GRAD ? NCM : 1][Q];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) rowacc[k] = 0.f;
+      for (int c = 0; c < (GRAD ? NCM : 1); ++c)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) rowacc[c][k] = 0.f;
       float lossrow[NCM];
 #pragma unroll
       for (int c = 0; c < NCM; ++c) lossrow[c] = 0.f;
@@ -223,8 +227,8 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
             if constexpr (GRAD) {
 #pragma unroll
               for (int k = 0; k < Q; ++k) {
-                rowacc[k] = fmaf(cc, dy[k], rowacc[k]);
-                colacc[y][k] = fmaf(-cc, dy[k], colacc[y][k]);
+                rowacc[c][k] = fmaf(cc, dy[k], rowacc[c][k]);
+                colacc[c][y][k] = fmaf(-cc, dy[k], colacc[c][y][k]);
               }
             }
           }
@@ -238,26 +242,34 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
       for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
       if constexpr (GRAD) {
 #pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          double v = static_cast<double>(rowacc[k]);
+        for (int c = 0; c < NCM; ++c) {
+          if (c >= nc) break;
 #pragma unroll
-          for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-          if (tj == 0) sRowTot[ri * Q + k] += v;
+          for (int k = 0; k < Q; ++k) {
+            double v = static_cast<double>(rowacc[c][k]);
+#pragma unroll
+            for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+            if (tj == 0) sRowTot[(c * kPT + ri) * Q + k] += v;
+          }
         }
       }
     }
     if constexpr (GRAD) {
-      if (half == 1) {  // column partials of block J (rows ti*4.. of both halves)
+      if (half == 1) {  // column partials of block J (rows ti*4.. of both halves), per candidate
 #pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          __syncthreads();
+        for (int c = 0; c < NCM; ++c) {
+          if (c >= nc) break;
 #pragma unroll
-          for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = static_cast<double>(colacc[y][k]);
-          __syncthreads();
-          if (tid < kPT) {
-            double s = 0.0;
-            for (int t = 0; t < kTG; ++t) s += sRed[t * kPT + tid];
-            a.colpart[(blk * kPT + tid) * Q + k] = s;
+          for (int k = 0; k < Q; ++k) {
+            __syncthreads();
+#pragma unroll
+            for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = static_cast<double>(colacc[c][y][k]);
+            __syncthreads();
+            if (tid < kPT) {
+              double s = 0.0;
+              for (int t = 0; t < kTG; ++t) s += sRed[t * kPT + tid];
+              a.colpart[c * a.cand_stride_col + (blk * kPT + tid) * Q + k] = s;
+            }
           }
         }
       }
@@ -267,7 +279,8 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   }
   if constexpr (GRAD) {
     __syncthreads();
-    for (int e = tid; e < kPT * Q; e += kThreads) a.rowpart[chunk * (kPT * Q) + e] = sRowTot[e];
+    for (int e = tid; e < nc * kPT * Q; e += kThreads)
+      a.rowpart[(e / (kPT * Q)) * a.cand_stride_row + chunk * (kPT * Q) + e % (kPT * Q)] = sRowTot[e];
   }
 #pragma unroll
   for (int c = 0; c < NCM; ++c) {
