@@ -58,6 +58,16 @@ def ops_per_pair(p, nnu):
     return p * int(np.ceil(np.log2(p))) + p + 2 * p * nnu
 
 
+def load_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            t = json.load(f)
+        g = lambda k: t[k]["dram_read_bytes"] + t[k]["dram_write_bytes"]
+        return g("gini_merge_kernel"), g("stress_tma_kernel_grad")
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -67,54 +77,60 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region, in-process
+    through NVML (nvidia-ml-py) every 500 ms -- spawning nvidia-smi at 200 ms was
+    measured to slow the distance kernel by ~10% on this box.  Falls back to
+    nvidia-smi when NVML is unavailable."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, device_index=0):
+    def __init__(self, device_index=0, period=0.5):
         self.dev = device_index
-        self.proc = None
+        self.period = period
+        self.samples = []
+        self.max_mhz = None
 
     def __enter__(self):
+        import threading
+
+        self._stop = threading.Event()
+        self._thread = None
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.QUERY}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": getattr(N, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                    "sw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                    "hw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                    "sw_power_cap": getattr(N, "nvmlClocksThrottleReasonSwPowerCap", 0x4)}
+
+            def run():
+                while True:
+                    try:
+                        mhz = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                        r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                        self.samples.append((mhz, [k for k, b in bits.items() if r & b]))
+                    except Exception:
+                        pass
+                    if self._stop.wait(self.period):
+                        return
+
+            self._thread = threading.Thread(target=run, daemon=True)
+            self._thread.start()
+        except Exception:
+            self._thread = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for name, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [m for m, _ in self.samples]
+        reasons = sorted({x for _, rs in self.samples for x in rs})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------------------------------
@@ -328,6 +344,7 @@ def run_engine(args, rank, world, dist):
     my_pairs = npairs  # all ranks together
     achieved = my_pairs * ops_pair / t_dist
     peaks = load_peaks()
+    traffic_dist, traffic_stress = load_traffic()
     stress_bytes = npairs * 4  # one read of the packed fp32 triangle per pass
     pass_time = t_stress / max(1, spasses / max(1, world))
     value = npairs / t_dist
@@ -348,12 +365,12 @@ def run_engine(args, rank, world, dist):
         "stress_passes_per_iter": spasses / max(1, siters),
         "gpu_launches": int(dist_launches + stress_launches),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu.value / 1e12, "unit": "Tops/s",
-                     "frac": achieved / alu.value, "traffic": None,
+                     "frac": achieved / alu.value, "traffic": traffic_dist, "traffic_unit": "bytes/launch (ncu)",
                      "kernel": "gini_merge_kernel", "ops_per_pair": ops_pair,
                      "peak_source": "measured on this GPU by gmds_probe_alu (FFMA + IADD3/LOP3 lane-op rate)"},
         "stress_roofline": {"bound": "hbm", "achieved": stress_bytes / pass_time / 1e9, "peak": peaks.get("hbm_gbs"),
                             "unit": "GB/s", "frac": stress_bytes / pass_time / 1e9 / peaks.get("hbm_gbs", 6446.6),
-                            "traffic": None, "kernel": "stress_pass_kernel (+ reductions, per pass)",
+                            "traffic": traffic_stress, "kernel": "stress_tma_kernel (+ reductions, per pass)",
                             "bytes_per_pass": stress_bytes},
         "clocks": clk.summary(),
         "clocks_stress": clk2.summary(),

@@ -2,6 +2,9 @@
 // preparation (bitmask-sparse rows when X is sparse), kernel and tile-size
 // selection, and the overflow pass.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -22,6 +25,19 @@ void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, cons
                      int nrows, int K, uint16_t* sidx, cudaStream_t st);
 
 namespace {
+
+// GMDS_TRACE=1: host-side phase timings of run_gini on stderr (observability)
+struct Trace {
+  bool on = std::getenv("GMDS_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto t = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gmds] %-22s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t0).count());
+    t0 = t;
+  }
+};
 
 // warp per row: presence masks, running popcounts, per-row nonzero counts
 template <typename T>
@@ -160,9 +176,11 @@ size_t split_smem(int tile, int p, int W, int maxnnz, size_t sz, int nnu, bool s
 
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
               int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag) {
+  Trace tr;
   const std::vector<double> lut = build_lut(static_cast<int>(p), nus, nnu);
   DevBuf<double> dlut(lut.size());
   GMDS_CUDA(cudaMemcpyAsync(dlut.get(), lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  tr.mark("lut", st);
   GiniTileArgs a{};
   a.n = n;
   a.d = static_cast<int>(p);
@@ -184,6 +202,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   }
   const size_t sz = dtype_size(xt);
   RowStore rs = build_rows(dX, xt, n, static_cast<int>(p), st, true);
+  tr.mark("row store", st);
   const bool sparse = rs.density < 0.5;
   auto full_kernel = [&]() {  // the all-keys warp kernel (dense data with large p)
     a.tile = gini_tile_size(static_cast<int>(p), xt, nnu);
@@ -225,12 +244,14 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * ma.s.ovf_cap)));
       DevBuf<unsigned long long> ovf_count(1);
       GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));
+      tr.mark("overflow buffers", st);
       ma.s.ovf_pairs = ovf.get();
       ma.s.ovf_count = ovf_count.get();
       const unsigned mblocks = static_cast<unsigned>(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30));
       launch_gini_merge(ma, dX, xt, dD, ot, msm, mblocks, st);
       count_launch();
       check_launch("gini_merge_kernel");
+      tr.mark("gini_merge_kernel", st);
       unsigned long long novf = 0;
       GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
       GMDS_CUDA(cudaStreamSynchronize(st));
