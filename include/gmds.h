@@ -180,6 +180,12 @@ gmds_status gmds_minimize_stress(const gmds_dmat* D, int32_t q, const gmds_stres
 gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
                          const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
                          double* mean_stress, double* nu_star, double* coords, double* stress);
+/* Fused nu-sweep scorer (the grid sweep of alternating_tune,
+ * tune.cpp:153-157): ks[g] = kruskal_stress(Y, pairwise_matrix(X, gini(grid[g])))
+ * for every grid value from ONE distance pass (one sort per pair serves every
+ * nu; no D_nu is materialised).  Y host n x q column-major. */
+gmds_status gmds_nu_sweep_kruskal(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                                  const double* Y, int32_t q, const double* grid, int32_t m, double* ks);
 gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
                                   int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
                                   double* nu_star, double* coords, double* stress);

@@ -256,13 +256,13 @@ void launch_midrank_t(const double* dv, const T* dX, const int64_t* dpairs, int6
 }
 
 template <typename T, typename TO>
-void launch_gini_t(GiniTileArgs a, const T* dX, TO* dout, cudaStream_t st) {
+void launch_gini_t(GiniTileArgs a, const T* dX, TO* dout, cudaStream_t st, int64_t max_blocks) {
   if (a.d <= 1024) {
     if (a.tile_end <= a.tile_begin) return;
     const size_t panel = (2 * static_cast<size_t>(a.tile) * a.d * sizeof(T) + 15) & ~static_cast<size_t>(15);
     const size_t smem = panel + static_cast<size_t>(a.nnu) * a.tile * (a.tile + 1) * sizeof(double);
     const int64_t ntiles = a.tile_end - a.tile_begin;
-    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ntiles, 1 << 30));
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(ntiles, max_blocks > 0 ? max_blocks : 1 << 30));
     const gmds_dtype xt = sizeof(T) == 4 ? GMDS_F32 : GMDS_F64;
     const gmds_dtype ot = sizeof(TO) == 4 ? GMDS_F32 : GMDS_F64;
     switch (pick_k(a.d)) {
@@ -318,15 +318,16 @@ int gini_tile_size(int d, gmds_dtype xt, int nnu) {
   return tile;
 }
 
-void launch_gini(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, cudaStream_t st) {
+void launch_gini(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, cudaStream_t st,
+                 int64_t max_blocks) {
   if (xt == GMDS_F32 && ot == GMDS_F32)
-    launch_gini_t<float, float>(a, static_cast<const float*>(dX), static_cast<float*>(dout), st);
+    launch_gini_t<float, float>(a, static_cast<const float*>(dX), static_cast<float*>(dout), st, max_blocks);
   else if (xt == GMDS_F32)
-    launch_gini_t<float, double>(a, static_cast<const float*>(dX), static_cast<double*>(dout), st);
+    launch_gini_t<float, double>(a, static_cast<const float*>(dX), static_cast<double*>(dout), st, max_blocks);
   else if (ot == GMDS_F32)
-    launch_gini_t<double, float>(a, static_cast<const double*>(dX), static_cast<float*>(dout), st);
+    launch_gini_t<double, float>(a, static_cast<const double*>(dX), static_cast<float*>(dout), st, max_blocks);
   else
-    launch_gini_t<double, double>(a, static_cast<const double*>(dX), static_cast<double*>(dout), st);
+    launch_gini_t<double, double>(a, static_cast<const double*>(dX), static_cast<double*>(dout), st, max_blocks);
 }
 
 void launch_euclid(const void* dX, gmds_dtype xt, int64_t n, int d, double* dout, cudaStream_t st) {

@@ -256,6 +256,9 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
   const T* gv = static_cast<const T*>(sa.vals);
   const double half_p = 0.5 * static_cast<double>(d);
   const unsigned lt = (1u << lane) - 1u;
+  __shared__ double s_score[2 * kMaxScoreNu];
+  __shared__ double s_red[32 * 8];
+  for (int e = threadIdx.x; e < 2 * kMaxScoreNu; e += blockDim.x) s_score[e] = 0.0;
 
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
@@ -434,33 +437,10 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
       __syncwarp();
     }
     __syncthreads();
-    for (int v = 0; v < a.nnu; ++v) {
-      const double* otv = otile + static_cast<size_t>(v) * tile * tstride;
-      TO* o = out + static_cast<size_t>(v) * a.out_stride;
-      if (a.packed) {
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int r = e / tile, c = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          const double val = otv[r * tstride + c];
-          if (j < a.n && i < j && val >= 0.0) o[packed_offset(i, j, a.nb_packed)] = static_cast<TO>(val);
-        }
-      } else {
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int r = e / tile, c = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          const double val = otv[r * tstride + c];
-          if (j < a.n && i < j && val >= 0.0) o[i * a.n + j] = static_cast<TO>(val);
-        }
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int c = e / tile, r = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          const double val = otv[r * tstride + c];
-          if (j < a.n && i < j && val >= 0.0) o[j * a.n + i] = static_cast<TO>(val);
-        }
-      }
-    }
+    tile_epilogue<TO>(a, otile, tile, tstride, i0, j0, out, s_score, s_red);
     __syncthreads();
   }
+  score_flush(a, s_score);
 }
 
 inline size_t merge_smem(int tile, int W, int maxnnz, size_t sz, int nnu) {

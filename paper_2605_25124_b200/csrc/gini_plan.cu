@@ -175,8 +175,34 @@ size_t split_smem(int tile, int p, int W, int maxnnz, size_t sz, int nnu, bool s
 }  // namespace
 
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
-              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag) {
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score) {
   Trace tr;
+  if (score && (p > 1024 || nnu > kMaxScoreNu)) {  // block path / too many nu: caller falls back
+    score->ok = false;
+    return;
+  }
+  // score mode: persistent grid (per-CTA partials), no D written
+  DevBuf<double> spart;
+  const int64_t score_grid = 148 * 2;
+  auto grid_of = [&](int64_t units_) -> int64_t { return score ? std::min<int64_t>(units_, score_grid) : units_; };
+  auto finish_score = [&](int64_t grid) {
+    if (!score) return;
+    int hflag = 0;
+    GMDS_CUDA(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    std::vector<double> h(static_cast<size_t>(grid) * 2 * nnu);
+    GMDS_CUDA(cudaMemcpyAsync(h.data(), spart.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    score->ok = (hflag & 2) == 0;
+    for (int v = 0; v < nnu; ++v) {
+      double sn = 0.0, sd = 0.0;
+      for (int64_t b = 0; b < grid; ++b) {  // fixed order: deterministic
+        sn += h[(b * nnu + v) * 2];
+        sd += h[(b * nnu + v) * 2 + 1];
+      }
+      score->num[v] = sn;
+      score->den[v] = sd;
+    }
+  };
   const std::vector<double> lut = build_lut(static_cast<int>(p), nus, nnu);
   DevBuf<double> dlut(lut.size());
   GMDS_CUDA(cudaMemcpyAsync(dlut.get(), lut.data(), lut.size() * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -190,6 +216,13 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   a.nb_packed = ceil_div(n, kPT);
   a.out_stride = packed ? packed_elems(n) : n * n;
   a.flag = dflag;
+  if (score) {
+    spart.alloc(static_cast<size_t>(score_grid) * 2 * nnu);
+    GMDS_CUDA(cudaMemsetAsync(spart.get(), 0, spart.n * sizeof(double), st));
+    a.Y = score->dY;
+    a.q = score->q;
+    a.score_part = spart.get();
+  }
   if (p > 1024) {  // CTA-per-pair block sort
     a.tile = 1;
     a.nbt = n;
@@ -210,7 +243,8 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
     a.tile_begin = units * shard / nshards;
     a.tile_end = units * (shard + 1) / nshards;
-    launch_gini(a, dX, xt, dD, ot, st);
+    launch_gini(a, dX, xt, dD, ot, st, score ? score_grid : 0);
+    finish_score(score ? std::min<int64_t>(a.tile_end - a.tile_begin, score_grid) : 0);
   };
   if (!sparse && p > 512) {
     full_kernel();
@@ -247,7 +281,9 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       tr.mark("overflow buffers", st);
       ma.s.ovf_pairs = ovf.get();
       ma.s.ovf_count = ovf_count.get();
-      const unsigned mblocks = static_cast<unsigned>(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30));
+      const unsigned mblocks =
+          static_cast<unsigned>(grid_of(std::min<int64_t>(a.tile_end - a.tile_begin, int64_t(1) << 30)));
+      ma.s.g = a;
       launch_gini_merge(ma, dX, xt, dD, ot, msm, mblocks, st);
       count_launch();
       check_launch("gini_merge_kernel");
@@ -255,7 +291,8 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       unsigned long long novf = 0;
       GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
       GMDS_CUDA(cudaStreamSynchronize(st));
-      if (novf == 0) return;
+      finish_score(mblocks);
+      if (novf == 0 || score) return;
       if (static_cast<int64_t>(novf) > ma.s.ovf_cap) {
         full_kernel();
       } else {
@@ -301,7 +338,8 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));
   sa.ovf_pairs = ovf.get();
   sa.ovf_count = ovf_count.get();
-  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30));
+  const unsigned blocks = static_cast<unsigned>(grid_of(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30)));
+  sa.g = a;
   if (p <= 256)
     launch_gini_split<8>(sa, dX, xt, dD, ot, smem, blocks, st);
   else
@@ -311,7 +349,8 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   unsigned long long novf = 0;
   GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
-  if (novf == 0) return;
+  finish_score(blocks);
+  if (novf == 0 || score) return;
   if (static_cast<int64_t>(novf) > sa.ovf_cap) {  // list too long: redo these tiles with the all-keys kernel
     full_kernel();
     GMDS_CUDA(cudaStreamSynchronize(st));

@@ -267,6 +267,9 @@ __global__ void __launch_bounds__(256, 2) gini_split_kernel(SplitArgs sa, const 
   const T* sv = static_cast<const T*>(sa.vals);
   const double half_p = 0.5 * static_cast<double>(d);
   const unsigned lt = (1u << lane) - 1u;
+  __shared__ double s_score[2 * kMaxScoreNu];
+  __shared__ double s_red[32 * 8];
+  for (int e = threadIdx.x; e < 2 * kMaxScoreNu; e += blockDim.x) s_score[e] = 0.0;
 
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
@@ -372,33 +375,10 @@ __global__ void __launch_bounds__(256, 2) gini_split_kernel(SplitArgs sa, const 
       __syncwarp();  // scratch reuse
     }
     __syncthreads();
-    for (int v = 0; v < a.nnu; ++v) {
-      const double* ot = otile + static_cast<size_t>(v) * tile * tstride;
-      TO* o = out + static_cast<size_t>(v) * a.out_stride;
-      if (a.packed) {
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int r = e / tile, c = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          const double val = ot[r * tstride + c];
-          if (j < a.n && i < j && val >= 0.0) o[packed_offset(i, j, a.nb_packed)] = static_cast<TO>(val);
-        }
-      } else {
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int r = e / tile, c = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          const double val = ot[r * tstride + c];
-          if (j < a.n && i < j && val >= 0.0) o[i * a.n + j] = static_cast<TO>(val);
-        }
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int c = e / tile, r = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          const double val = ot[r * tstride + c];
-          if (j < a.n && i < j && val >= 0.0) o[j * a.n + i] = static_cast<TO>(val);
-        }
-      }
-    }
+    tile_epilogue<TO>(a, otile, tile, tstride, i0, j0, out, s_score, s_red);
     __syncthreads();
   }
+  score_flush(a, s_score);
 }
 
 template <int KMAX>

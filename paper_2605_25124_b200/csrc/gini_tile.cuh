@@ -35,6 +35,94 @@ __device__ __forceinline__ void decode_tile(int64_t t, int64_t nbt, int64_t& I, 
 }  // namespace gini_detail
 using namespace gini_detail;
 
+__host__ __device__ int64_t packed_offset(int64_t i, int64_t j, int64_t nb);
+
+// Tile epilogue shared by the tile / split / merge kernels.  Store mode:
+// otile (per nu, tile x (tile+1)) written coalesced to the full n x n image
+// (both triangles) or the packed triangle; negative values mark pairs the
+// overflow pass fills.  Score mode: per-nu sums of (dist - D)^2 and D^2,
+// reduced in a fixed order (warp xor-trees, then warp partials in order)
+// into the CTA accumulator sacc[2 nu].
+template <typename TO>
+__device__ __forceinline__ void tile_epilogue(const GiniTileArgs& a, const double* otile, int tile, int tstride,
+                                              int64_t i0, int64_t j0, TO* out, double* sacc, double* sred) {
+  if (a.Y == nullptr) {
+    for (int v = 0; v < a.nnu; ++v) {
+      const double* ot = otile + static_cast<size_t>(v) * tile * tstride;
+      TO* o = out + static_cast<size_t>(v) * a.out_stride;
+      if (a.packed) {
+        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
+          const int r = e / tile, c = e % tile;
+          const int64_t i = i0 + r, j = j0 + c;
+          const double val = ot[r * tstride + c];
+          if (j < a.n && i < j && val >= 0.0) o[packed_offset(i, j, a.nb_packed)] = static_cast<TO>(val);
+        }
+      } else {
+        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
+          const int r = e / tile, c = e % tile;
+          const int64_t i = i0 + r, j = j0 + c;
+          const double val = ot[r * tstride + c];
+          if (j < a.n && i < j && val >= 0.0) o[i * a.n + j] = static_cast<TO>(val);
+        }
+        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
+          const int c = e / tile, r = e % tile;
+          const int64_t i = i0 + r, j = j0 + c;
+          const double val = ot[r * tstride + c];
+          if (j < a.n && i < j && val >= 0.0) o[j * a.n + i] = static_cast<TO>(val);
+        }
+      }
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int v0 = 0; v0 < a.nnu; v0 += 4) {
+    const int nv = min(4, a.nnu - v0);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
+      const int r = e / tile, c = e % tile;
+      const int64_t i = i0 + r, j = j0 + c;
+      if (!(j < a.n && i < j)) continue;
+      double d2 = 0.0;  // embedded_distance (embed.cpp:32-34)
+      for (int k = 0; k < a.q; ++k) {
+        const double dy = a.Y[i * a.q + k] - a.Y[j * a.q + k];
+        d2 += dy * dy;
+      }
+      const double dist = sqrt(d2);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        if (v >= nv) break;
+        const double Dv = otile[(static_cast<size_t>(v0 + v) * tile + r) * tstride + c];
+        if (Dv < 0.0) atomicOr(a.flag, 2);  // overflow pair: not computed here
+        const double ee = dist - Dv;
+        acc[2 * v] += ee * ee;
+        acc[2 * v + 1] += Dv * Dv;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double x = acc[k];
+#pragma unroll
+      for (int dd = 16; dd > 0; dd >>= 1) x += __shfl_xor_sync(0xffffffffu, x, dd);
+      if (lane == 0) sred[warp * 8 + k] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * nv) {
+      double t = 0.0;
+      for (int w = 0; w < nwarps; ++w) t += sred[w * 8 + threadIdx.x];
+      sacc[2 * v0 + threadIdx.x] += t;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void score_flush(const GiniTileArgs& a, const double* sacc) {
+  if (a.Y == nullptr) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2 * a.nnu; e += blockDim.x)
+    a.score_part[static_cast<size_t>(blockIdx.x) * 2 * a.nnu + e] = sacc[e];
+}
+
+
 // ---------------------------------------------------------------------------
 // K1: segmented midrank, warp per segment (segment length d <= 32*K).
 
@@ -90,6 +178,9 @@ __global__ void __launch_bounds__(256) gini_tile_kernel(GiniTileArgs a, const T*
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
   const double half_p = 0.5 * static_cast<double>(d);
+  __shared__ double s_score[2 * kMaxScoreNu];
+  __shared__ double s_red[32 * 8];
+  for (int e = threadIdx.x; e < 2 * kMaxScoreNu; e += blockDim.x) s_score[e] = 0.0;
 
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
@@ -143,34 +234,10 @@ __global__ void __launch_bounds__(256) gini_tile_kernel(GiniTileArgs a, const T*
       }
     }
     __syncthreads();
-    // write-out
-    for (int v = 0; v < a.nnu; ++v) {
-      const double* ot = otile + static_cast<size_t>(v) * tile * tstride;
-      if (a.packed) {
-        TO* o = out + static_cast<size_t>(v) * a.out_stride;
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int r = e / tile, c = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          if (j < a.n && i < j) o[packed_offset(i, j, a.nb_packed)] = static_cast<TO>(ot[r * tstride + c]);
-        }
-      } else {
-        TO* o = out + static_cast<size_t>(v) * a.out_stride;
-        // rows (i, j): j fastest
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int r = e / tile, c = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          if (j < a.n && i < j) o[i * a.n + j] = static_cast<TO>(ot[r * tstride + c]);
-        }
-        // mirror (j, i): i fastest
-        for (int e = threadIdx.x; e < tile * tile; e += blockDim.x) {
-          const int c = e / tile, r = e % tile;
-          const int64_t i = i0 + r, j = j0 + c;
-          if (j < a.n && i < j) o[j * a.n + i] = static_cast<TO>(ot[r * tstride + c]);
-        }
-      }
-    }
+    tile_epilogue<TO>(a, otile, tile, tstride, i0, j0, out, s_score, s_red);
     __syncthreads();
   }
+  score_flush(a, s_score);
 }
 
 

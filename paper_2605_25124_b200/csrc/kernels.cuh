@@ -28,8 +28,16 @@ struct GiniTileArgs {
   int packed;          // 0: full n x n per nu; 1: packed tile image per nu
   int64_t nb_packed;   // ceil(n / kPT)
   int64_t out_stride;  // elements between consecutive nu outputs
-  int* flag;           // device: bit0 = non-finite distance produced
+  int* flag;           // device: bit0 = non-finite distance produced, bit1 = pair not scored
+  // score mode (fused nu-sweep scorer): instead of storing D_nu, accumulate
+  // sum (|y_i - y_j| - D_nu)^2 and sum D_nu^2 for every nu (kruskal_stress of
+  // a fixed embedding against every grid value).
+  const double* Y;     // n x q row-major fp64 (nullptr: store mode)
+  int q;
+  double* score_part;  // [gridDim][nnu][2] per-CTA partials (fixed-order sums)
 };
+
+constexpr int kMaxScoreNu = 64;
 
 void count_launch(int64_t k = 1);
 int64_t launch_count();
@@ -37,7 +45,8 @@ int64_t launch_count();
 int gini_tile_size(int d, gmds_dtype xt, int nnu);
 void launch_midrank(const double* dv, const void* dX, gmds_dtype xt, const int64_t* dpairs, int64_t nseg, int d,
                     double* dranks, cudaStream_t st);
-void launch_gini(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, cudaStream_t st);
+void launch_gini(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, cudaStream_t st,
+                 int64_t max_blocks = 0);
 void launch_euclid(const void* dX, gmds_dtype xt, int64_t n, int d, double* dout, cudaStream_t st);
 void launch_transpose(const void* din, gmds_dtype t, int64_t rows, int64_t cols, void* dout, cudaStream_t st);
 

@@ -24,8 +24,18 @@ void check_finite_host(const void* X, gmds_dtype xt, int64_t count, const char* 
 std::vector<double> build_lut(int d, const double* nus, int nnu);
 DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
                                   cudaStream_t st);
+// Fused nu-sweep scoring request: instead of storing D_nu, return per nu
+// num = sum (|y_i - y_j| - D_nu)^2 and den = sum D_nu^2 over i < j (host arrays).
+struct ScoreSpec {
+  const double* dY = nullptr;  // n x q row-major fp64, device
+  int q = 0;
+  double* num = nullptr;
+  double* den = nullptr;
+  bool ok = false;  // out: false when a pair needed the overflow path (caller falls back)
+};
+
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
-              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag);
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score = nullptr);
 void check_flag(int* dflag, cudaStream_t st);
 
 }  // namespace gmds

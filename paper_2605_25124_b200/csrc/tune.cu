@@ -140,6 +140,40 @@ std::vector<double> rows_of(const void* X, gmds_dtype xt, gmds_layout lx, int64_
   return out;
 }
 
+// kruskal_stress(Y, D_nu) for every grid nu from ONE distance pass (SURVEY
+// 8f-1): the distance kernels run in score mode and never store D_nu.  Falls
+// back to materialised matrices when a pair needs the overflow path.
+void sweep_kruskal(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* grid, int m,
+                   const double* coords_colmajor, int q, cudaStream_t st, double* ks) {
+  std::vector<double> Yr(static_cast<size_t>(n) * q);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < q; ++k) Yr[i * q + k] = coords_colmajor[k * n + i];
+  DevBuf<double> dY(Yr.size());
+  GMDS_CUDA(cudaMemcpyAsync(dY.get(), Yr.data(), Yr.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+  std::vector<double> num(static_cast<size_t>(m)), den(static_cast<size_t>(m));
+  ScoreSpec sc;
+  sc.dY = dY.get();
+  sc.q = q;
+  sc.num = num.data();
+  sc.den = den.data();
+  DevBuf<int> flag(1);
+  GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
+  run_gini(dX, xt, n, p, grid, m, GMDS_F64, 1, nullptr, 0, 1, st, flag.get(), &sc);
+  if (sc.ok) {
+    int hflag = 0;
+    GMDS_CUDA(cudaMemcpyAsync(&hflag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    if (hflag & 1) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
+    for (int g = 0; g < m; ++g) {
+      if (den[g] <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
+      ks[g] = std::sqrt(num[g] / den[g]);
+    }
+    return;
+  }
+  const auto Ds = gini_multi(dX, xt, n, p, grid, m, st);
+  for (int g = 0; g < m; ++g) ks[g] = kruskal_of(Ds[g].get(), coords_colmajor, q, st);
+}
+
 DevBuf<double> upload_f64(const std::vector<double>& h, cudaStream_t st) {
   DevBuf<double> d(h.size());
   GMDS_CUDA(cudaMemcpyAsync(d.get(), h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -206,6 +240,23 @@ gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n
   });
 }
 
+gmds_status gmds_nu_sweep_kruskal(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
+                                  const double* Y, int32_t q, const double* grid, int32_t m, double* ks) {
+  return guard([&] {
+    check_grid(grid, m);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    if (q < 1) fail(GMDS_INVALID_INPUT, "kruskal_stress: coords have no columns");
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    for (int64_t k = 0; k < n * q; ++k)
+      if (!std::isfinite(Y[k])) fail(GMDS_INVALID_INPUT, "kruskal_stress: non-finite coordinates");
+    require_device();
+    Stream st;
+    DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
+    sweep_kruskal(dX.get(), xt, n, p, grid, m, Y, q, st.s, ks);
+  });
+}
+
 gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
                                   int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
                                   double* nu_star, double* coords, double* stress) {
@@ -220,16 +271,15 @@ gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, 
     std::vector<int> all(static_cast<size_t>(n));
     std::iota(all.begin(), all.end(), 0);
     DevBuf<double> dX = upload_f64(rows_of(X, xt, lx, n, p, all), st.s);
-    // every grid value's D from one sort per pair, reused by all outer iterations
-    const auto Dgrid = gini_multi(dX.get(), GMDS_F64, n, p, grid, m, st.s);
     double nu = 2.0;
     Emb emb;
     for (int t = 0; t < outer_iters; ++t) {
       const auto D = gini_multi(dX.get(), GMDS_F64, n, p, &nu, 1, st.s);
       emb = embed(D[0].get(), q, GMDS_M_SAMMON, seed, st.s);
+      // grid sweep: every grid nu scored against the current embedding in one pass (no D_nu stored)
       int best = 0;
       std::vector<double> sweep(static_cast<size_t>(m));
-      for (int g = 0; g < m; ++g) sweep[g] = kruskal_of(Dgrid[g].get(), emb.coords.data(), q, st.s);
+      sweep_kruskal(dX.get(), GMDS_F64, n, p, grid, m, emb.coords.data(), q, st.s, sweep.data());
       for (int g = 1; g < m; ++g)
         if (sweep[g] < sweep[best]) best = g;
       nu = grid[best];

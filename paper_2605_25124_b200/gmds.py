@@ -435,3 +435,15 @@ def double_center(S) -> np.ndarray:
     out = np.zeros_like(S, order="F")
     _check(lib().gmds_double_center(_p(S), _i64(S.shape[0]), _p(out)))
     return np.ascontiguousarray(out)
+
+
+def nu_sweep_kruskal(X, Y, grid) -> np.ndarray:
+    """kruskal_stress(Y, pairwise_matrix(X, gini(nu))) for every grid nu, one distance pass."""
+    X, xt, lx = _xarg(X)
+    n, p = X.shape
+    Y = _coords(Y)
+    g = np.ascontiguousarray(np.asarray(grid, dtype=np.float64))
+    out = np.zeros(g.size)
+    _check(lib().gmds_nu_sweep_kruskal(_vp(X), _i32(xt), _i32(lx), _i64(n), _i64(p), _p(Y), _i32(Y.shape[1]), _p(g),
+                                       _i32(g.size), _p(out)))
+    return out
