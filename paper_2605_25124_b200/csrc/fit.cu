@@ -35,7 +35,6 @@ namespace {
 
 constexpr int64_t kChunk = 4;
 constexpr double kTiny = 1e-300;  // embed.cpp:13
-constexpr bool kFusedTrials = false;
 
 int padded_q(int q) { return q <= 4 ? q : q; }
 
@@ -65,11 +64,10 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
     GMDS_CUDA(cudaMemcpyAsync(chunk_J0.get(), cJ.data(), cJ.size() * 8, cudaMemcpyHostToDevice, st));
     GMDS_CUDA(cudaMemcpyAsync(strip_first.get(), sf.data(), sf.size() * 8, cudaMemcpyHostToDevice, st));
     const int64_t nblk = nb * (nb + 1) / 2;
-    gcand = (D->storage == GMDS_F32) ? kTmaCands : 1;  // fp32 passes can carry two trial gradients
     stride_row = nchunks * kPT * Q;
     stride_col = nblk * kPT * Q;
-    rowpart.alloc(static_cast<size_t>(stride_row * gcand));
-    colpart.alloc(static_cast<size_t>(stride_col * gcand));
+    rowpart.alloc(static_cast<size_t>(stride_row));
+    colpart.alloc(static_cast<size_t>(stride_col));
     losspart.alloc(static_cast<size_t>(nchunks * kMaxCand));
   } else {
     nchunks = n;
@@ -119,26 +117,6 @@ PassArgs Engine::args(int kind, double delta) const {
   a.cand_stride_row = stride_row;
   a.cand_stride_col = stride_col;
   return a;
-}
-
-// One pass: losses AND gradient partials at nc <= gcand trial points (fp32 D).
-std::vector<double> Engine::fused_trials(int kind, double delta, const double* const* Ys, int nc) {
-  PassArgs a = args(kind, delta);
-  for (int c = 0; c < nc; ++c) a.Y[c] = Ys[c];
-  a.ncand = nc;
-  launch_stress_pass(a, Q, true, D->storage, st);
-  launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
-  std::vector<double> out(static_cast<size_t>(nc));
-  GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
-  GMDS_CUDA(cudaStreamSynchronize(st));
-  ++passes;
-  return out;
-}
-
-// graw <- reduced gradient of trial point c of the last fused pass
-void Engine::reduce_candidate(int c) {
-  launch_reduce_rows(rowpart.get() + c * stride_row, colpart.get() + c * stride_col, strip_first.get(), n, nb, Q,
-                     graw.get(), st);
 }
 
 std::vector<double> Engine::loss_raw(int kind, double delta, const double* const* Ys, int nc) {
@@ -346,11 +324,9 @@ struct IterResult {
 IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double rel_tol) {
   IterResult r;
   const int kind = rp.kind;
-  // Fused trial gradients are implemented (fused_trials / reduce_candidate) but
-  // measured slower on B200 than a separate gradient pass (one 2-candidate
-  // GRAD pass: 800 us vs 333 + 239 us for the two passes at n = 20000; the
-  // per-row shuffle trees double with the candidates), so they stay off.
-  const bool fused = kFusedTrials && (E.gcand >= 2) && !E.rows_mode;
+  // (A variant carrying both trial gradients in the trial pass was measured at
+  // 800 us per pass vs 333 + 239 us for separate gradient and loss passes at
+  // n = 20000, so trial passes compute losses only.)
   double* Yc[kMaxCand];
   // f = loss_value(coords) and the first gradient come from one pass
   double raw = E.grad_raw(kind, rp.delta, E.Y.get());
@@ -392,9 +368,7 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
       }
       for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();  // buffers rotate on acceptance
       launch_axpy_cand(E.Y.get(), E.graw.get(), E.n * E.Q, s, Yc, E.st);
-      const bool with_grad = fused && first;
-      const std::vector<double> raws =
-          with_grad ? E.fused_trials(kind, rp.delta, Yc, s.n) : E.loss_raw(kind, rp.delta, Yc, s.n);
+      const std::vector<double> raws = E.loss_raw(kind, rp.delta, Yc, s.n);
       for (int c = 0; c < s.n; ++c) {
         const double fc = E.loss_of(kind, raws[c]);
         if (fc <= f - armijo * s.v[c] * grad_sq) {
@@ -402,11 +376,6 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
           acc_c = c;
           f_new = fc;
           step = s.v[c];
-          if (with_grad) {
-            E.reduce_candidate(c);  // gradient at the accepted point, same pass
-            raw = raws[c];
-            have_grad = true;
-          }
           break;
         }
       }

@@ -19,7 +19,6 @@ struct Engine {
   cudaStream_t st;
   int64_t n = 0, nb = 0, nchunks = 0;
   int64_t passes = 0;  // passes over D issued by this engine
-  int gcand = 1;        // trial points a GRAD pass can carry (2 with fp32 D)
   int64_t stride_row = 0, stride_col = 0;
   const void* W = nullptr;
   DevBuf<int64_t> chunk_I, chunk_J0, strip_first;
@@ -34,9 +33,6 @@ struct Engine {
   std::vector<double> loss_raw(int kind, double delta, const double* const* Ys, int nc);
   // raw gradient sums into graw, returns the raw loss at Yd (one pass)
   double grad_raw(int kind, double delta, const double* Yd);
-  // losses + gradient partials at nc trial points (one pass); reduce_candidate picks one
-  std::vector<double> fused_trials(int kind, double delta, const double* const* Ys, int nc);
-  void reduce_candidate(int c);
   // raw sums over one shard's chunks (sharded fits; summed across ranks)
   double grad_raw_shard(int kind, double delta, const double* Yd, int shard, int nshards);
   // graw *= scale, returns |graw|^2

@@ -89,15 +89,15 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 template <int Q, bool GRAD, int KIND>
 __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
-  constexpr int NCM = kTmaCand;  // GRAD passes may carry the gradient of both Armijo trial points
+  // loss passes carry two Armijo trial points; gradient passes one point
+  constexpr int NCM = GRAD ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
-  float* ring = reinterpret_cast<float*>(dyn);  // [kStages][kHalfFloats]
+  float* ring = reinterpret_cast<float*>(dyn);  // [kStages = 2][kHalfFloats]: stage == half
   __shared__ __align__(8) uint64_t bars[kStages];
   __shared__ float sYi[NCM][kPT][Q];
   __shared__ float sYj[NCM][kPT][Q];  // [yslot(r)]
-  __shared__ double sRed[GRAD ? kTG * kPT : 1];
+  __shared__ float sRed[GRAD ? kTG * kPT : 1];
   __shared__ double sLoss[kThreads / 32][kMaxCand];
-  __shared__ double sRowTot[GRAD ? NCM * kPT * Q : 1];
 
   const int tid = threadIdx.x;
   const int ti = tid / kTG, tj = tid % kTG;
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   const int64_t J1 = min(J0 + a.chunk_len, a.nb);
   const int nblocks = static_cast<int>(J1 - J0);
   const int nhalves = 2 * nblocks;
-  const int nc = a.ncand;
+  const int nc = GRAD ? 1 : a.ncand;
   const float* __restrict__ D = static_cast<const float*>(a.D);
   const float* __restrict__ W = static_cast<const float*>(a.W);
   const float delta = static_cast<float>(a.huber_delta);
@@ -120,9 +120,9 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   auto issue = [&](int h) {
     const int64_t J = J0 + h / 2;
     const float* src = D + blk_index(I, J, a.nb) * (kPT * kPT) + (h & 1) * kHalfFloats;
-    uint64_t* bar = &bars[h % kStages];
+    uint64_t* bar = &bars[h & 1];
     mbar_expect_tx(bar, kHalfFloats * 4);
-    bulk_g2s(ring + (h % kStages) * kHalfFloats, src, kHalfFloats * 4, bar);
+    bulk_g2s(ring + (h & 1) * kHalfFloats, src, kHalfFloats * 4, bar);
   };
   if (tid == 0)
     for (int h = 0; h < min(kStages, nhalves); ++h) issue(h);
@@ -132,155 +132,146 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
     const int64_t i = I * kPT + r;
     sYi[c][r][k] = (i < a.n) ? static_cast<float>(a.Y[c][i * Q + k]) : 0.f;
   }
-  if constexpr (GRAD) {
-    for (int e = tid; e < NCM * kPT * Q; e += kThreads) sRowTot[e] = 0.0;
-  }
   double lossacc[NCM];
 #pragma unroll
   for (int c = 0; c < NCM; ++c) lossacc[c] = 0.0;
-  float colacc[GRAD ? NCM : 1][GRAD ? kMT : 1][Q];
+  // GRAD: this thread's 8 rows (4 per half) accumulate over every block of the
+  // chunk in registers and are reduced across the 16 tj-threads once per chunk
+  float rowsum[GRAD ? 2 : 1][GRAD ? kMR : 1][Q];
+  if constexpr (GRAD) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int x = 0; x < kMR; ++x)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) rowsum[hh][x][k] = 0.f;
+  }
   float yj[NCM][kMT][Q];  // this thread's 8 columns, loaded once per block
 
-  for (int h = 0; h < nhalves; ++h) {
-    const int64_t J = J0 + h / 2;
-    const int half = h & 1;
-    if (half == 0) {
-      __syncthreads();  // sYj / sRed of the previous block are consumed
-      for (int e = tid; e < nc * kPT * Q; e += kThreads) {
-        const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
-        const int64_t j = J * kPT + r;
-        sYj[c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
-      }
-      if constexpr (GRAD) {
+  for (int b = 0; b < nblocks; ++b) {
+    const int64_t J = J0 + b;
+    __syncthreads();  // sYj / sRed of the previous block are consumed
+    for (int e = tid; e < nc * kPT * Q; e += kThreads) {
+      const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
+      const int64_t j = J * kPT + r;
+      sYj[c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < NCM; ++c)
+#pragma unroll
+      for (int y = 0; y < kMT; ++y)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) yj[c][y][k] = (c < nc) ? sYj[c][y * kTG + tj][k] : 0.f;
+    float colacc[GRAD ? kMT : 1][Q];
+    if constexpr (GRAD) {
+#pragma unroll
+      for (int y = 0; y < kMT; ++y)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) colacc[y][k] = 0.f;
+    }
+    const int64_t blk = blk_index(I, J, a.nb);
+    const bool edge = (I == J) || (J * kPT + kPT > a.n);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int h = 2 * b + half;
+      mbar_wait(&bars[half], static_cast<uint32_t>(b & 1));
+      const float* Ds = ring + half * kHalfFloats;
+      const float* Wb = W ? W + blk * (kPT * kPT) + half * kHalfFloats : nullptr;
+#pragma unroll
+      for (int x = 0; x < kMR; ++x) {
+        const int rloc = ti * kMR + x;           // row within the half
+        const int ri = half * kHalfRows + rloc;  // row within the block
+        const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT);
+        const float4 v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT + 4);
+        const float dv[kMT] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        float wv[kMT];
+#pragma unroll
+        for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tj * kMT + y] : 1.f;
+        float lossrow[NCM];
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) lossrow[c] = 0.f;
+        float yi[NCM][Q];
 #pragma unroll
         for (int c = 0; c < NCM; ++c)
 #pragma unroll
-          for (int y = 0; y < kMT; ++y)
+          for (int k = 0; k < Q; ++k) yi[c][k] = (c < nc) ? sYi[c][ri][k] : 0.f;
+        // interior blocks: no masks at all; edge blocks (diagonal / last column block) mask per pair
+        auto pairs = [&](auto edge_tag) {
+          constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
-            for (int k = 0; k < Q; ++k) colacc[c][y][k] = 0.f;
-      }
-      __syncthreads();
+          for (int y = 0; y < kMT; ++y) {
+            const int rj = tj * kMT + y;
+            bool keep = true;
+            if constexpr (EDGE) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
+            const float Dv = dv[y];
+            const float invD = (KIND == kSammon) ? 1.f / fmaxf(Dv, FLT_MIN) : 0.f;
 #pragma unroll
-      for (int c = 0; c < NCM; ++c)
-#pragma unroll
-        for (int y = 0; y < kMT; ++y)
-#pragma unroll
-          for (int k = 0; k < Q; ++k) yj[c][y][k] = (c < nc) ? sYj[c][y * kTG + tj][k] : 0.f;
-    }
-    mbar_wait(&bars[h % kStages], static_cast<uint32_t>((h / kStages) & 1));
-    const float* Ds = ring + (h % kStages) * kHalfFloats;
-    const int64_t blk = blk_index(I, J, a.nb);
-    const float* Wb = W ? W + blk * (kPT * kPT) + half * kHalfFloats : nullptr;
-    const bool edge = (I == J) || (J * kPT + kPT > a.n);
-#pragma unroll 1
-    for (int x = 0; x < kMR; ++x) {
-      const int rloc = ti * kMR + x;           // row within the half
-      const int ri = half * kHalfRows + rloc;  // row within the block
-      const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT);
-      const float4 v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT + 4);
-      const float dv[kMT] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      float wv[kMT];
-#pragma unroll
-      for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tj * kMT + y] : 1.f;
-      float rowacc[GRAD ? NCM : 1][Q];
-#pragma unroll
-      for (int c = 0; c < (GRAD ? NCM : 1); ++c)
-#pragma unroll
-        for (int k = 0; k < Q; ++k) rowacc[c][k] = 0.f;
-      float lossrow[NCM];
-#pragma unroll
-      for (int c = 0; c < NCM; ++c) lossrow[c] = 0.f;
-      float yi[NCM][Q];
-#pragma unroll
-      for (int c = 0; c < NCM; ++c)
-#pragma unroll
-        for (int k = 0; k < Q; ++k) yi[c][k] = (c < nc) ? sYi[c][ri][k] : 0.f;
-      // interior blocks: no masks at all; edge blocks (diagonal / last column block) mask per pair
-      auto pairs = [&](auto edge_tag) {
-        constexpr bool EDGE = decltype(edge_tag)::value;
-#pragma unroll
-        for (int y = 0; y < kMT; ++y) {
-          const int rj = tj * kMT + y;
-          bool keep = true;
-          if constexpr (EDGE) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
-          const float Dv = dv[y];
-          const float invD = (KIND == kSammon) ? 1.f / fmaxf(Dv, FLT_MIN) : 0.f;
-#pragma unroll
-          for (int c = 0; c < NCM; ++c) {
-            if (c >= nc) break;
-            float dy[Q];
-            float d2 = 0.f;
-#pragma unroll
-            for (int k = 0; k < Q; ++k) {
-              dy[k] = yi[c][k] - yj[c][y][k];
-              d2 = fmaf(dy[k], dy[k], d2);
-            }
-            const float inv = rsqrtf(fmaxf(d2, FLT_MIN));
-            const float dist = d2 * inv;
-            float term, cc;
-            kind_terms<KIND>(Dv, invD, dist, inv, wv[y], delta, term, cc);
-            if constexpr (EDGE) {
-              term = keep ? term : 0.f;
-              cc = keep ? cc : 0.f;
-            }
-            lossrow[c] += term;
-            if constexpr (GRAD) {
+            for (int c = 0; c < NCM; ++c) {
+              if (c >= nc) break;
+              float dy[Q];
+              float d2 = 0.f;
 #pragma unroll
               for (int k = 0; k < Q; ++k) {
-                rowacc[c][k] = fmaf(cc, dy[k], rowacc[c][k]);
-                colacc[c][y][k] = fmaf(-cc, dy[k], colacc[c][y][k]);
+                dy[k] = yi[c][k] - yj[c][y][k];
+                d2 = fmaf(dy[k], dy[k], d2);
+              }
+              const float inv = rsqrtf(fmaxf(d2, FLT_MIN));
+              const float dist = d2 * inv;
+              float term, cc;
+              kind_terms<KIND>(Dv, invD, dist, inv, wv[y], delta, term, cc);
+              if constexpr (EDGE) {
+                term = keep ? term : 0.f;
+                cc = keep ? cc : 0.f;
+              }
+              lossrow[c] += term;
+              if constexpr (GRAD) {
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                  rowsum[half][x][k] = fmaf(cc, dy[k], rowsum[half][x][k]);
+                  colacc[y][k] = fmaf(-cc, dy[k], colacc[y][k]);
+                }
               }
             }
           }
-        }
-      };
-      if (edge)
-        pairs(std::true_type{});
-      else
-        pairs(std::false_type{});
+        };
+        if (edge)
+          pairs(std::true_type{});
+        else
+          pairs(std::false_type{});
 #pragma unroll
-      for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
-      if constexpr (GRAD) {
+        for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
+      }
+      __syncthreads();  // stage `half` is free
+      if (tid == 0 && h + kStages < nhalves) issue(h + kStages);
+    }
+    if constexpr (GRAD) {  // column partials of block J: 16 ti-threads per column, fixed order
 #pragma unroll
-        for (int c = 0; c < NCM; ++c) {
-          if (c >= nc) break;
+      for (int k = 0; k < Q; ++k) {
+        if (k > 0) __syncthreads();
 #pragma unroll
-          for (int k = 0; k < Q; ++k) {
-            double v = static_cast<double>(rowacc[c][k]);
-#pragma unroll
-            for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-            if (tj == 0) sRowTot[(c * kPT + ri) * Q + k] += v;
-          }
+        for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = colacc[y][k];
+        __syncthreads();
+        if (tid < kPT) {
+          float s = 0.f;
+          for (int t = 0; t < kTG; ++t) s += sRed[t * kPT + tid];
+          a.colpart[(blk * kPT + tid) * Q + k] = static_cast<double>(s);
         }
       }
     }
-    if constexpr (GRAD) {
-      if (half == 1) {  // column partials of block J (rows ti*4.. of both halves), per candidate
-#pragma unroll
-        for (int c = 0; c < NCM; ++c) {
-          if (c >= nc) break;
-#pragma unroll
-          for (int k = 0; k < Q; ++k) {
-            __syncthreads();
-#pragma unroll
-            for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = static_cast<double>(colacc[c][y][k]);
-            __syncthreads();
-            if (tid < kPT) {
-              double s = 0.0;
-              for (int t = 0; t < kTG; ++t) s += sRed[t * kPT + tid];
-              a.colpart[c * a.cand_stride_col + (blk * kPT + tid) * Q + k] = s;
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();  // stage h % kStages is free
-    if (tid == 0 && h + kStages < nhalves) issue(h + kStages);
   }
-  if constexpr (GRAD) {
-    __syncthreads();
-    for (int e = tid; e < nc * kPT * Q; e += kThreads)
-      a.rowpart[(e / (kPT * Q)) * a.cand_stride_row + chunk * (kPT * Q) + e % (kPT * Q)] = sRowTot[e];
+  if constexpr (GRAD) {  // row partials of the chunk: xor-trees over the 16 tj-threads of each row
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int x = 0; x < kMR; ++x)
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          float v = rowsum[hh][x][k];
+#pragma unroll
+          for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+          if (tj == 0) a.rowpart[(chunk * kPT + hh * kHalfRows + ti * kMR + x) * Q + k] = static_cast<double>(v);
+        }
   }
 #pragma unroll
   for (int c = 0; c < NCM; ++c) {
