@@ -24,7 +24,7 @@ void launch_gini_merge(const MergeArgs& ma, const void* dX, gmds_dtype xt, void*
 template <int K, typename T>
 __global__ void row_sort_kernel(const T* __restrict__ vals, const uint16_t* __restrict__ fidx,
                                 const int64_t* __restrict__ rowptr, const int* __restrict__ rows, int nrows,
-                                uint16_t* __restrict__ sidx) {
+                                uint16_t* __restrict__ sidx, T* __restrict__ svs) {
   const int lane = threadIdx.x & 31;
   for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nrows; q += (gridDim.x * blockDim.x) >> 5) {
     const int64_t row = rows[q];
@@ -42,21 +42,24 @@ __global__ void row_sort_kernel(const T* __restrict__ vals, const uint16_t* __re
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       const int g = lane * K + r;
-      if (g < cnt) sidx[b + g] = static_cast<uint16_t>(idx[r]);
+      if (g < cnt) {
+        sidx[b + g] = static_cast<uint16_t>(idx[r]);
+        svs[b + g] = static_cast<T>(key[r]);  // exact: the key is the widened input value
+      }
     }
   }
 }
 
 void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, const int64_t* rowptr, const int* rows,
-                     int nrows, int K, uint16_t* sidx, cudaStream_t st) {
+                     int nrows, int K, uint16_t* sidx, void* svs, cudaStream_t st) {
   if (nrows <= 0) return;
   const unsigned blocks = static_cast<unsigned>(std::max(1, std::min((nrows + 7) / 8, 148 * 8)));
 #define GMDS_RS(KK)                                                                                                \
   case KK:                                                                                                         \
     if (xt == GMDS_F32)                                                                                            \
-      row_sort_kernel<KK, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(vals), fidx, rowptr, rows, nrows, sidx); \
+      row_sort_kernel<KK, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(vals), fidx, rowptr, rows, nrows, sidx, static_cast<float*>(svs)); \
     else                                                                                                           \
-      row_sort_kernel<KK, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(vals), fidx, rowptr, rows, nrows, sidx); \
+      row_sort_kernel<KK, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(vals), fidx, rowptr, rows, nrows, sidx, static_cast<double*>(svs)); \
     break;
   switch (K) {
     GMDS_RS(1) GMDS_RS(2) GMDS_RS(4) GMDS_RS(8) GMDS_RS(16) GMDS_RS(32)

@@ -24,6 +24,7 @@ namespace gmds {
 struct MergeArgs {
   SplitArgs s;
   const uint16_t* sidx;  // per row, its nonzero features sorted by value (rowptr layout)
+  const void* svs;       // per row, its nonzero values sorted ascending (rowptr layout)
 };
 
 namespace merge_detail {
@@ -252,7 +253,9 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
   uint16_t* spre = reinterpret_cast<uint16_t*>(smask + 2 * tile * W);          // [2 tile][W]
   int* scnt = reinterpret_cast<int*>(pbase + ((2 * static_cast<size_t>(tile) * W * 6 + 15) & ~static_cast<size_t>(15)));
   T* svals = reinterpret_cast<T*>(scnt + 2 * tile + 4);                        // [2 tile][stride]
-  uint16_t* ssidx = reinterpret_cast<uint16_t*>(svals + 2 * static_cast<size_t>(tile) * stride);  // [2 tile][stride]
+  T* ssv = svals + 2 * static_cast<size_t>(tile) * stride;                        // [2 tile][stride] sorted values
+  uint16_t* ssidx = reinterpret_cast<uint16_t*>(ssv + 2 * static_cast<size_t>(tile) * stride);  // [2 tile][stride]
+  const T* gsv = static_cast<const T*>(ma.svs);
   const T* gv = static_cast<const T*>(sa.vals);
   const double half_p = 0.5 * static_cast<double>(d);
   const unsigned lt = (1u << lane) - 1u;
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
         for (int64_t k = b + lane; k < e1; k += 32) {
           svals[static_cast<size_t>(r) * stride + (k - b)] = gv[k];
           ssidx[static_cast<size_t>(r) * stride + (k - b)] = ma.sidx[k];
+          ssv[static_cast<size_t>(r) * stride + (k - b)] = gsv[k];
         }
       }
       if (lane == 0) scnt[r] = cnt;
@@ -300,6 +304,8 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
       const T* vi = svals + static_cast<size_t>(ri) * stride;
       const T* vj = svals + static_cast<size_t>(rj) * stride;
       const uint16_t* si = ssidx + static_cast<size_t>(ri) * stride;
+      const T* svi = ssv + static_cast<size_t>(ri) * stride;
+      const T* svj = ssv + static_cast<size_t>(rj) * stride;
       const uint16_t* sj = ssidx + static_cast<size_t>(rj) * stride;
       const int ci = scnt[ri], cj = scnt[rj];
       double* ot = otile + static_cast<size_t>(r) * tstride + c;
@@ -314,7 +320,7 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
         const int w = f >> 5, b = f & 31;
         const uint32_t mjw = mj[w];
         const bool inj = in && ((mjw >> b) & 1u);
-        const T avt = in ? vi[pi[w] + __popc(mi[w] & ((1u << b) - 1u))] : T(0);
+        const T avt = in ? svi[k] : T(0);  // row i's k-th smallest nonzero (no feature-order gather)
         const double av = static_cast<double>(avt);
         const unsigned bp = __ballot_sync(kFull, in && !inj);
         if (in && !inj) {
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
         if (in && !ini) {
           const int pos = cn + __popc(bn & lt);
           if (pos < kHalfCap)
-            A32[sk32(pos)] = neg_key(static_cast<float>(vj[pj[w] + __popc(mj[w] & ((1u << b) - 1u))]), false);
+            A32[sk32(pos)] = neg_key(static_cast<float>(svj[cj - 1 - q]), false);
         }
         cn += __popc(bn);
       }
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
 inline size_t merge_smem(int tile, int W, int maxnnz, size_t sz, int nnu) {
   return static_cast<size_t>(16) * merge_detail::kWarpScratch * 8 + static_cast<size_t>(nnu) * tile * (tile + 1) * 8 +
          ((2 * static_cast<size_t>(tile) * W * 6 + 15) & ~static_cast<size_t>(15)) + (2 * tile + 4) * 4 +
-         2 * static_cast<size_t>(tile) * maxnnz * (sz + 2) + 16;
+         2 * static_cast<size_t>(tile) * maxnnz * (2 * sz + 2) + 16;
 }
 
 void launch_gini_merge(const MergeArgs& ma, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, size_t smem,

@@ -22,7 +22,7 @@ void launch_gini_list(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64
                       gmds_dtype ot, cudaStream_t st);
 
 void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, const int64_t* rowptr, const int* rows,
-                     int nrows, int K, uint16_t* sidx, cudaStream_t st);
+                     int nrows, int K, uint16_t* sidx, void* svs, cudaStream_t st);
 
 namespace {
 
@@ -85,6 +85,7 @@ __global__ void row_fill_kernel(const T* __restrict__ X, int64_t n, int p, int W
 
 struct RowStore {
   DevBuf<uint16_t> fidx, sidx;
+  DevBuf<unsigned char> svs;  // values in ascending order per row (merge path)
   bool nonneg = false;
   DevBuf<uint32_t> masks;
   DevBuf<uint16_t> prefix;
@@ -141,6 +142,7 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
   if (rs.nonneg) {
     // value-sorted feature order per row (the merge kernel's runs); rows bucketed by sort width
     rs.sidx.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
+    rs.svs.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])) * dtype_size(xt));
     std::vector<std::vector<int>> buckets(6);
     for (int64_t i = 0; i < n; ++i) {
       int K = 1;
@@ -155,7 +157,7 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
       GMDS_CUDA(cudaMemcpyAsync(rows.get(), buckets[bk].data(), buckets[bk].size() * sizeof(int),
                                 cudaMemcpyHostToDevice, st));
       launch_row_sort(rs.vals.get(), xt, rs.fidx.get(), rs.rowptr.get(), rows.get(),
-                      static_cast<int>(buckets[bk].size()), 1 << bk, rs.sidx.get(), st);
+                      static_cast<int>(buckets[bk].size()), 1 << bk, rs.sidx.get(), rs.svs.get(), st);
       GMDS_CUDA(cudaStreamSynchronize(st));
     }
   }
@@ -273,6 +275,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       ma.s.maxnnz = std::max(1, rs.maxnnz);
       ma.s.sparse = 1;
       ma.sidx = rs.sidx.get();
+      ma.svs = rs.svs.get();
       const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(mt) * mt;
       ma.s.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 20) : 0;
       DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * ma.s.ovf_cap)));
