@@ -32,5 +32,7 @@ struct gmds_dmat {
   mutable std::mutex mu;
   mutable std::vector<std::pair<int, std::shared_ptr<gmds::Engine>>> engines;
   mutable std::vector<bool> busy;
+  // dense row-major fp64 copy for the single-CTA small-n fit (n <= 1024), built once
+  mutable std::shared_ptr<gmds::DevBuf<double>> dense;
   const void* ptr() const { return shared ? static_cast<const void*>(shared->get() + offset) : buf.get(); }
 };

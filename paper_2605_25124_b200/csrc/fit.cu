@@ -16,7 +16,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <map>
 #include <limits>
 #include <string>
 #include <vector>
@@ -27,6 +29,7 @@
 #include "fit.h"
 #include "kernels.cuh"
 #include "lib_internal.h"
+#include "small_fit.h"
 #include "stress.cuh"
 
 namespace gmds {
@@ -37,6 +40,21 @@ constexpr int64_t kChunk = 4;
 constexpr double kTiny = 1e-300;  // embed.cpp:13
 
 int padded_q(int q) { return q <= 4 ? q : q; }
+
+// One cuSOLVER handle per (host thread, device), created on first use and kept:
+// creating one costs milliseconds, which dominated small classical fits.
+cusolverDnHandle_t solver_handle(cudaStream_t st) {
+  static thread_local std::map<int, cusolverDnHandle_t> handles;
+  int dev = 0;
+  GMDS_CUDA(cudaGetDevice(&dev));
+  cusolverDnHandle_t& h = handles[dev];
+  if (!h && cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) {
+    h = nullptr;
+    fail(GMDS_CUDA_ERROR, "cusolverDnCreate failed");
+  }
+  cusolverDnSetStream(h, st);
+  return h;
+}
 
 }  // namespace
 
@@ -463,13 +481,7 @@ void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigval
   DevBuf<double> B(static_cast<size_t>(n * n));
   unpack_full(D->ptr(), D->storage, n, B.get(), true, st);  // S = D o D
   double_center_dev(B.get(), n, st);
-  cusolverDnHandle_t h = nullptr;
-  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(GMDS_CUDA_ERROR, "cusolverDnCreate failed");
-  struct Guard {
-    cusolverDnHandle_t h;
-    ~Guard() { cusolverDnDestroy(h); }
-  } guard{h};
-  cusolverDnSetStream(h, st);
+  cusolverDnHandle_t h = solver_handle(st);
   DevBuf<double> w(static_cast<size_t>(n));
   int lwork = 0;
   if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), B.get(),
@@ -540,13 +552,7 @@ DevBuf<double> weights_pinv(const double* weights, int64_t n, cudaStream_t st) {
     }
   DevBuf<double> dV(static_cast<size_t>(n * n));
   GMDS_CUDA(cudaMemcpyAsync(dV.get(), V.data(), V.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-  cusolverDnHandle_t h = nullptr;
-  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) fail(GMDS_CUDA_ERROR, "cusolverDnCreate failed");
-  struct G {
-    cusolverDnHandle_t h;
-    ~G() { cusolverDnDestroy(h); }
-  } g{h};
-  cusolverDnSetStream(h, st);
+  cusolverDnHandle_t h = solver_handle(st);
   DevBuf<double> w(static_cast<size_t>(n));
   int lwork = 0;
   cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(n), dV.get(),
@@ -582,6 +588,67 @@ DevBuf<double> weights_pinv(const double* weights, int64_t n, cudaStream_t st) {
   GMDS_CUDA(cudaMemcpyAsync(dP.get(), P.data(), P.size() * sizeof(double), cudaMemcpyHostToDevice, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
   return dP;
+}
+
+// The whole fit in one cooperative persistent kernel (small_fit.cu): same control flow as
+// gradient_descent / smacof_iterate above, no host round trip per pass.
+bool small_fit(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, const Resolved& rp,
+               const std::vector<double>& init, gmds_fit_result* res, cudaStream_t st) {
+  const int64_t n = D->n;
+  const int grid = small_fit_grid(n);
+  if (grid == 0) return false;
+  std::shared_ptr<DevBuf<double>> dense;
+  {
+    std::lock_guard<std::mutex> g(D->mu);
+    if (!D->dense) {
+      auto b = std::make_shared<DevBuf<double>>(static_cast<size_t>(n * n));
+      unpack_full(D->ptr(), D->storage, n, b->get(), false, st);
+      D->dense = b;
+    }
+    dense = D->dense;
+  }
+  const size_t nq = static_cast<size_t>(n) * q;
+  const size_t hist = static_cast<size_t>(cfg.max_iters) + 2;
+  // Yout | history | out | 4 slots | partials
+  DevBuf<double> buf(nq + hist + 1 + 4 * nq + 8 * static_cast<size_t>(grid));
+  DevBuf<int> ibuf(4);
+  std::vector<double> h(nq);
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < q; ++k) h[static_cast<size_t>(i) * q + k] = init[static_cast<size_t>(k) * n + i];
+  SmallFitArgs a{};
+  a.D = dense->get();
+  a.Yout = buf.get();
+  a.history = a.Yout + nq;
+  a.out = a.history + hist;
+  for (int s = 0; s < 4; ++s) a.buf[s] = a.out + 1 + s * nq;
+  a.lossp = a.buf[3] + nq;
+  a.iout = ibuf.get();
+  GMDS_CUDA(cudaMemcpyAsync(a.buf[0], h.data(), nq * sizeof(double), cudaMemcpyHostToDevice, st));
+  a.n = static_cast<int>(n);
+  a.kind = rp.kind;
+  a.delta = rp.delta;
+  a.sum = D->sum;
+  a.sum_sq = D->sum_sq;
+  a.max_iters = cfg.max_iters;
+  a.rel_tol = cfg.rel_tol;
+  launch_small_fit(a, q, grid, st);
+  std::vector<double> back(nq + hist + 1);
+  int iv[4];
+  GMDS_CUDA(cudaMemcpyAsync(back.data(), a.Yout, back.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(iv, a.iout, sizeof(iv), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < n; ++i)
+    for (int k = 0; k < q; ++k) res->coords[static_cast<size_t>(k) * n + i] = back[static_cast<size_t>(i) * q + k];
+  res->history_len = iv[2];
+  if (res->history)
+    for (int64_t t = 0; t < std::min<int64_t>(res->history_len, res->history_cap); ++t)
+      res->history[t] = back[nq + static_cast<size_t>(t)];
+  res->iterations = iv[0];
+  res->converged = iv[1];
+  res->stress = back[nq + hist];
+  res->huber_delta = (cfg.kind == GMDS_HUBER) ? cfg.huber_delta : 0.0;
+  res->passes = iv[3];
+  return true;
 }
 
 }  // namespace
@@ -645,6 +712,9 @@ void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, 
     return;
   }
   const Resolved rp = resolve(D, cfg.kind, cfg.huber_delta, cfg.smacof_weights, "minimize_stress");
+  if (!rp.weighted && small_fit_supported(n, q) && !std::getenv("GMDS_NO_SMALL_FIT")) {
+    if (small_fit(D, q, cfg, rp, init, res, st)) return;
+  }
   EngineLease L = acquire_engine(D, q, st);
   Engine& E = *L;
   DevBuf<unsigned char> W;

@@ -248,3 +248,26 @@ def test_tune_contract():
     direct = G.classical_mds(D, 2)
     assert r["mean_stress"][0] == pytest.approx(G.kruskal_stress(direct["coords"], D), rel=1e-12)
     assert np.allclose(r["coords"], direct["coords"], atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["kruskal", "huber", "sammon", "smacof"])
+@pytest.mark.parametrize("n,q", [(2, 1), (37, 3), (300, 2), (1024, 4), (2048, 2)])
+def test_small_fit_matches_pass_engine(monkeypatch, kind, n, q):
+    # n <= 2048, q <= 4 fits run as one cooperative persistent kernel (small_fit.cu); the
+    # multi-kernel pass engine (GMDS_NO_SMALL_FIT) is the same algorithm
+    D = rand_dissim(n + q, n)
+    hd = 0.6 if kind == "huber" else None
+    Y0 = np.random.default_rng(n).normal(0.0, 0.1, (n, q))
+    e = G.minimize_stress(D, q, kind, huber_delta=hd, max_iters=120, rel_tol=1e-300, Y0=Y0)
+    monkeypatch.setenv("GMDS_NO_SMALL_FIT", "1")
+    r = G.minimize_stress(D, q, kind, huber_delta=hd, max_iters=120, rel_tol=1e-300, Y0=Y0)
+    h, hr = np.array(e["stress_history"]), np.array(r["stress_history"])
+    k = min(len(h), len(hr), 51)
+    assert k >= min(len(hr), 2)
+    assert np.max(np.abs(h[:k] - hr[:k]) / np.maximum(hr[:k], 1e-8 * hr[0])) <= 1e-9
+    assert abs(e["stress"] - r["stress"]) <= FINAL * max(r["stress"], 1e-8 * hr[0])
+    if n <= 300:
+        o = O.minimize_stress(D, q, kind, huber_delta=hd, max_iters=60, rel_tol=1e-300, Y0=Y0)
+        ho = np.array(o.stress_history)
+        k = min(len(h), len(ho), 51)
+        assert np.max(np.abs(h[:k] - ho[:k]) / np.maximum(ho[:k], 1e-8 * ho[0])) <= TRAJ
