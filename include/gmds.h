@@ -146,6 +146,17 @@ gmds_status gmds_double_center(const double* S, int64_t n, double* B);
 gmds_status gmds_classical_mds(const gmds_dmat* D, int32_t q, double* coords, double* eigvals, int32_t* clamped_count,
                                double* clamped_mass, double* stress);
 
+/* classical_mds, top-q only: the q largest eigenpairs of the
+ * double-centred Gram matrix by device subspace iteration (cuBLAS DGEMM on the
+ * dense B, Rayleigh-Ritz), same sign rule and clamp as gmds_classical_mds but
+ * without the full spectrum (no clamped_mass).  Converged when every top-q
+ * residual ||B u - theta u|| <= tol * max|theta|.  GMDS_NUMERIC_FAILURE when
+ * not converged in max_iters or when the top q are not separated from the
+ * rest of the spectrum.  minimize_stress's classical init uses it for
+ * n > 4096.  iterations may be NULL. */
+gmds_status gmds_classical_mds_topq(const gmds_dmat* D, int32_t q, double tol, int32_t max_iters, double* coords,
+                                    double* eigvals, int32_t* clamped_count, int32_t* iterations);
+
 /* StressConfig (embed.hpp:19-29). */
 typedef struct gmds_stress_cfg {
   int32_t kind;         /* gmds_stress_kind */

@@ -30,6 +30,7 @@
 #include "kernels.cuh"
 #include "lib_internal.h"
 #include "small_fit.h"
+#include "classical_topq.h"
 #include "stress.cuh"
 
 namespace gmds {
@@ -668,7 +669,21 @@ void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, 
     std::vector<double> ev(static_cast<size_t>(q));
     int cc = 0;
     double cm = 0.0;
-    classical_mds_dev(D, q, init.data(), ev.data(), &cc, &cm, nullptr, st);
+    // classical init: only the coordinates are used, so large n takes the
+    // top-q subspace solver instead of the O(n^3) dense one
+    const char* mode = std::getenv("GMDS_CLASSICAL");
+    const bool dense = mode ? std::string(mode) == "dense" : n <= kDenseEigMaxN;
+    bool done = false;
+    if (!dense && q <= 16) {
+      try {
+        int its = 0;
+        classical_topq_dev(D, q, 1e-10, 2000, init.data(), ev.data(), &cc, &its, st);
+        done = true;
+      } catch (const Failure& e) {
+        if (e.status != GMDS_NUMERIC_FAILURE) throw;  // not separated / not converged: dense path
+      }
+    }
+    if (!done) classical_mds_dev(D, q, init.data(), ev.data(), &cc, &cm, nullptr, st);
   }
   if (cfg.kind == GMDS_HUBER && std::isnan(cfg.huber_delta)) {
     const double med = packed_median(D->ptr(), D->storage, n, st);
@@ -971,6 +986,18 @@ gmds_status gmds_classical_mds(const gmds_dmat* D, int32_t q, double* coords, do
     int cc = 0;
     classical_mds_dev(D, q, coords, eigvals, &cc, clamped_mass, stress, st.s);
     *clamped_count = cc;
+  });
+}
+
+gmds_status gmds_classical_mds_topq(const gmds_dmat* D, int32_t q, double tol, int32_t max_iters, double* coords,
+                                    double* eigvals, int32_t* clamped_count, int32_t* iterations) {
+  return guard([&] {
+    if (!D) fail(GMDS_INVALID_INPUT, "classical_mds: null distance matrix");
+    Stream st;
+    int cc = 0, its = 0;
+    classical_topq_dev(D, q, tol, max_iters, coords, eigvals, &cc, &its, st.s);
+    *clamped_count = cc;
+    if (iterations) *iterations = its;
   });
 }
 

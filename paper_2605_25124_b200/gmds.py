@@ -337,6 +337,19 @@ def classical_mds(D, q: int) -> dict:
                 clamped_mass=cm.value, stress=st.value)
 
 
+def classical_mds_topq(D, q: int, tol: float = 1e-10, max_iters: int = 2000) -> dict:
+    """Top-q classical MDS by device subspace iteration."""
+    Dm = _as_dmat(D)
+    coords = np.zeros((Dm.n, q), order="F")
+    ev = np.zeros(max(q, 1))
+    cc = ctypes.c_int32()
+    its = ctypes.c_int32()
+    _check(lib().gmds_classical_mds_topq(Dm.handle, _i32(q), ctypes.c_double(tol), _i32(max_iters), _p(coords),
+                                         _p(ev), ctypes.byref(cc), ctypes.byref(its)))
+    return dict(coords=np.ascontiguousarray(coords), eigenvalues=ev[:q], clamped_count=cc.value,
+                iterations=its.value)
+
+
 def minimize_stress(D, q: int, kind: str = "smacof", huber_delta=None, weights=None, max_iters: int = 300,
                     rel_tol: float = 1e-6, Y0=None, storage=F64) -> dict:
     """minimize_stress (embed.cpp:491-532); Y0 = seeded-init mode."""

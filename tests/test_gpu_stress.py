@@ -271,3 +271,63 @@ def test_small_fit_matches_pass_engine(monkeypatch, kind, n, q):
         ho = np.array(o.stress_history)
         k = min(len(h), len(ho), 51)
         assert np.max(np.abs(h[:k] - ho[:k]) / np.maximum(ho[:k], 1e-8 * ho[0])) <= TRAJ
+
+
+@pytest.mark.parametrize("q", [1, 2, 3])
+def test_classical_topq_matches_dense(q):
+    # top-q subspace iteration == the dense eigensolver's top q
+    rng = np.random.default_rng(7 + q)
+    X = rng.standard_normal((700, 12)) * np.linspace(3.0, 0.5, 12)
+    D = G.pairwise_matrix(X, 2.0)
+    Dm = G.dmat_from_host(D)
+    r = G.classical_mds(Dm, q)
+    t = G.classical_mds_topq(Dm, q, tol=1e-12)
+    assert t["iterations"] >= 1
+    assert np.allclose(t["eigenvalues"], r["eigenvalues"], rtol=1e-10)
+    assert np.max(np.abs(t["coords"] - r["coords"])) <= 1e-7 * np.max(np.abs(r["coords"]))
+    assert t["clamped_count"] == r["clamped_count"]
+
+
+def test_classical_topq_full_subspace_indefinite():
+    # k == n (tiny n): the subspace is the whole space, clamped eigenvalues included
+    for seed in range(64):
+        rng = O.Rng(seed)
+        X = O.random_matrix(rng, 8, 3, 5.0)
+        D = O.pairwise_matrix(X, 3.0)
+        lam = np.linalg.eigvalsh(O.double_center(D * D))
+        if lam[0] < -1e-9 * np.max(np.abs(lam)):
+            r = G.classical_mds(D, 7)
+            t = G.classical_mds_topq(D, 7, tol=1e-13)
+            # B's exact null eigenvalue (J 1 = 0) has a round-off sign in both solvers:
+            # count clamps only for eigenvalues clearly below zero
+            big = 1e-9 * np.max(np.abs(lam))
+            assert np.sum(t["eigenvalues"] < -big) == np.sum(r["eigenvalues"] < -big) > 0
+            assert np.allclose(t["eigenvalues"], r["eigenvalues"], rtol=1e-8, atol=1e-9 * np.max(np.abs(lam)))
+            assert np.max(np.abs(t["coords"] - r["coords"])) <= 1e-6 * np.max(np.abs(r["coords"]))
+            return
+    pytest.fail("no indefinite instance found")
+
+
+def test_classical_topq_errors():
+    D = rand_dissim(1, 50)
+    with pytest.raises(G.InvalidInput):
+        G.classical_mds_topq(D, 0)
+    with pytest.raises(G.InvalidConfig):
+        G.classical_mds_topq(D, 2, tol=0.0)
+    with pytest.raises(G.NumericFailure):
+        G.classical_mds_topq(D, 2, tol=1e-300, max_iters=2)
+
+
+def test_minimize_stress_subspace_classical_init(monkeypatch):
+    # the classical init of minimize_stress switches to the subspace solver above
+    # n = 4096; both inits must give the same trajectory
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((900, 10)) * np.linspace(2.0, 0.5, 10)
+    D = G.pairwise_matrix(X, 2.0)
+    monkeypatch.setenv("GMDS_CLASSICAL", "dense")
+    a = G.minimize_stress(D, 2, "kruskal", max_iters=60, rel_tol=1e-300)
+    monkeypatch.setenv("GMDS_CLASSICAL", "subspace")
+    b = G.minimize_stress(D, 2, "kruskal", max_iters=60, rel_tol=1e-300)
+    ha, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
+    assert len(ha) == len(hb)
+    assert np.max(np.abs(ha - hb) / ha) <= 1e-8
