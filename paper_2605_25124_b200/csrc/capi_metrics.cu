@@ -87,6 +87,27 @@ DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, 
   return out;
 }
 
+namespace {
+template <typename T>
+__global__ void finite_check_kernel(const T* __restrict__ X, int64_t m, int* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= !isfinite(X[k]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 4);
+}
+}  // namespace
+
+void launch_finite_check(const void* dX, gmds_dtype xt, int64_t m, int* dflag, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 148 * 8)));
+  if (xt == GMDS_F32)
+    finite_check_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dX), m, dflag);
+  else
+    finite_check_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dX), m, dflag);
+  count_launch();
+  check_launch("finite_check_kernel");
+}
+
 void check_flag(int* dflag, cudaStream_t st) {
   int flag = 0;
   GMDS_CUDA(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -261,19 +282,70 @@ gmds_status gmds_pairwise_gini(const void* X, gmds_dtype xt, gmds_layout lx, int
     for (int v = 0; v < nnu; ++v) check_nu(nus[v]);
     if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
     if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
-    check_finite_host(X, xt, n * p, "gen_gini_directed");
     require_device();
     Stream st;
     DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
-    const size_t bytes = static_cast<size_t>(nnu) * n * n * dtype_size(out_t);
-    DevBuf<unsigned char> dD(bytes);
     DevBuf<int> flag(1);
     GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st.s));
+    // gen_gini_directed_checked (metrics.cpp:84-93): every input entry finite
+    // -- checked on the device (bit 2 of the flag), reported before any result
+    launch_finite_check(dX.get(), xt, n * p, flag.get(), st.s);
+    const size_t plane = static_cast<size_t>(n) * n * dtype_size(out_t);
+    const size_t bytes = static_cast<size_t>(nnu) * plane;
+    DevBuf<unsigned char> dD(bytes);
     GMDS_CUDA(cudaMemsetAsync(dD.get(), 0, bytes, st.s));
-    run_gini(dX.get(), xt, n, p, nus, nnu, out_t, 0, dD.get(), 0, 1, st.s, flag.get());
-    check_flag(flag.get(), st.s);
-    GMDS_CUDA(cudaMemcpyAsync(D, dD.get(), bytes, cudaMemcpyDeviceToHost, st.s));
+    // A pinned destination is filled row stripe by row stripe while later
+    // tiles are still computing (copy stream + one event per stripe).
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, D) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    struct CopySink : RowSink {
+      cudaStream_t cs = nullptr;
+      std::vector<cudaEvent_t> evs;
+      unsigned char* host;
+      const unsigned char* dev;
+      size_t plane, row_bytes;
+      int nnu;
+      int64_t prev = 0;
+      void rows_done(int64_t rows, cudaStream_t st) override {
+        cudaEvent_t ev;
+        GMDS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        evs.push_back(ev);
+        GMDS_CUDA(cudaEventRecord(ev, st));
+        GMDS_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+        for (int v = 0; v < nnu; ++v)
+          GMDS_CUDA(cudaMemcpyAsync(host + v * plane + prev * row_bytes, dev + v * plane + prev * row_bytes,
+                                    (rows - prev) * row_bytes, cudaMemcpyDeviceToHost, cs));
+        prev = rows;
+      }
+      ~CopySink() override {
+        if (cs) {
+          cudaStreamSynchronize(cs);
+          cudaStreamDestroy(cs);
+        }
+        for (auto e : evs) cudaEventDestroy(e);
+      }
+    } sink;
+    sink.host = static_cast<unsigned char*>(D);
+    sink.dev = dD.get();
+    sink.plane = plane;
+    sink.row_bytes = static_cast<size_t>(n) * dtype_size(out_t);
+    sink.nnu = nnu;
+    if (pinned) GMDS_CUDA(cudaStreamCreateWithFlags(&sink.cs, cudaStreamNonBlocking));
+    run_gini(dX.get(), xt, n, p, nus, nnu, out_t, 0, dD.get(), 0, 1, st.s, flag.get(), nullptr,
+             pinned ? &sink : nullptr);
+    int hflag = 0;
+    GMDS_CUDA(cudaMemcpyAsync(&hflag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st.s));
     GMDS_CUDA(cudaStreamSynchronize(st.s));
+    if (hflag & 4) fail(GMDS_INVALID_INPUT, "gen_gini_directed: non-finite input entry");
+    if (hflag & 1) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
+    if (pinned && sink.prev == n && !sink.late_writes) {
+      GMDS_CUDA(cudaStreamSynchronize(sink.cs));
+    } else {
+      if (pinned) GMDS_CUDA(cudaStreamSynchronize(sink.cs));
+      GMDS_CUDA(cudaMemcpyAsync(D, dD.get(), bytes, cudaMemcpyDeviceToHost, st.s));
+      GMDS_CUDA(cudaStreamSynchronize(st.s));
+    }
   });
 }
 

@@ -31,7 +31,7 @@ namespace merge_detail {
 
 constexpr int kHalfCap = 256;  // max keys per sign half on the merge path
 constexpr int kMCap = 128;     // max |S_ab| on the merge path
-constexpr int kAB32 = 272;     // skewed u32 half buffer (256 + 256/32, rounded)
+constexpr int kAB32 = 272;     // u32 half buffer (256 keys; 16-byte aligned halves)
 constexpr int kMB = kMCap + kMCap / 16;
 // per-warp scratch in doubles: A32 | B32 (u32 keys) | M (fp64 S_ab) | RA | RB (residuals)
 constexpr int kOffB = kAB32 / 2, kOffM = kAB32, kOffRA = kOffM + kMB, kOffRB = kOffRA + kMCap;
@@ -39,8 +39,9 @@ constexpr int kWarpScratch = kOffRB + kMCap;
 static_assert(kWarpScratch >= kSplitCap, "fallback scratch");
 
 // skewed indices: blocked reads of K consecutive elements per lane hit distinct banks
-__device__ __forceinline__ int sk(int e) { return e + (e >> 4); }    // 8-byte elements
-__device__ __forceinline__ int sk32(int e) { return e + (e >> 5); }  // 4-byte elements
+__device__ __forceinline__ int sk(int e) { return e + (e >> 4); }  // 8-byte elements
+// The u32 key halves are NOT skewed: they are read as 16-byte vectors.
+__device__ __forceinline__ int sk32(int e) { return e; }
 
 // Exact 32-bit keys of one sign half.  With f = z rounded toward zero to fp32
 // and x = 1 when that rounding was inexact, the magnitude code 2*bits(f) + x
@@ -171,10 +172,27 @@ __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint
   const uint32_t* src = hiB ? B32 : A32;
   const int head = hiB ? cp : cn;
   const int tail = H - (hiB ? mpos : mneg);
+  if constexpr (K >= 4) {
+    // pad the gap between the head (compacted row-only keys) and the tail
+    // (sorted S_ab keys) so the blocked reads are unconditional 16-byte loads
+    uint32_t* dst = const_cast<uint32_t*>(src);
+    for (int e = head + l16; e < tail; e += 16) dst[e] = 0xFFFFFFFFu;
+    __syncwarp();
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + l16 * K);
 #pragma unroll
-  for (int r = 0; r < K; ++r) {
-    const int g = l16 * K + r;  // slot within the half
-    key[r] = (g < head || g >= tail) ? src[sk32(g)] : 0xFFFFFFFFu;
+    for (int m = 0; m < K / 4; ++m) {
+      const uint4 v = s4[m];
+      key[4 * m] = v.x;
+      key[4 * m + 1] = v.y;
+      key[4 * m + 2] = v.z;
+      key[4 * m + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int g = l16 * K + r;  // slot within the half
+      key[r] = (g < head || g >= tail) ? src[g] : 0xFFFFFFFFu;
+    }
   }
   __syncwarp();
   warp_merge_u32<K>(key, lane);

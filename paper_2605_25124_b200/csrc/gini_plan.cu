@@ -177,8 +177,35 @@ size_t split_smem(int tile, int p, int W, int maxnnz, size_t sz, int nnu, bool s
 }  // namespace
 
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
-              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score) {
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score,
+              RowSink* sink) {
   Trace tr;
+  if (packed || score || nshards != 1) sink = nullptr;
+  // Launch tiles [a.tile_begin, a.tile_end) -- in block-row chunks when a sink
+  // wants the finished rows as they complete.
+  auto chunked = [&](GiniTileArgs& ga, auto&& launch) {
+    if (!sink) {
+      launch(ga);
+      return;
+    }
+    const int64_t nbt = ga.nbt, b0 = ga.tile_begin, b1 = ga.tile_end;
+    auto start = [nbt](int64_t r) { return r * nbt - (r * (r - 1)) / 2; };
+    int64_t R = 0;
+    for (int c = 1; c <= sink->chunks; ++c) {
+      const int64_t target = b0 + (b1 - b0) * c / sink->chunks;
+      int64_t R1 = R;
+      while (R1 < nbt && start(R1 + 1) <= target) ++R1;
+      if (c == sink->chunks) R1 = nbt;
+      if (R1 == R) continue;
+      ga.tile_begin = start(R);
+      ga.tile_end = start(R1);
+      launch(ga);
+      sink->rows_done(std::min<int64_t>(n, R1 * ga.tile), st);
+      R = R1;
+    }
+    ga.tile_begin = b0;
+    ga.tile_end = b1;
+  };
   if (score && (p > 1024 || nnu > kMaxScoreNu)) {  // block path / too many nu: caller falls back
     score->ok = false;
     return;
@@ -245,7 +272,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
     a.tile_begin = units * shard / nshards;
     a.tile_end = units * (shard + 1) / nshards;
-    launch_gini(a, dX, xt, dD, ot, st, score ? score_grid : 0);
+    chunked(a, [&](GiniTileArgs& ga) { launch_gini(ga, dX, xt, dD, ot, st, score ? score_grid : 0); });
     finish_score(score ? std::min<int64_t>(a.tile_end - a.tile_begin, score_grid) : 0);
   };
   if (!sparse && p > 512) {
@@ -287,17 +314,26 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       const unsigned mblocks =
           static_cast<unsigned>(grid_of(std::min<int64_t>(a.tile_end - a.tile_begin, int64_t(1) << 30)));
       ma.s.g = a;
-      launch_gini_merge(ma, dX, xt, dD, ot, msm, mblocks, st);
-      count_launch();
-      check_launch("gini_merge_kernel");
+      chunked(a, [&](GiniTileArgs& ga) {
+        ma.s.g = ga;
+        const unsigned blk = static_cast<unsigned>(grid_of(std::min<int64_t>(ga.tile_end - ga.tile_begin, int64_t(1) << 30)));
+        launch_gini_merge(ma, dX, xt, dD, ot, msm, blk, st);
+        count_launch();
+        check_launch("gini_merge_kernel");
+      });
+      ma.s.g = a;
       tr.mark("gini_merge_kernel", st);
       unsigned long long novf = 0;
       GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
       GMDS_CUDA(cudaStreamSynchronize(st));
       finish_score(mblocks);
       if (novf == 0 || score) return;
+      if (sink) sink->late_writes = true;
       if (static_cast<int64_t>(novf) > ma.s.ovf_cap) {
+        RowSink* keep = sink;
+        sink = nullptr;  // rewrites already-copied rows
         full_kernel();
+        sink = keep;
       } else {
         launch_gini_list<32>(a, dX, xt, ovf.get(), static_cast<int64_t>(novf), dD, ot, st);
         count_launch();
@@ -343,18 +379,26 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   sa.ovf_count = ovf_count.get();
   const unsigned blocks = static_cast<unsigned>(grid_of(std::min<int64_t>(a.tile_end - a.tile_begin, 1 << 30)));
   sa.g = a;
-  if (p <= 256)
-    launch_gini_split<8>(sa, dX, xt, dD, ot, smem, blocks, st);
-  else
-    launch_gini_split<16>(sa, dX, xt, dD, ot, smem, blocks, st);
-  count_launch();
-  check_launch("gini_split_kernel");
+  (void)blocks;
+  chunked(a, [&](GiniTileArgs& ga) {
+    sa.g = ga;
+    const unsigned blk = static_cast<unsigned>(grid_of(std::min<int64_t>(ga.tile_end - ga.tile_begin, 1 << 30)));
+    if (p <= 256)
+      launch_gini_split<8>(sa, dX, xt, dD, ot, smem, blk, st);
+    else
+      launch_gini_split<16>(sa, dX, xt, dD, ot, smem, blk, st);
+    count_launch();
+    check_launch("gini_split_kernel");
+  });
+  sa.g = a;
   unsigned long long novf = 0;
   GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
   finish_score(blocks);
   if (novf == 0 || score) return;
+  if (sink) sink->late_writes = true;
   if (static_cast<int64_t>(novf) > sa.ovf_cap) {  // list too long: redo these tiles with the all-keys kernel
+    sink = nullptr;
     full_kernel();
     GMDS_CUDA(cudaStreamSynchronize(st));
     return;

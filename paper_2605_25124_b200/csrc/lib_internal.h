@@ -34,8 +34,24 @@ struct ScoreSpec {
   bool ok = false;  // out: false when a pair needed the overflow path (caller falls back)
 };
 
+// Progress of a full-layout (unpacked) distance run: tiles are enumerated
+// block row by block row, and a tile (I, J) writes block (I, J) and its mirror
+// (J, I), so once the tiles of block rows [0, R) are done, output rows
+// [0, R * tile) are final.  run_gini then calls rows_done(rows, st) (after the
+// launch on st); a caller may start copying those rows out.  late_writes is
+// set when a pass over overflow pairs rewrote arbitrary entries afterwards.
+struct RowSink {
+  virtual ~RowSink() = default;
+  virtual void rows_done(int64_t rows, cudaStream_t st) = 0;
+  bool late_writes = false;
+  int chunks = 12;
+};
+
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
-              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score = nullptr);
+              int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score = nullptr,
+              RowSink* sink = nullptr);
 void check_flag(int* dflag, cudaStream_t st);
+// flag |= 4 when any of the m input entries is not finite
+void launch_finite_check(const void* dX, gmds_dtype xt, int64_t m, int* dflag, cudaStream_t st);
 
 }  // namespace gmds

@@ -177,13 +177,19 @@ def gen_gini_distance(x, y, nu: float) -> float:
     return float(out[0])
 
 
-def pairwise_gini(X, nus, out_dtype=np.float64) -> np.ndarray:
-    """pairwise_matrix(X, gini(nu)) for every nu at once -> (len(nus), n, n)."""
+def pairwise_gini(X, nus, out_dtype=np.float64, out=None) -> np.ndarray:
+    """pairwise_matrix(X, gini(nu)) for every nu at once -> (len(nus), n, n).
+    `out` may be a caller buffer of that shape (e.g. pinned host memory, which
+    the library fills row stripe by row stripe while later tiles compute)."""
     X, xt, lx = _xarg(X)
     n, p = X.shape
     nus = np.ascontiguousarray(np.atleast_1d(np.asarray(nus, dtype=np.float64)))
     ot = F32 if np.dtype(out_dtype) == np.float32 else F64
-    out = np.zeros((nus.size, n, n), dtype=np.float32 if ot == F32 else np.float64)
+    shape, dt = (nus.size, n, n), (np.float32 if ot == F32 else np.float64)
+    if out is None:
+        out = np.zeros(shape, dtype=dt)
+    elif out.shape != shape or out.dtype != dt or not out.flags.c_contiguous:
+        raise ValueError("pairwise_gini: out must be a C-contiguous %s array of shape %s" % (np.dtype(dt), shape))
     _check(lib().gmds_pairwise_gini(_vp(X), _i32(xt), _i32(lx), _i64(n), _i64(p), _p(nus), _i32(nus.size), _i32(ot),
                                     _vp(out)))
     return out

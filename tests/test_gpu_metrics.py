@@ -270,3 +270,36 @@ def test_merge_path_exact_keys_adversarial():
         iu = np.triu_indices(48, 1)
         big = ref[iu] > 1e-6 * ref.max()
         assert np.max(np.abs(D[iu][big] - ref[iu][big]) / ref[iu][big]) <= 1e-9
+
+
+@pytest.mark.parametrize("case", ["merge", "split", "full"])
+def test_pairwise_pinned_output_pipelined(case):
+    # a pinned destination is filled stripe by stripe during the computation
+    # (copy stream); the result must equal the copy-after path bit for bit
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(5)
+    if case == "merge":  # sparse non-negative fp32, p > 32
+        X = (rng.random((700, 300)) * (rng.random((700, 300)) < 0.2)).astype(np.float32)
+        nus = [2.0, 3.5]
+    elif case == "split":  # dense, small p
+        X = rng.standard_normal((650, 40))
+        nus = [1.5]
+    else:  # dense fp32, p > 512: the all-keys kernel
+        X = rng.standard_normal((300, 600)).astype(np.float32)
+        nus = [2.0]
+    ref = G.pairwise_gini(X, nus)
+    pinned = torch.zeros((len(nus),) + ref.shape[1:], dtype=torch.float64).pin_memory().numpy()
+    got = G.pairwise_gini(X, nus, out=pinned)
+    assert np.array_equal(got, ref)
+    sub = X[:60].astype(np.float64)
+    assert np.max(np.abs(ref[0][:60, :60] - O.pairwise_matrix(sub, nus[0]))) <= 1e-9 * max(1.0, np.max(ref[0]))
+
+
+def test_pairwise_nonfinite_input_device_check():
+    X = np.ones((50, 10))
+    X[7, 3] = np.nan
+    with pytest.raises(G.InvalidInput, match="non-finite input"):
+        G.pairwise_gini(X, [2.0])
+    X[7, 3] = np.inf
+    with pytest.raises(G.InvalidInput, match="non-finite input"):
+        G.pairwise_gini(X, [2.0])
