@@ -21,6 +21,7 @@
 
 #include <type_traits>
 
+#include "f32x2.cuh"
 #include "stress_pass.cuh"
 
 namespace gmds {
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
 #pragma unroll
         for (int k = 0; k < Q; ++k) rowsum[hh][x][k] = 0.f;
   }
-  float yj[NCM][kMT][Q];  // this thread's 8 columns, loaded once per block
+  float2 yj2[NCM][kMT / 2][Q];  // this thread's 8 columns as (y, y+1) pairs, loaded once per block
 
   for (int b = 0; b < nblocks; ++b) {
     const int64_t J = J0 + b;
@@ -160,15 +161,17 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
 #pragma unroll
     for (int c = 0; c < NCM; ++c)
 #pragma unroll
-      for (int y = 0; y < kMT; ++y)
+      for (int y = 0; y < kMT; y += 2)
 #pragma unroll
-        for (int k = 0; k < Q; ++k) yj[c][y][k] = (c < nc) ? sYj[c][y * kTG + tj][k] : 0.f;
-    float colacc[GRAD ? kMT : 1][Q];
+        for (int k = 0; k < Q; ++k)
+          yj2[c][y / 2][k] = (c < nc) ? make_float2(sYj[c][y * kTG + tj][k], sYj[c][(y + 1) * kTG + tj][k])
+                                      : make_float2(0.f, 0.f);
+    float2 colacc2[GRAD ? kMT / 2 : 1][Q];  // column sums of columns (y, y+1)
     if constexpr (GRAD) {
 #pragma unroll
-      for (int y = 0; y < kMT; ++y)
+      for (int y = 0; y < kMT / 2; ++y)
 #pragma unroll
-        for (int k = 0; k < Q; ++k) colacc[y][k] = 0.f;
+        for (int k = 0; k < Q; ++k) colacc2[y][k] = make_float2(0.f, 0.f);
     }
     const int64_t blk = blk_index(I, J, a.nb);
     const bool edge = (I == J) || (J * kPT + kPT > a.n);
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
               float d2 = 0.f;
 #pragma unroll
               for (int k = 0; k < Q; ++k) {
-                dy[k] = yi[c][k] - yj[c][y][k];
+                dy[k] = yi[c][k] - ((y & 1) ? yj2[c][y / 2][k].y : yj2[c][y / 2][k].x);
                 d2 = fmaf(dy[k], dy[k], d2);
               }
               const float inv = rsqrtf(fmaxf(d2, FLT_MIN));
@@ -229,14 +232,65 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
                   rowsum[half][x][k] = fmaf(cc, dy[k], rowsum[half][x][k]);
-                  colacc[y][k] = fmaf(-cc, dy[k], colacc[y][k]);
+                  float& ca = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
+                  ca = fmaf(-cc, dy[k], ca);
                 }
               }
             }
           }
         };
+        // Kruskal / Guttman, interior, unweighted: two pairs (y, y+1) per
+        // FADD2 / FMUL2 / FFMA2, bare MUFU.RSQ on d2 seeded with FLT_MIN (so no
+        // clamp: coincident points give dy = 0 and add exactly 0)
+        auto pairs_packed = [&]() {
+          constexpr bool KR = (KIND == kKruskal);
+          const float2 dvp[kMT / 2] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
+                                       make_float2(v1.z, v1.w)};
+#pragma unroll
+          for (int c = 0; c < NCM; ++c) {
+            if (c >= nc) break;
+            float2 yi2[Q];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) yi2[k] = make_float2(yi[c][k], yi[c][k]);
+            float2 lacc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int yy = 0; yy < kMT / 2; ++yy) {
+              float2 dy2[Q];
+              float2 d2 = make_float2(FLT_MIN, FLT_MIN);
+#pragma unroll
+              for (int k = 0; k < Q; ++k) {
+                dy2[k] = f2sub(yi2[k], yj2[c][yy][k]);
+                d2 = f2fma(dy2[k], dy2[k], d2);
+              }
+              const float2 inv = make_float2(rsqrt_mufu(d2.x), rsqrt_mufu(d2.y));
+              const float2 dist = f2mul(d2, inv);
+              const float2 e = f2sub(dvp[yy], dist);
+              lacc = f2fma(e, e, lacc);  // kruskal and guttman: term = e^2
+              if constexpr (GRAD) {
+                // row += c dy, column -= c dy with kruskal c = -e/dist = -u,
+                // guttman c = D/dist = u
+                const float2 u = KR ? f2mul(e, inv) : f2mul(dvp[yy], inv);
+#pragma unroll
+                for (int k = 0; k < Q; ++k) {
+                  if constexpr (KR) {
+                    rowsum[half][x][k] = fmaf(-u.x, dy2[k].x, rowsum[half][x][k]);
+                    rowsum[half][x][k] = fmaf(-u.y, dy2[k].y, rowsum[half][x][k]);
+                    colacc2[yy][k] = f2fma(u, dy2[k], colacc2[yy][k]);
+                  } else {
+                    rowsum[half][x][k] = fmaf(u.x, dy2[k].x, rowsum[half][x][k]);
+                    rowsum[half][x][k] = fmaf(u.y, dy2[k].y, rowsum[half][x][k]);
+                    colacc2[yy][k] = f2sub(colacc2[yy][k], f2mul(u, dy2[k]));
+                  }
+                }
+              }
+            }
+            lossrow[c] += lacc.x + lacc.y;
+          }
+        };
         if (edge)
           pairs(std::true_type{});
+        else if ((KIND == kKruskal || KIND == kGuttman) && !Wb)
+          pairs_packed();
         else
           pairs(std::false_type{});
 #pragma unroll
@@ -250,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
       for (int k = 0; k < Q; ++k) {
         if (k > 0) __syncthreads();
 #pragma unroll
-        for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = colacc[y][k];
+        for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
         __syncthreads();
         if (tid < kPT) {
           float s = 0.f;
