@@ -209,6 +209,39 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
   return out;
 }
 
+Engine::GradTrials Engine::grad_and_trials(int kind, double delta, double s0, double s1) {
+  if (q > 64) fail(GMDS_INVALID_INPUT, "stress gradient: embedding dimension above 64 is not supported");
+  PassArgs a = args(kind, delta);
+  a.Y[0] = Y.get();
+  a.ncand = 1;
+  launch_stress_pass(a, Q, true, D->storage, st);
+  if (!rows_mode)
+    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
+  else
+    GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
+  const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
+                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sqpart.get(), scal.get(), st);
+  PassArgs b = args(kind, delta);
+  b.Y[0] = cand[0].get();
+  b.Y[1] = cand[1].get();
+  b.ncand = 2;
+  launch_stress_pass(b, Q, false, D->storage, st);
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, 2, scal.get() + 1, st);
+  double h[3];
+  std::vector<double> sq(static_cast<size_t>(nsq));
+  GMDS_CUDA(cudaMemcpyAsync(h, scal.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(sq.data(), sqpart.get(), nsq * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  passes += 2;
+  GradTrials r;
+  r.raw = h[0];
+  r.trial[0] = h[1];
+  r.trial[1] = h[2];
+  r.gsq = 0.0;
+  for (double v : sq) r.gsq += v;  // fixed order
+  return r;
+}
+
 double Engine::scale_grad(double scale) {
   launch_scale_sqnorm(graw.get(), n * Q, scale, scal.get() + 4, sqpart.get(), st);
   double gsq = 0.0;
@@ -343,29 +376,26 @@ struct IterResult {
 IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double rel_tol) {
   IterResult r;
   const int kind = rp.kind;
+  // One host round trip per iteration in the common case: the gradient pass,
+  // the scale, |g|^2 and the first trial pair (step, step/2) are queued
+  // together (Engine::grad_and_trials).  Further halvings, when neither is
+  // accepted, are loss-only passes of four (fp64) or two (fp32) trial points.
   // (A variant carrying both trial gradients in the trial pass was measured at
   // 800 us per pass vs 333 + 239 us for separate gradient and loss passes at
   // n = 20000, so trial passes compute losses only.)
   double* Yc[kMaxCand];
-  // f = loss_value(coords) and the first gradient come from one pass
-  double raw = E.grad_raw(kind, rp.delta, E.Y.get());
-  double f = E.loss_of(kind, raw);
-  r.history.push_back(f);
-  bool have_grad = true;
+  double f = 0.0;
   double step = 1.0;
   constexpr double armijo = 1e-4;
   int it = 0;
   bool stalled = false;
   for (; it < max_iters; ++it) {
-    if (!have_grad) raw = E.grad_raw(kind, rp.delta, E.Y.get());
-    double scale = 1.0;
-    if (kind == kKruskal) {
-      const double ks = std::sqrt(raw / E.D->sum_sq);
-      scale = (ks <= 0.0) ? 0.0 : 1.0 / (ks * E.D->sum_sq);  // embed.cpp:179-181
-    } else if (kind == kSammon) {
-      scale = 2.0 * (1.0 / E.D->sum);  // q = -2 * scale * e / D
+    const Engine::GradTrials gt = E.grad_and_trials(kind, rp.delta, step, step * 0.5);
+    if (it == 0) {
+      f = E.loss_of(kind, gt.raw);  // f = loss_value(coords) before the loop
+      r.history.push_back(f);
     }
-    const double grad_sq = E.scale_grad(scale);
+    const double grad_sq = gt.gsq;
     if (grad_sq <= 0.0) {
       stalled = true;
       break;
@@ -373,19 +403,26 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     double f_new = f;
     bool accepted = false;
     int acc_c = -1;
-    have_grad = false;
-    for (int halvings = 0; halvings < 60 && !accepted;) {
+    for (int c = 0; c < 2 && !accepted; ++c) {
+      const double sc = (c == 0) ? step : step * 0.5;
+      const double fc = E.loss_of(kind, gt.trial[c]);
+      if (fc <= f - armijo * sc * grad_sq) {
+        accepted = true;
+        acc_c = c;
+        f_new = fc;
+        step = sc;
+      }
+    }
+    if (!accepted) step *= 0.25;
+    for (int halvings = 2; halvings < 60 && !accepted;) {
       Steps s{};
-      // first batch: step and step/2 (the common accept pattern after a doubling);
-      // further batches: loss-only passes, four (fp64) or two (fp32) halvings each
-      const bool first = (halvings == 0);
-      s.n = std::min((first || E.D->storage == GMDS_F32) ? 2 : kMaxCand, 60 - halvings);
+      s.n = std::min(E.D->storage == GMDS_F32 ? 2 : kMaxCand, 60 - halvings);
       double sv = step;
       for (int c = 0; c < s.n; ++c) {
         s.v[c] = sv;
         sv *= 0.5;
       }
-      for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();  // buffers rotate on acceptance
+      for (int c = 0; c < kMaxCand; ++c) Yc[c] = E.cand[c].get();
       launch_axpy_cand(E.Y.get(), E.graw.get(), E.n * E.Q, s, Yc, E.st);
       const std::vector<double> raws = E.loss_raw(kind, rp.delta, Yc, s.n);
       for (int c = 0; c < s.n; ++c) {

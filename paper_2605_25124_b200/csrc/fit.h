@@ -37,6 +37,14 @@ struct Engine {
   double grad_raw_shard(int kind, double delta, const double* Yd, int shard, int nshards);
   // graw *= scale, returns |graw|^2
   double scale_grad(double scale);
+  // One round trip per gradient-descent iteration: gradient pass at Y, the
+  // kind's scale applied on the device, trial points Y - s0 g -> cand[0] and
+  // Y - s1 g -> cand[1], and their loss pass.  Returns raw loss at Y, |g|^2
+  // (scaled g) and the two raw trial losses.
+  struct GradTrials {
+    double raw, gsq, trial[2];
+  };
+  GradTrials grad_and_trials(int kind, double delta, double s0, double s1);
   double loss_of(int kind, double raw) const;
 };
 

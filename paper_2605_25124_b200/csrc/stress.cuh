@@ -42,6 +42,11 @@ void launch_reduce_rows(const double* rowpart, const double* colpart, const int6
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
+// raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;
+// returns the number of partials written to sqpart (<= kSqBlocks)
+int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int kind, double sum_sq, double sum,
+                       double* g, const double* Y, int64_t m, double s0, double s1, double* T0, double* T1,
+                       double* sqpart, double* raw_out, cudaStream_t st);
 void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& s, double* const* outs,
                       cudaStream_t st);
 void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st);

@@ -118,6 +118,54 @@ __global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double sc
   if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 
+// One kernel between the gradient pass and the first trial pass: every block
+// sums the pass's loss partials (same fixed order in every block) to the raw
+// loss at Y, derives the kind's gradient scale exactly as the host would
+// (embed.cpp:179-181 for Kruskal; 2/sum(D) for Sammon; 1 otherwise), scales
+// its slice of g, writes the two trial points Y - s0 g and Y - s1 g, and leaves
+// a per-block partial of |g|^2 (summed in order on the host).
+__global__ void finish_grad_kernel(const double* __restrict__ losspart, int64_t nparts, int stride, int kind,
+                                   double sum_sq, double sum, double* __restrict__ g, const double* __restrict__ Y,
+                                   int64_t m, double s0, double s1, double* __restrict__ T0, double* __restrict__ T1,
+                                   double* __restrict__ sqpart, double* __restrict__ raw_out) {
+  __shared__ double red[256];
+  double r = 0.0;
+  for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) r += losspart[k * stride];
+  red[threadIdx.x] = r;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double raw = red[0];
+  __syncthreads();
+  double scale = 1.0;
+  if (kind == kKruskal) {
+    const double ks = sqrt(raw / sum_sq);
+    scale = (ks <= 0.0) ? 0.0 : 1.0 / (ks * sum_sq);
+  } else if (kind == kSammon) {
+    scale = 2.0 * (1.0 / sum);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *raw_out = raw;
+  double sq = 0.0;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = g[k] * scale;
+    g[k] = v;
+    sq += v * v;
+    const double y = Y[k];
+    T0[k] = y - s0 * v;
+    T1[k] = y - s1 * v;
+  }
+  red[threadIdx.x] = sq;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sqpart[blockIdx.x] = red[0];
+}
+
 // out_c = Y - step_c * G for each candidate (trial = coords - step * grad, embed.cpp:243).
 __global__ void axpy_cand_kernel(const double* __restrict__ Y, const double* __restrict__ G, int64_t m, Steps s,
                                  double* __restrict__ out0, double* __restrict__ out1, double* __restrict__ out2,
@@ -173,6 +221,17 @@ void launch_reduce_rows(const double* rowpart, const double* colpart, const int6
                                                                              q, out);
   count_launch();
   check_launch("reduce_rows_kernel");
+}
+
+int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int kind, double sum_sq, double sum,
+                       double* g, const double* Y, int64_t m, double s0, double s1, double* T0, double* T1,
+                       double* sqpart, double* raw_out, cudaStream_t st) {
+  const int blocks = static_cast<int>(std::min<int64_t>(kSqBlocks, std::max<int64_t>(1, ceil_div(m, 256))));
+  finish_grad_kernel<<<blocks, 256, 0, st>>>(losspart, nparts, stride, kind, sum_sq, sum, g, Y, m, s0, s1, T0, T1,
+                                             sqpart, raw_out);
+  count_launch();
+  check_launch("finish_grad_kernel");
+  return blocks;
 }
 
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st) {
