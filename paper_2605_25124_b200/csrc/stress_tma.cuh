@@ -28,7 +28,8 @@ namespace gmds {
 
 namespace tma_detail {
 
-constexpr int kStages = 2;
+constexpr int kStages = 2;      // loss passes (3 CTAs/SM: 192 KB of stages per SM)
+constexpr int kStagesGrad = 2;  // gradient passes (3 stages measured no faster)
 constexpr int kHalfRows = 64;
 constexpr int kHalfFloats = kHalfRows * kPT;  // 8192 floats = 32 KB
 constexpr int kMR = 4;                        // micro-tile rows per half (ti*4 + x)
@@ -93,11 +94,12 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   // loss passes carry two Armijo trial points; gradient passes one point
   constexpr int NCM = GRAD ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
-  float* ring = reinterpret_cast<float*>(dyn);  // [kStages = 2][kHalfFloats]: stage == half
-  __shared__ __align__(8) uint64_t bars[kStages];
+  constexpr int NS = GRAD ? kStagesGrad : kStages;
+  float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
+  __shared__ __align__(8) uint64_t bars[NS];
   __shared__ float sYi[NCM][kPT][Q];
-  __shared__ float sYj[NCM][kPT][Q];  // [yslot(r)]
-  __shared__ float sRed[GRAD ? kTG * kPT : 1];
+  __shared__ float sYj[2][NCM][kPT][Q];  // [block parity][cand][yslot(r)][k]: double-buffered
+  __shared__ float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   const int tid = threadIdx.x;
@@ -114,19 +116,19 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   const float delta = static_cast<float>(a.huber_delta);
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   auto issue = [&](int h) {
     const int64_t J = J0 + h / 2;
     const float* src = D + blk_index(I, J, a.nb) * (kPT * kPT) + (h & 1) * kHalfFloats;
-    uint64_t* bar = &bars[h & 1];
+    uint64_t* bar = &bars[h % NS];
     mbar_expect_tx(bar, kHalfFloats * 4);
-    bulk_g2s(ring + (h & 1) * kHalfFloats, src, kHalfFloats * 4, bar);
+    bulk_g2s(ring + (h % NS) * kHalfFloats, src, kHalfFloats * 4, bar);
   };
   if (tid == 0)
-    for (int h = 0; h < min(kStages, nhalves); ++h) issue(h);
+    for (int h = 0; h < min(NS, nhalves); ++h) issue(h);
 
   for (int e = tid; e < nc * kPT * Q; e += kThreads) {
     const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
@@ -149,13 +151,16 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   }
   float2 yj2[NCM][kMT / 2][Q];  // this thread's 8 columns as (y, y+1) pairs, loaded once per block
 
+  // Barriers per block: one after the column coordinates are staged (their
+  // buffer alternates, so no barrier is needed before writing it), one per
+  // half to free its stage -- the second also publishes the column partials.
   for (int b = 0; b < nblocks; ++b) {
     const int64_t J = J0 + b;
-    __syncthreads();  // sYj / sRed of the previous block are consumed
+    const int yb = b & 1;
     for (int e = tid; e < nc * kPT * Q; e += kThreads) {
       const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
       const int64_t j = J * kPT + r;
-      sYj[c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+      sYj[yb][c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
       for (int y = 0; y < kMT; y += 2)
 #pragma unroll
         for (int k = 0; k < Q; ++k)
-          yj2[c][y / 2][k] = (c < nc) ? make_float2(sYj[c][y * kTG + tj][k], sYj[c][(y + 1) * kTG + tj][k])
+          yj2[c][y / 2][k] = (c < nc) ? make_float2(sYj[yb][c][y * kTG + tj][k], sYj[yb][c][(y + 1) * kTG + tj][k])
                                       : make_float2(0.f, 0.f);
     float2 colacc2[GRAD ? kMT / 2 : 1][Q];  // column sums of columns (y, y+1)
     if constexpr (GRAD) {
@@ -178,8 +183,9 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
       const int h = 2 * b + half;
-      mbar_wait(&bars[half], static_cast<uint32_t>(b & 1));
-      const float* Ds = ring + half * kHalfFloats;
+      const int stage = h % NS;
+      mbar_wait(&bars[stage], static_cast<uint32_t>((h / NS) & 1));
+      const float* Ds = ring + stage * kHalfFloats;
       const float* Wb = W ? W + blk * (kPT * kPT) + half * kHalfFloats : nullptr;
 #pragma unroll
       for (int x = 0; x < kMR; ++x) {
@@ -296,21 +302,25 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
 #pragma unroll
         for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
       }
-      __syncthreads();  // stage `half` is free
-      if (tid == 0 && h + kStages < nhalves) issue(h + kStages);
+      if constexpr (GRAD) {
+        if (half == 1) {
+#pragma unroll
+          for (int k = 0; k < Q; ++k)
+#pragma unroll
+            for (int y = 0; y < kMT; ++y)
+              sRed[(k * kTG + ti) * kPT + tj * kMT + y] = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
+        }
+      }
+      __syncthreads();  // stage `half` is free (and, after half 1, the column partials are in sRed)
+      if (tid == 0 && h + NS < nhalves) issue(h + NS);
     }
     if constexpr (GRAD) {  // column partials of block J: 16 ti-threads per column, fixed order
+      for (int e = tid; e < kPT * Q; e += kThreads) {
+        const int col = e / Q, k = e % Q;
+        float s = 0.f;
 #pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        if (k > 0) __syncthreads();
-#pragma unroll
-        for (int y = 0; y < kMT; ++y) sRed[ti * kPT + tj * kMT + y] = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
-        __syncthreads();
-        if (tid < kPT) {
-          float s = 0.f;
-          for (int t = 0; t < kTG; ++t) s += sRed[t * kPT + tid];
-          a.colpart[(blk * kPT + tid) * Q + k] = static_cast<double>(s);
-        }
+        for (int t = 0; t < kTG; ++t) s += sRed[(k * kTG + t) * kPT + col];
+        a.colpart[(blk * kPT + col) * Q + k] = static_cast<double>(s);
       }
     }
   }
@@ -342,13 +352,15 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   }
 }
 
-constexpr size_t kTmaSmem = static_cast<size_t>(tma_detail::kStages) * tma_detail::kHalfFloats * 4;
+constexpr size_t kTmaSmemLoss = static_cast<size_t>(tma_detail::kStages) * tma_detail::kHalfFloats * 4;
+constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * tma_detail::kHalfFloats * 4;
 
 #define GMDS_TMA_KIND(QQ, KK)                                                                              \
   case KK:                                                                                                 \
     GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, GRAD, KK>,                                        \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmem))); \
-    stress_tma_kernel<QQ, GRAD, KK><<<g, kThreads, kTmaSmem, st>>>(a);                                      \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,                            \
+                                   static_cast<int>(GRAD ? kTmaSmemGrad : kTmaSmemLoss)));                 \
+    stress_tma_kernel<QQ, GRAD, KK><<<g, kThreads, GRAD ? kTmaSmemGrad : kTmaSmemLoss, st>>>(a);             \
     break;
 #define GMDS_TMA_Q(QQ)                                                                                    \
   case QQ:                                                                                                \

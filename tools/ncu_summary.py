@@ -13,6 +13,10 @@ WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throug
 
 
 def run(rep, page):
+    """rep: an .ncu-rep, or a `--page details --csv` export whose `raw` twin sits
+    beside it (name with 'details' -> 'raw'), as copied back from a GPU box."""
+    if rep.endswith(".csv"):
+        return list(csv.reader(open(rep.replace("details", page))))
     out = subprocess.run(["ncu", "-i", rep, "--page", page, "--csv"], capture_output=True, text=True).stdout
     return list(csv.reader(io.StringIO(out)))
 
