@@ -242,6 +242,32 @@ Engine::GradTrials Engine::grad_and_trials(int kind, double delta, double s0, do
   return r;
 }
 
+Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, double s1) {
+  if (!gnext.get()) gnext.alloc(static_cast<size_t>(n * Q));
+  const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
+                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sqpart.get(), scal.get(), st);
+  PassArgs b = args(kind, delta);
+  b.Y[0] = cand[0].get();
+  b.Y[1] = cand[1].get();
+  b.ncand = 2;
+  launch_pass_fused_f32(b, Q, st);
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st);
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, 2, scal.get() + 1, st);
+  double h[3];
+  std::vector<double> sq(static_cast<size_t>(nsq));
+  GMDS_CUDA(cudaMemcpyAsync(h, scal.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(sq.data(), sqpart.get(), nsq * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  passes += 1;
+  GradTrials r;
+  r.raw = h[0];
+  r.trial[0] = h[1];
+  r.trial[1] = h[2];
+  r.gsq = 0.0;
+  for (double v : sq) r.gsq += v;  // fixed order
+  return r;
+}
+
 double Engine::scale_grad(double scale) {
   launch_scale_sqnorm(graw.get(), n * Q, scale, scal.get() + 4, sqpart.get(), st);
   double gsq = 0.0;
@@ -383,17 +409,43 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
   // (A variant carrying both trial gradients in the trial pass was measured at
   // 800 us per pass vs 333 + 239 us for separate gradient and loss passes at
   // n = 20000, so trial passes compute losses only.)
+  // Speculation (fp32 storage, q <= 4): the trial pass also carries the
+  // gradient at the trial point predicted to be accepted (the same choice,
+  // step or step/2, as the previous iteration -- Armijo acceptance is sticky),
+  // so a correct prediction saves the next iteration's gradient pass: one
+  // pass over D per iteration.  The arithmetic is unchanged; only the order
+  // in which the two trial points sit in the pass differs.
   double* Yc[kMaxCand];
   double f = 0.0;
   double step = 1.0;
   constexpr double armijo = 1e-4;
   int it = 0;
   bool stalled = false;
+  const bool spec = E.fused_ok() && !std::getenv("GMDS_NO_SPECULATION");
+  bool have_grad = false;  // graw holds the raw gradient at Y (speculative mode)
+  int pred = 0;            // 0: step accepted last time, 1: step/2
   for (; it < max_iters; ++it) {
-    const Engine::GradTrials gt = E.grad_and_trials(kind, rp.delta, step, step * 0.5);
-    if (it == 0) {
-      f = E.loss_of(kind, gt.raw);  // f = loss_value(coords) before the loop
-      r.history.push_back(f);
+    Engine::GradTrials gt;
+    int slot_of[2] = {0, 1};  // slot of (step, step/2) in gt.trial / E.cand
+    if (spec) {
+      if (!have_grad) {
+        const double raw0 = E.grad_raw(kind, rp.delta, E.Y.get());
+        if (it == 0) {
+          f = E.loss_of(kind, raw0);  // f = loss_value(coords) before the loop
+          r.history.push_back(f);
+        }
+      }
+      if (pred == 1) {
+        slot_of[0] = 1;
+        slot_of[1] = 0;
+      }
+      gt = E.fused_trials(kind, rp.delta, pred == 0 ? step : step * 0.5, pred == 0 ? step * 0.5 : step);
+    } else {
+      gt = E.grad_and_trials(kind, rp.delta, step, step * 0.5);
+      if (it == 0) {
+        f = E.loss_of(kind, gt.raw);  // f = loss_value(coords) before the loop
+        r.history.push_back(f);
+      }
     }
     const double grad_sq = gt.gsq;
     if (grad_sq <= 0.0) {
@@ -403,16 +455,18 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     double f_new = f;
     bool accepted = false;
     int acc_c = -1;
-    for (int c = 0; c < 2 && !accepted; ++c) {
+    for (int c = 0; c < 2 && !accepted; ++c) {  // step first, then step/2 (the reference's order)
       const double sc = (c == 0) ? step : step * 0.5;
-      const double fc = E.loss_of(kind, gt.trial[c]);
+      const double fc = E.loss_of(kind, gt.trial[slot_of[c]]);
       if (fc <= f - armijo * sc * grad_sq) {
         accepted = true;
-        acc_c = c;
+        acc_c = slot_of[c];
         f_new = fc;
         step = sc;
+        pred = c;
       }
     }
+    if (spec) have_grad = accepted && acc_c == 0;  // the fused pass computed the gradient at cand[0]
     if (!accepted) step *= 0.25;
     for (int halvings = 2; halvings < 60 && !accepted;) {
       Steps s{};
@@ -443,6 +497,7 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
       break;
     }
     std::swap(E.Y, E.cand[acc_c]);
+    if (have_grad) std::swap(E.graw, E.gnext);
     r.history.push_back(f_new);
     const double decrease = (f - f_new) / std::max(f, kTiny);
     f = f_new;

@@ -45,6 +45,14 @@ struct Engine {
     double raw, gsq, trial[2];
   };
   GradTrials grad_and_trials(int kind, double delta, double s0, double s1);
+  // Speculative variant (fp32 storage, q <= 4): with graw holding the raw
+  // gradient at Y (and losspart column 0 the raw loss at Y), scale it, form
+  // cand[0] = Y - s0 g and cand[1] = Y - s1 g, and in ONE pass over D get both
+  // trial losses plus the raw gradient at cand[0] (into gnext; losspart column
+  // 0 then holds the raw loss at cand[0]).
+  bool fused_ok() const { return D->storage == GMDS_F32 && !rows_mode; }
+  GradTrials fused_trials(int kind, double delta, double s0, double s1);
+  DevBuf<double> gnext;
   double loss_of(int kind, double raw) const;
 };
 

@@ -40,6 +40,8 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
                         int64_t nb, int q, double* out, cudaStream_t st);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
+// fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass
+void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 // raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;

@@ -88,11 +88,14 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 
 }  // namespace tma_detail
 
-template <int Q, bool GRAD, int KIND>
-__global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(PassArgs a) {
+// MODE 0: loss of up to two trial points; 1: loss + gradient at one point;
+// 2 (fused): loss of two trial points + gradient at the first (the predicted
+// Armijo acceptance, so the next iteration usually needs no gradient pass).
+template <int Q, int MODE, int KIND>
+__global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
-  // loss passes carry two Armijo trial points; gradient passes one point
-  constexpr int NCM = GRAD ? 1 : kTmaCand;
+  constexpr bool GRAD = (MODE != 0);  // gradient accumulation (of configuration 0)
+  constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
   constexpr int NS = GRAD ? kStagesGrad : kStages;
   float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
   const int64_t J1 = min(J0 + a.chunk_len, a.nb);
   const int nblocks = static_cast<int>(J1 - J0);
   const int nhalves = 2 * nblocks;
-  const int nc = GRAD ? 1 : a.ncand;
+  const int nc = (MODE == 1) ? 1 : a.ncand;
   const float* __restrict__ D = static_cast<const float*>(a.D);
   const float* __restrict__ W = static_cast<const float*>(a.W);
   const float delta = static_cast<float>(a.huber_delta);
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
               }
               lossrow[c] += term;
               if constexpr (GRAD) {
+                if (c != 0) continue;
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
                   rowsum[half][x][k] = fmaf(cc, dy[k], rowsum[half][x][k]);
@@ -273,6 +277,7 @@ __global__ void __launch_bounds__(kThreads, GRAD ? 2 : 3) stress_tma_kernel(Pass
               const float2 e = f2sub(dvp[yy], dist);
               lacc = f2fma(e, e, lacc);  // kruskal and guttman: term = e^2
               if constexpr (GRAD) {
+                if (c != 0) continue;
                 // row += c dy, column -= c dy with kruskal c = -e/dist = -u,
                 // guttman c = D/dist = u
                 const float2 u = KR ? f2mul(e, inv) : f2mul(dvp[yy], inv);
@@ -357,10 +362,10 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
 
 #define GMDS_TMA_KIND(QQ, KK)                                                                              \
   case KK:                                                                                                 \
-    GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, GRAD, KK>,                                        \
+    GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, MODE, KK>,                                        \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,                            \
-                                   static_cast<int>(GRAD ? kTmaSmemGrad : kTmaSmemLoss)));                 \
-    stress_tma_kernel<QQ, GRAD, KK><<<g, kThreads, GRAD ? kTmaSmemGrad : kTmaSmemLoss, st>>>(a);             \
+                                   static_cast<int>(MODE ? kTmaSmemGrad : kTmaSmemLoss)));                 \
+    stress_tma_kernel<QQ, MODE, KK><<<g, kThreads, MODE ? kTmaSmemGrad : kTmaSmemLoss, st>>>(a);             \
     break;
 #define GMDS_TMA_Q(QQ)                                                                                    \
   case QQ:                                                                                                \
@@ -370,10 +375,23 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
       default: fail(GMDS_ERROR, "stress pass: bad kind");                                                 \
     }                                                                                                     \
     break;
+#define GMDS_TMA_SWITCH                                                                                   \
+    const unsigned g = static_cast<unsigned>(a.nchunks);                                                  \
+    switch (Q) {                                                                                          \
+      GMDS_TMA_Q(1) GMDS_TMA_Q(2) GMDS_TMA_Q(3) GMDS_TMA_Q(4)                                             \
+      default: fail(GMDS_ERROR, "stress pass: unsupported padded dimension");                             \
+    }
+#define GMDS_INSTANTIATE_TMA_FUSED                                                                        \
+  void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st) {                                 \
+    constexpr int MODE = 2;                                                                               \
+    GMDS_TMA_SWITCH                                                                                       \
+    count_launch();                                                                                       \
+    check_launch("stress_tma_kernel (fused)");                                                            \
+  }
 #define GMDS_INSTANTIATE_TMA(GR)                                                                          \
   template <>                                                                                             \
   void launch_pass_td<float, GR>(const PassArgs& a, int Q, cudaStream_t st) {                              \
-    constexpr bool GRAD = GR;                                                                             \
+    constexpr int MODE = GR ? 1 : 0;                                                                      \
     const unsigned g = static_cast<unsigned>(a.nchunks);                                                  \
     switch (Q) {                                                                                          \
       GMDS_TMA_Q(1) GMDS_TMA_Q(2) GMDS_TMA_Q(3) GMDS_TMA_Q(4)                                             \

@@ -331,3 +331,25 @@ def test_minimize_stress_subspace_classical_init(monkeypatch):
     ha, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
     assert len(ha) == len(hb)
     assert np.max(np.abs(ha - hb) / ha) <= 1e-8
+
+
+@pytest.mark.parametrize("kind,q", [("kruskal", 2), ("kruskal", 3), ("huber", 2), ("sammon", 1)])
+def test_speculative_trial_gradient_identical(monkeypatch, kind, q):
+    # fp32 storage above the small-fit size: the trial pass also carries the
+    # gradient of the predicted acceptance; the arithmetic per trial point is the
+    # same as separate loss / gradient passes, so trajectories are bit-identical
+    rng = np.random.default_rng(11)
+    n = 2600
+    X = rng.standard_normal((n, 6)) * np.linspace(2.0, 0.5, 6)
+    D = G.pairwise_matrix(X, 2.0)
+    Y0 = rng.normal(0.0, 0.1, (n, q))
+    hd = 0.5 * float(np.median(D)) if kind == "huber" else None
+    a = G.minimize_stress(D, q, kind, huber_delta=hd, max_iters=40, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    monkeypatch.setenv("GMDS_NO_SPECULATION", "1")
+    b = G.minimize_stress(D, q, kind, huber_delta=hd, max_iters=40, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    assert np.array_equal(np.array(a["stress_history"]), np.array(b["stress_history"]))
+    assert np.array_equal(a["coords"], b["coords"])
+    assert a["passes"] < b["passes"]
+    o = O.minimize_stress(D, q, kind, huber_delta=hd, max_iters=10, rel_tol=1e-300, Y0=Y0)
+    h, ho = np.array(a["stress_history"][:11]), np.array(o.stress_history[:11])
+    assert np.max(np.abs(h - ho) / ho) <= TRAJ
