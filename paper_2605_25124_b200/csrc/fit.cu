@@ -87,6 +87,7 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
     stride_col = nblk * kPT * Q;
     rowpart.alloc(static_cast<size_t>(stride_row));
     colpart.alloc(static_cast<size_t>(stride_col));
+    gpart.alloc(reduce_rows_scratch(nb, Q));
     losspart.alloc(static_cast<size_t>(nchunks * kMaxCand));
   } else {
     nchunks = n;
@@ -158,7 +159,7 @@ double Engine::grad_raw(int kind, double delta, const double* Yd) {
   a.ncand = 1;
   launch_stress_pass(a, Q, true, D->storage, st);
   if (!rows_mode)
-    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
+    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get());
   else
     GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
@@ -200,7 +201,7 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
   a.rowpart = rowpart.get() + c0 * kPT * Q;
   a.losspart = losspart.get() + c0 * kMaxCand;
   if (a.nchunks > 0) launch_stress_pass(a, Q, true, D->storage, st);
-  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get());
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
   double out = 0.0;
   GMDS_CUDA(cudaMemcpyAsync(&out, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -216,7 +217,7 @@ Engine::GradTrials Engine::grad_and_trials(int kind, double delta, double s0, do
   a.ncand = 1;
   launch_stress_pass(a, Q, true, D->storage, st);
   if (!rows_mode)
-    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st);
+    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get());
   else
     GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
   const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
@@ -251,7 +252,7 @@ Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, doubl
   b.Y[1] = cand[1].get();
   b.ncand = 2;
   launch_pass_fused_f32(b, Q, st);
-  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st);
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get());
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 2, scal.get() + 1, st);
   double h[3];
   std::vector<double> sq(static_cast<size_t>(nsq));

@@ -53,6 +53,7 @@ struct Engine {
   bool fused_ok() const { return D->storage == GMDS_F32 && !rows_mode; }
   GradTrials fused_trials(int kind, double delta, double s0, double s1);
   DevBuf<double> gnext;
+  DevBuf<double> gpart;  // two-level row reduction scratch
   double loss_of(int kind, double raw) const;
 };
 

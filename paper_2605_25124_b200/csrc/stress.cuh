@@ -37,8 +37,10 @@ struct Steps {
 };
 
 void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage, cudaStream_t st);
+// gpart (reduce_rows_scratch(nb, q) doubles): the two-level reduction; nullptr: one-level
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
-                        int64_t nb, int q, double* out, cudaStream_t st);
+                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart = nullptr);
+size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass
 void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st);

@@ -80,6 +80,40 @@ __global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const dou
   if (live && sub == 0) out[e] = s;
 }
 
+// Two-level version of the same sums, bandwidth-friendly: CTA (R, s) adds
+// group s of strip R's terms (its chunks' row partials, then the column
+// partials of blocks (I, R), I <= R) for all 128 x Q entries at once -- every
+// term is a contiguous 128 x Q run, read coalesced -- and combine_kernel adds
+// the kRedGroups group sums of each entry in order.  Fixed order throughout.
+constexpr int kRedGroups = 8;
+__global__ void reduce_groups_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+                                     const int64_t* __restrict__ strip_first, int64_t nb, int Q,
+                                     double* __restrict__ gpart) {
+  const int64_t R = blockIdx.x / kRedGroups;
+  const int s = blockIdx.x % kRedGroups;
+  const int64_t c0 = strip_first[R], nrow = strip_first[R + 1] - c0;
+  const int64_t T = nrow + R + 1;
+  const int64_t t0 = T * s / kRedGroups, t1 = T * (s + 1) / kRedGroups;
+  const int e = threadIdx.x;  // (rr, k), < 128 Q
+  const int64_t run = static_cast<int64_t>(kPT) * Q;
+  double acc = 0.0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const double* src = (t < nrow) ? rowpart + (c0 + t) * run : colpart + blk_index(t - nrow, R, nb) * run;
+    acc += src[e];
+  }
+  gpart[(R * kRedGroups + s) * run + e] = acc;
+}
+__global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int Q, double* __restrict__ out) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n * Q) return;
+  const int64_t r = idx / Q, R = r / kPT;
+  const int64_t e = (r % kPT) * Q + idx % Q, run = static_cast<int64_t>(kPT) * Q;
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < kRedGroups; ++s) acc += gpart[(R * kRedGroups + s) * run + e];
+  out[idx] = acc;
+}
+
 // Deterministic single-CTA sums: out[c] = sum_k part[k*stride + c] for c < m.
 __global__ void sum_parts_kernel(const double* __restrict__ part, int64_t count, int stride, int m,
                                  double* __restrict__ out) {
@@ -215,13 +249,25 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
 }
 
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
-                        int64_t nb, int q, double* out, cudaStream_t st) {
+                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart) {
+  if (gpart) {
+    reduce_groups_kernel<<<static_cast<unsigned>(nb * kRedGroups), kPT * q, 0, st>>>(rowpart, colpart, strip_first,
+                                                                                    nb, q, gpart);
+    count_launch();
+    check_launch("reduce_groups_kernel");
+    combine_kernel<<<static_cast<unsigned>(ceil_div(n * q, 256)), 256, 0, st>>>(gpart, n, q, out);
+    count_launch();
+    check_launch("combine_kernel");
+    return;
+  }
   const int64_t m = n * q * 8;
   reduce_rows_kernel<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, st>>>(rowpart, colpart, strip_first, n, nb,
                                                                              q, out);
   count_launch();
   check_launch("reduce_rows_kernel");
 }
+
+size_t reduce_rows_scratch(int64_t nb, int q) { return static_cast<size_t>(nb) * kRedGroups * kPT * q; }
 
 int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int kind, double sum_sq, double sum,
                        double* g, const double* Y, int64_t m, double s0, double s1, double* T0, double* T1,
