@@ -160,6 +160,58 @@ __device__ __forceinline__ void warp_merge_u32(uint32_t (&v)[K], int lane) {
   }
 }
 
+// Tie groups of the merged halves (lanes 0-15 negatives, 16-31 positives),
+// as warp_tie_groups but with a group start forced at slot H: a negative can
+// never tie a positive, even when a full negative half's last code equals the
+// positive half's first code numerically.  (A "no ties in this pair" fast
+// path was measured slower on the metric data, whose clipped values tie often.)
+template <int K>
+__device__ __forceinline__ void merge_tie_groups(const uint32_t (&v)[K], int (&h)[K], int lane) {
+  const int l16 = lane & 15;
+  const uint32_t prev_last = __shfl_up_sync(kFull, v[K - 1], 1);
+  int start_pos[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const uint32_t prev = (r == 0) ? prev_last : v[r - 1];
+    const bool st = (r == 0 && l16 == 0) ? true : (v[r] != prev);
+    start_pos[r] = st ? (lane * K + r) : -1;
+  }
+  int run = -1;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    run = max(run, start_pos[r]);
+    h[r] = run;
+  }
+  int carry = run;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(kFull, carry, d);
+    if (lane >= d) carry = max(carry, o);
+  }
+  int excl = __shfl_up_sync(kFull, carry, 1);
+  if (lane == 0) excl = -1;
+#pragma unroll
+  for (int r = 0; r < K; ++r) h[r] = max(h[r], excl);
+  constexpr int N = 32 * K;
+  int runb = N;
+  int bpos[K];
+#pragma unroll
+  for (int r = K - 1; r >= 0; --r) {
+    bpos[r] = runb;
+    runb = min(runb, (start_pos[r] >= 0) ? start_pos[r] : N);
+  }
+  int carryb = runb;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_down_sync(kFull, carryb, d);
+    if (lane + d < 32) carryb = min(carryb, o);
+  }
+  int exclb = __shfl_down_sync(kFull, carryb, 1);
+  if (lane == 31) exclb = N;
+#pragma unroll
+  for (int r = 0; r < K; ++r) h[r] += min(bpos[r], exclb);
+}
+
 template <int K>
 __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint32_t* B32, const double* RA,
                                                  const double* RB, int cn, int mneg, int cp, int mpos, int zeros,
@@ -197,8 +249,8 @@ __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint
   __syncwarp();
   warp_merge_u32<K>(key, lane);
   int h[K];
-  warp_tie_groups<K>(key, h, lane);
   const int n_neg = cn + mneg, n_pos = cp + mpos;
+  merge_tie_groups<K>(key, h, lane);
   const int shiftB = 2 * (n_neg + zeros) - 2 * H;
   // values: +-f from the key, plus the residual of inexact (odd-code) S_ab keys
   int nodd = 0;
