@@ -225,19 +225,19 @@ __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint
   const int head = hiB ? cp : cn;
   const int tail = H - (hiB ? mpos : mneg);
   if constexpr (K >= 4) {
-    // pad the gap between the head (compacted row-only keys) and the tail
-    // (sorted S_ab keys) so the blocked reads are unconditional 16-byte loads
-    uint32_t* dst = const_cast<uint32_t*>(src);
-    for (int e = head + l16; e < tail; e += 16) dst[e] = 0xFFFFFFFFu;
-    __syncwarp();
+    // blocked 16-byte reads; the gap between the head (compacted row-only
+    // keys) and the tail (sorted S_ab keys) is replaced by the pad key through
+    // a per-lane slot mask
+    const int lo = min(max(head - l16 * K, 0), K), hi = min(max(tail - l16 * K, 0), K);
+    const uint32_t gapm = (hi > lo) ? (((K >= 32 ? 0u : (1u << hi)) - 1u) & ~((1u << lo) - 1u)) : 0u;
     const uint4* s4 = reinterpret_cast<const uint4*>(src + l16 * K);
 #pragma unroll
     for (int m = 0; m < K / 4; ++m) {
       const uint4 v = s4[m];
-      key[4 * m] = v.x;
-      key[4 * m + 1] = v.y;
-      key[4 * m + 2] = v.z;
-      key[4 * m + 3] = v.w;
+      key[4 * m] = ((gapm >> (4 * m)) & 1u) ? 0xFFFFFFFFu : v.x;
+      key[4 * m + 1] = ((gapm >> (4 * m + 1)) & 1u) ? 0xFFFFFFFFu : v.y;
+      key[4 * m + 2] = ((gapm >> (4 * m + 2)) & 1u) ? 0xFFFFFFFFu : v.z;
+      key[4 * m + 3] = ((gapm >> (4 * m + 3)) & 1u) ? 0xFFFFFFFFu : v.w;
     }
   } else {
 #pragma unroll
@@ -251,33 +251,34 @@ __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint
   int h[K];
   const int n_neg = cn + mneg, n_pos = cp + mpos;
   merge_tie_groups<K>(key, h, lane);
-  const int shiftB = 2 * (n_neg + zeros) - 2 * H;
-  // values: +-f from the key, plus the residual of inexact (odd-code) S_ab keys
-  int nodd = 0;
+  // values: +-f from the key (negatives: complemented code, sign bit set), plus
+  // the residual of inexact (odd-code) S_ab keys; per-lane constants hoisted
+  const uint32_t flip = hiB ? 0u : 0xFFFFFFFFu;
+  const uint32_t sgn = hiB ? 0u : 0x80000000u;
+  const int lim = (hiB ? n_pos : n_neg) - l16 * K;  // slot r is real iff r < lim
+  const int hadd = hiB ? 2 * (n_neg + zeros) - 2 * H : 0;
+  uint32_t oddm = 0;  // bit r: real slot with an inexact (odd) code
   double z[K];
 #pragma unroll
   for (int r = 0; r < K; ++r) {
-    const int g = lane * K + r;
-    const bool real = hiB ? (g - H < n_pos) : (g < n_neg);
-    const uint32_t code = hiB ? key[r] : 0xFFFFFFFFu - key[r];
-    const double f = static_cast<double>(__uint_as_float(code >> 1));
-    z[r] = hiB ? f : -f;
-    h[r] = real ? (hiB ? h[r] + shiftB : h[r]) : -1;
-    nodd += (real && (code & 1u)) ? 1 : 0;
+    const uint32_t code = key[r] ^ flip;
+    z[r] = static_cast<double>(__uint_as_float((code >> 1) | sgn));
+    const bool real = r < lim;
+    h[r] = real ? h[r] + hadd : -1;
+    oddm |= (real ? (code & 1u) : 0u) << r;
   }
+  const int nodd = __popc(oddm);
   int incl = nodd;
 #pragma unroll
   for (int dd = 1; dd < 16; dd <<= 1) {
     const int o = __shfl_up_sync(kFull, incl, dd, 16);
     if (l16 >= dd) incl += o;
   }
-  int t = incl - nodd;
+  const int t0 = incl - nodd;
   const double* R = hiB ? RB : RA;
 #pragma unroll
-  for (int r = 0; r < K; ++r) {
-    const uint32_t code = hiB ? key[r] : 0xFFFFFFFFu - key[r];
-    if (h[r] >= 0 && (code & 1u)) z[r] += R[t++];
-  }
+  for (int r = 0; r < K; ++r)
+    if ((oddm >> r) & 1u) z[r] += R[t0 + __popc(oddm & ((1u << r) - 1u))];
   for (int v = 0; v < nnu; ++v) {
     const double* L = lut + static_cast<size_t>(v) * 2 * d;
     double acc = 0.0;
