@@ -565,13 +565,62 @@ DevBuf<double> weights_pinv(const double* weights, int64_t n, cudaStream_t st);
 
 }  // namespace
 
+namespace {
+
+// The reference's bookkeeping after the eigensolver (embed.cpp:428-458): the
+// clamped mass over the full spectrum lam (ascending, n values), then for the
+// top q eigenpairs the sign rule (largest-|v| entry positive, first index
+// wins) and coords = v sqrt(max(lambda, 0)).  V: the top q eigenvectors,
+// column c = the c-th largest.
+void classical_finish(int64_t n, int q, const std::vector<double>& lam, const double* V, double* coords,
+                      double* eigvals, int* clamped_count, double* clamped_mass) {
+  double negative_mass = 0.0, total_mass = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    total_mass += std::abs(lam[i]);
+    if (lam[i] < 0.0) negative_mass += -lam[i];
+  }
+  *clamped_mass = total_mass > 0.0 ? negative_mass / total_mass : 0.0;
+  *clamped_count = 0;
+  for (int c = 0; c < q; ++c) {
+    const double lambda = lam[n - 1 - c];
+    eigvals[c] = lambda;
+    const double* v = V + static_cast<size_t>(c) * n;
+    int64_t arg = 0;
+    double best = std::abs(v[0]);
+    for (int64_t i = 1; i < n; ++i)
+      if (std::abs(v[i]) > best) {
+        best = std::abs(v[i]);
+        arg = i;
+      }
+    const double sgn = (v[arg] < 0.0) ? -1.0 : 1.0;
+    if (lambda < 0.0) ++*clamped_count;
+    const double sc = std::sqrt(std::max(lambda, 0.0));
+    for (int64_t i = 0; i < n; ++i) coords[static_cast<size_t>(c) * n + i] = (sgn * v[i]) * sc;
+  }
+}
+
+void check_classical_q(int64_t n, int q) {
+  if (q < 1 || q > n - 1)
+    fail(GMDS_INVALID_INPUT, "classical_mds: target dimension must satisfy 1 <= p <= n-1, got p=" +
+                                 std::to_string(q) + " with n=" + std::to_string(n));
+}
+
+double kruskal_at(const gmds_dmat* D, const double* coords, int q, cudaStream_t st) {
+  if (!(D->sum_sq > 0.0)) return 0.0;
+  EngineLease L = acquire_engine(D, q, st);
+  Engine& E = *L;
+  E.upload(coords, E.Y.get());
+  const double* y = E.Y.get();
+  return E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
+}
+
+}  // namespace
+
 // classical_mds (embed.cpp:415-460)
 void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigvals, int* clamped_count,
                        double* clamped_mass, double* stress, cudaStream_t st) {
   const int64_t n = D->n;
-  if (q < 1 || q > n - 1)
-    fail(GMDS_INVALID_INPUT, "classical_mds: target dimension must satisfy 1 <= p <= n-1, got p=" +
-                                 std::to_string(q) + " with n=" + std::to_string(n));
+  check_classical_q(n, q);
   DevBuf<double> B(static_cast<size_t>(n * n));
   unpack_full(D->ptr(), D->storage, n, B.get(), true, st);  // S = D o D
   double_center_dev(B.get(), n, st);
@@ -597,40 +646,68 @@ void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigval
                               cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
   if (hinfo != 0) fail(GMDS_NUMERIC_FAILURE, "classical_mds: eigensolver failed");
-  double negative_mass = 0.0, total_mass = 0.0;
-  for (int64_t i = 0; i < n; ++i) {
-    total_mass += std::abs(lam[i]);
-    if (lam[i] < 0.0) negative_mass += -lam[i];
+  classical_finish(n, q, lam, V.data(), coords, eigvals, clamped_count, clamped_mass);
+  if (stress) *stress = kruskal_at(D, coords, q, st);
+}
+
+// classical_mds of several same-size matrices (the grid cells of one tune_nu
+// fold): one batched eigensolver call (cusolverDnXsyevBatched) instead of one
+// dense solve per cell.  Results per matrix as classical_mds_dev; false when
+// the batched solver is not available for this size (caller goes one by one).
+bool classical_mds_batch_dev(const std::vector<const gmds_dmat*>& Ds, int q, std::vector<std::vector<double>>& coords,
+                             std::vector<double>& stress, cudaStream_t st) {
+  const int64_t n = Ds[0]->n;
+  check_classical_q(n, q);
+  const int64_t bs = static_cast<int64_t>(Ds.size());
+  const size_t nn = static_cast<size_t>(n) * n;
+  DevBuf<double> B(nn * bs), w(static_cast<size_t>(n * bs));
+  for (int64_t b = 0; b < bs; ++b) {
+    unpack_full(Ds[b]->ptr(), Ds[b]->storage, n, B.get() + b * nn, true, st);
+    double_center_dev(B.get() + b * nn, n, st);
   }
-  *clamped_mass = total_mass > 0.0 ? negative_mass / total_mass : 0.0;
-  *clamped_count = 0;
-  for (int c = 0; c < q; ++c) {
-    const double lambda = lam[n - 1 - c];
-    eigvals[c] = lambda;
-    double* v = V.data() + static_cast<size_t>(c) * n;
-    int64_t arg = 0;
-    double best = std::abs(v[0]);
-    for (int64_t i = 1; i < n; ++i)
-      if (std::abs(v[i]) > best) {
-        best = std::abs(v[i]);
-        arg = i;
-      }
-    const double sgn = (v[arg] < 0.0) ? -1.0 : 1.0;
-    if (lambda < 0.0) ++*clamped_count;
-    const double sc = std::sqrt(std::max(lambda, 0.0));
-    for (int64_t i = 0; i < n; ++i) coords[static_cast<size_t>(c) * n + i] = (sgn * v[i]) * sc;
+  cusolverDnHandle_t h = solver_handle(st);
+  cusolverDnParams_t params = nullptr;
+  if (cusolverDnCreateParams(&params) != CUSOLVER_STATUS_SUCCESS) return false;
+  struct P {
+    cusolverDnParams_t p;
+    ~P() { cusolverDnDestroyParams(p); }
+  } pg{params};
+  size_t dws = 0, hws = 0;
+  if (cusolverDnXsyevBatched_bufferSize(h, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F,
+                                        B.get(), n, CUDA_R_64F, w.get(), CUDA_R_64F, &dws, &hws,
+                                        bs) != CUSOLVER_STATUS_SUCCESS)
+    return false;
+  DevBuf<unsigned char> dwork(std::max<size_t>(dws, 1));
+  std::vector<unsigned char> hwork(std::max<size_t>(hws, 1));
+  DevBuf<int> info(static_cast<size_t>(bs));
+  if (cusolverDnXsyevBatched(h, params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, B.get(), n,
+                             CUDA_R_64F, w.get(), CUDA_R_64F, dwork.get(), dws, hwork.data(), hws, info.get(),
+                             bs) != CUSOLVER_STATUS_SUCCESS)
+    return false;
+  count_launch();
+  std::vector<int> hinfo(static_cast<size_t>(bs));
+  std::vector<double> lam(static_cast<size_t>(n * bs));
+  std::vector<double> V(static_cast<size_t>(n) * q * bs);
+  GMDS_CUDA(cudaMemcpyAsync(hinfo.data(), info.get(), bs * sizeof(int), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaMemcpyAsync(lam.data(), w.get(), lam.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  for (int64_t b = 0; b < bs; ++b)
+    for (int c = 0; c < q; ++c)
+      GMDS_CUDA(cudaMemcpyAsync(V.data() + (static_cast<size_t>(b) * q + c) * n, B.get() + b * nn + (n - 1 - c) * n,
+                                n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  for (int64_t b = 0; b < bs; ++b)
+    if (hinfo[b] != 0) fail(GMDS_NUMERIC_FAILURE, "classical_mds: eigensolver failed");
+  coords.assign(static_cast<size_t>(bs), std::vector<double>(static_cast<size_t>(n) * q));
+  stress.assign(static_cast<size_t>(bs), 0.0);
+  std::vector<double> ev(static_cast<size_t>(q));
+  for (int64_t b = 0; b < bs; ++b) {
+    const std::vector<double> lb(lam.begin() + b * n, lam.begin() + (b + 1) * n);
+    int cc = 0;
+    double cm = 0.0;
+    classical_finish(n, q, lb, V.data() + static_cast<size_t>(b) * q * n, coords[b].data(), ev.data(), &cc, &cm);
+    stress[b] = kruskal_at(Ds[b], coords[b].data(), q, st);
   }
-  if (stress) {
-    if (D->sum_sq > 0.0) {
-      EngineLease L = acquire_engine(D, q, st);
-      Engine& E = *L;
-      E.upload(coords, E.Y.get());
-      const double* y = E.Y.get();
-      *stress = E.loss_of(kKruskal, E.loss_raw(kKruskal, 0.0, &y, 1)[0]);
-    } else {
-      *stress = 0.0;
-    }
-  }
+  return true;
 }
 
 namespace {

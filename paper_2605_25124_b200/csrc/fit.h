@@ -78,6 +78,8 @@ EngineLease acquire_engine(const gmds_dmat* D, int q, cudaStream_t st);
 void dmat_finish(gmds_dmat* d, cudaStream_t st);
 void classical_mds_dev(const gmds_dmat* D, int q, double* coords, double* eigvals, int* clamped_count,
                        double* clamped_mass, double* stress, cudaStream_t st);
+bool classical_mds_batch_dev(const std::vector<const gmds_dmat*>& Ds, int q, std::vector<std::vector<double>>& coords,
+                             std::vector<double>& stress, cudaStream_t st);
 void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, const double* Y0, gmds_fit_result* res,
                          cudaStream_t st, const double* init_cache);
 

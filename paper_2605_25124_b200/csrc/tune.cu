@@ -8,6 +8,7 @@
 // smaller nu, refit) follows the reference line by line.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -211,12 +212,32 @@ gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n
       if (nf < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
       DevBuf<double> dX = upload_f64(Xf, st.s);
       const auto Ds = gini_multi(dX.get(), GMDS_F64, nf, p, grid, m, st.s);
+      std::vector<int> todo;
       for (int g = 0; g < m; ++g) {
-        const gmds_dmat* D = Ds[g].get();
-        if (D->max_val <= 0.0) {  // all points coincide (tune.cpp:106-110)
+        if (Ds[g]->max_val <= 0.0)  // all points coincide (tune.cpp:106-110)
           cell[static_cast<size_t>(g) * k_folds + f] = 0.0;
-          continue;
+        else
+          todo.push_back(g);
+      }
+      if (method == GMDS_M_CLASSICAL && !std::getenv("GMDS_NO_BATCHED_EIG")) {
+        // the fold's grid cells are same-size classical MDS problems: batched
+        // eigensolver, at most ~2 GB of Gram matrices per call
+        const int64_t per = std::max<int64_t>(1, (int64_t(2) << 30) / std::max<int64_t>(1, nf * nf * 8));
+        size_t i0 = 0;
+        while (i0 < todo.size()) {
+          const size_t i1 = std::min(todo.size(), i0 + static_cast<size_t>(per));
+          std::vector<const gmds_dmat*> batch;
+          for (size_t i = i0; i < i1; ++i) batch.push_back(Ds[todo[i]].get());
+          std::vector<std::vector<double>> bc;
+          std::vector<double> bst;
+          if (!classical_mds_batch_dev(batch, q, bc, bst, st.s)) break;
+          for (size_t i = i0; i < i1; ++i) cell[static_cast<size_t>(todo[i]) * k_folds + f] = bst[i - i0];
+          i0 = i1;
         }
+        todo.erase(todo.begin(), todo.begin() + static_cast<std::ptrdiff_t>(i0));
+      }
+      for (const int g : todo) {
+        const gmds_dmat* D = Ds[g].get();
         const Emb e = embed(D, q, method, seed, st.s);
         cell[static_cast<size_t>(g) * k_folds + f] = kruskal_of(D, e.coords.data(), q, st.s);
       }
