@@ -8,7 +8,7 @@ namespace gmds {
   do {                                                                                                       \
     GMDS_CUDA(cudaFuncSetAttribute(gini_merge_kernel<T, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                    static_cast<int>(smem)));                                                 \
-    gini_merge_kernel<T, TO><<<blocks, 512, smem, st>>>(ma, static_cast<const T*>(dX), static_cast<TO*>(dout)); \
+    gini_merge_kernel<T, TO><<<blocks, merge_detail::kMergeThreads, smem, st>>>(ma, static_cast<const T*>(dX), static_cast<TO*>(dout)); \
   } while (0)
 
 void launch_gini_merge(const MergeArgs& ma, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, size_t smem,

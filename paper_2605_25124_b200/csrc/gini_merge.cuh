@@ -29,6 +29,12 @@ struct MergeArgs {
 
 namespace merge_detail {
 
+#ifndef GMDS_MERGE_THREADS
+#define GMDS_MERGE_THREADS 640
+#endif
+// 20 warps per CTA, one CTA per SM (96 registers): measured 724 ms per metric
+// matrix vs 779 ms at 16 warps (126 registers), 773 / 742 / 761 ms at 18 / 24 / 22
+constexpr int kMergeThreads = GMDS_MERGE_THREADS;
 constexpr int kHalfCap = 256;  // max keys per sign half on the merge path
 constexpr int kMCap = 128;     // max |S_ab| on the merge path
 constexpr int kAB32 = 272;     // u32 half buffer (256 keys; 16-byte aligned halves)
@@ -298,7 +304,7 @@ __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint
 
 // 16 warps per CTA on a tile x tile block of pairs (sparse panels + sorted-order index).
 template <typename T, typename TO>
-__global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const T* __restrict__ X, TO* __restrict__ out) {
+__global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_kernel(MergeArgs ma, const T* __restrict__ X, TO* __restrict__ out) {
   using namespace merge_detail;
   using namespace split_detail;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -521,7 +527,7 @@ __global__ void __launch_bounds__(512, 1) gini_merge_kernel(MergeArgs ma, const 
 }
 
 inline size_t merge_smem(int tile, int W, int maxnnz, size_t sz, int nnu) {
-  return static_cast<size_t>(16) * merge_detail::kWarpScratch * 8 + static_cast<size_t>(nnu) * tile * (tile + 1) * 8 +
+  return static_cast<size_t>(merge_detail::kMergeThreads / 32) * merge_detail::kWarpScratch * 8 + static_cast<size_t>(nnu) * tile * (tile + 1) * 8 +
          ((2 * static_cast<size_t>(tile) * W * 6 + 15) & ~static_cast<size_t>(15)) + (2 * tile + 4) * 4 +
          2 * static_cast<size_t>(tile) * maxnnz * (2 * sz + 2) + 16;
 }
