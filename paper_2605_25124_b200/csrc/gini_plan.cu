@@ -176,6 +176,9 @@ size_t split_smem(int tile, int p, int W, int maxnnz, size_t sz, int nnu, bool s
 
 }  // namespace
 
+// CTAs per SM of the split kernel instance p selects (K = 8 for p <= 256)
+inline int split_detail_min_blocks(int64_t p) { return split_min_blocks(p <= 256 ? 8 : 16); }
+
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
               int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score,
               RowSink* sink) {
@@ -280,7 +283,8 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     GMDS_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  const size_t two_per_sm = 113 * 1024, one_per_sm = 220 * 1024;
+  // split kernel: split_min_blocks(K) CTAs per SM (its __launch_bounds__) share ~226 KB of smem
+  const size_t two_per_sm = (split_detail_min_blocks(p) >= 3 ? 74 : 113) * 1024, one_per_sm = 220 * 1024;
   if (sparse && rs.nonneg && p > 32 && xt == GMDS_F32) {  // merge path (exact u32 keys need fp32 inputs): pre-sorted row runs + one bitonic merge per sign half
     int mt = 32;
     while (mt > 4 && merge_smem(mt, rs.W, std::max(1, rs.maxnnz), sz, nnu) > one_per_sm) mt >>= 1;
