@@ -277,6 +277,7 @@ def run_engine(args, rank, world, dist):
             times.append(e0.elapsed_time(e1) / 1e3)
     barrier()
     dist_launches = G.launch_count() - launches0
+    print(f"[bench] distance step times (ms): {[round(t * 1e3, 2) for t in times]}", file=sys.stderr, flush=True)
     t_dist = max_over_ranks(dist, float(np.mean(times)))
 
     # ---- stress: S Kruskal iterations on the packed matrix of this step.  One GPU: the
@@ -315,6 +316,7 @@ def run_engine(args, rank, world, dist):
             siters += r["iterations"]
             spasses += r["passes"]
     stress_launches = G.launch_count() - launches1
+    print(f"[bench] stress step times (ms): {[round(t * 1e3, 2) for t in stimes]}", file=sys.stderr, flush=True)
     t_stress = max_over_ranks(dist, float(np.sum(stimes)))
     iters_per_sec = siters / t_stress
     Dm.free()

@@ -129,8 +129,10 @@ Stream::Stream() {
   } else {
     GMDS_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   }
+  call_stream_push(s, &prev);
 }
 Stream::~Stream() {
+  call_stream_pop(prev);
   if (s && owned) cudaStreamDestroy(s);
 }
 
@@ -379,6 +381,7 @@ gmds_status gmds_pairwise_gini_device(const void* dX, gmds_dtype xt, int64_t n, 
     if (nshards < 1 || shard < 0 || shard >= nshards) fail(GMDS_INVALID_CONFIG, "pairwise_matrix: bad shard");
     require_device();
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CallScope scope(st);
     DevBuf<int> flag(1);
     GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st));
     run_gini(dX, xt, n, p, nus, nnu, out_t, packed, dD, shard, nshards, st, flag.get());

@@ -50,39 +50,55 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 inline size_t dtype_size(gmds_dtype t) { return t == GMDS_F32 ? 4 : 8; }
 
+// Device memory: a caching pool (pool.cu).  Buffers released while a library
+// call is running (a Stream is live on this thread) go back to a per-device
+// free list with an event recorded on the call's stream; a later allocation
+// reuses a block only once that event has completed.  cudaMalloc/cudaFree on
+// every call cost 2-300 ms of host-side stalls at the metric shape (the e2e
+// output alone is 3.2 GB).  Buffers released outside a call, or while an
+// exception unwinds, are returned with cudaFree.
+void* pool_alloc(size_t bytes, size_t* cap);
+void pool_free(void* p, size_t cap);
+void pool_trim();  // return every idle cached block to the driver
+
 // RAII device buffer.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  size_t cap = 0;  // bytes held from the pool
   DevBuf() = default;
   explicit DevBuf(size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) {
     o.p = nullptr;
     o.n = 0;
+    o.cap = 0;
   }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
       p = o.p;
       n = o.n;
+      cap = o.cap;
       o.p = nullptr;
       o.n = 0;
+      o.cap = 0;
     }
     return *this;
   }
   ~DevBuf() { release(); }
   void alloc(size_t count) {
     release();
-    if (count) GMDS_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    if (count) p = static_cast<T*>(pool_alloc(count * sizeof(T), &cap));
     n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) pool_free(p, cap);
     p = nullptr;
     n = 0;
+    cap = 0;
   }
   T* get() const { return p; }
 };

@@ -9,8 +9,24 @@
 
 namespace gmds {
 
+void call_stream_push(cudaStream_t s, cudaStream_t* prev);
+void call_stream_pop(cudaStream_t prev);
+
+// The stream of one library call (the caller's, via gmds_set_stream, or a
+// private one).  While it lives, DevBufs released on this thread return to
+// the pool ordered after this stream's work (pool.cu).
+// A call on a caller-provided stream (the *_device entry points).
+struct CallScope {
+  cudaStream_t prev = nullptr;
+  explicit CallScope(cudaStream_t s) { call_stream_push(s, &prev); }
+  ~CallScope() { call_stream_pop(prev); }
+  CallScope(const CallScope&) = delete;
+  CallScope& operator=(const CallScope&) = delete;
+};
+
 struct Stream {
   cudaStream_t s = nullptr;
+  cudaStream_t prev = nullptr;
   bool owned = true;
   Stream();
   ~Stream();
