@@ -25,6 +25,13 @@ struct MergeArgs {
   SplitArgs s;
   const uint16_t* sidx;  // per row, its nonzero features sorted by value (rowptr layout)
   const void* svs;       // per row, its nonzero values sorted ascending (rowptr layout)
+  int fast;              // try the rank-by-counting path first (GMDS_MERGE_NOFAST=1 disables)
+  int linear;            // every nu is 2 or 3: the linear-weight path (gmd_pair)
+  const uint16_t* pmap;  // row store: sorted position of each nonzero (feature order)
+  const double* suf;     // row store: suffix sums of the sorted values
+  const double* s1;      // per row: sum of its values
+  const double* tm;      // per row: sum_k v_(k) k
+  unsigned long long* fast_miss;  // optional: pairs the fast path handed to the merge path
 };
 
 namespace merge_detail {
@@ -300,6 +307,552 @@ __device__ __forceinline__ void merge_and_finish(const uint32_t* A32, const uint
   }
 }
 
+// ---------------------------------------------------------------------------
+// Rank-by-counting fast path (no merged array at all).
+//
+// With P = S_a u S_ab+ (the positives) and N = S_b u S_ab- (the negatives),
+// the midrank of every element is a COUNT that the pre-sorted rows give
+// directly:
+//   x in S_a  at position k of row i's sorted list (tie group [g0, g1)):
+//     #less  = n_neg + zeros + (g0 - removed_i(g0)) + #{m in S_ab+ : m < x}
+//     #equal = (g1 - g0) - (removed_i(g1) - removed_i(g0))
+//   -x in S_b at position k of row j's sorted list (tie group [g0, g1)):
+//     #less  = #{non-removed row-j entries > x} + #{m in S_ab- : m < -x}
+//   m in S_ab+ (index q in sorted S_ab+):
+//     #less  = n_neg + zeros + q + #{x in S_a : x < m}
+//   m in S_ab- likewise against row j.
+// "removed" = the feature is nonzero in both rows (its z is in S_ab);
+// removed_i(pos) is a popc prefix over the ballot words of the row-i scan.
+// #{m in S_ab+ : m < x_k} = #{q : lb_q <= k} with lb_q = #{row-i values < m_q}
+// (no S_ab value equals a row value on this path), so each S_ab element adds
+// one count at its row position (a per-warp histogram) and the row pass reads
+// it back with a warp scan.  The LUT index of a midrank is 2 #less + #equal
+// (gini_tile.cuh).  Only S_ab is sorted (fp64, exact); all counts are exact
+// integers, so the ranks are those of the sorted difference vector
+// (metrics.cpp:42-56).  The path gives up (returns false, warp-uniform,
+// before touching the histogram) -- and the caller runs the merge path --
+// when an S_ab value equals another S_ab value or any value of its row, two
+// inexact S_ab values share a 32-bit key, or a half of S_ab exceeds kFastCap.
+constexpr int kFastCap = 64;   // max |S_ab+|, |S_ab-| on the fast path (16 * KM, KM <= 4)
+constexpr int kFastNu = 4;     // nu values per launch on the fast path
+constexpr int kRowWords = 8;   // ballot words per row (rows of <= 256 nonzeros)
+constexpr int kOffH = kOffRB + kMCap;  // per-warp histograms: 2 rows x 256 u16 counters (128 u32 each)
+constexpr int kHistWords = 128;
+constexpr int kWarpScratchAll = kOffH + kHistWords;  // doubles per warp, fast path included
+
+struct FastRows {
+  const uint32_t* mi;
+  const uint32_t* mj;
+  const uint16_t* pj;
+  const float* vj;
+  const uint16_t* si;
+  const float* svi;
+  const uint16_t* sj;
+  const float* svj;
+  int ci, cj;
+};
+
+__device__ __forceinline__ uint32_t fkey(float v) { return 2u * __float_as_uint(v); }  // exact code of v >= 0
+
+// # of entries of the sorted row (n <= 256) whose code is < t (LE: <= t); branch-free
+template <bool LE>
+__device__ __forceinline__ int row_bound(const float* sv, int n, uint32_t t) {
+  int pos = 0;
+#pragma unroll
+  for (int step = 256; step > 0; step >>= 1) {
+    const int np = pos + step;
+    if (np <= n) {
+      const uint32_t c = fkey(sv[np - 1]);
+      if (LE ? (c <= t) : (c < t)) pos = np;
+    }
+  }
+  return pos;
+}
+// removed entries before sorted position pos (words rm[], per-word exclusive prefix pre[])
+__device__ __forceinline__ int removed_before(const uint32_t* rm, const uint32_t* pre, int pos, int cnt, int total) {
+  if (pos >= cnt) return total;
+  const int w = pos >> 5;
+  return static_cast<int>(pre[w]) + __popc(rm[w] & ((1u << (pos & 31)) - 1u));
+}
+__device__ __forceinline__ void hist_add(uint32_t* H, int pos) { atomicAdd(H + (pos >> 1), 1u << ((pos & 1) << 4)); }
+__device__ __forceinline__ int hist_get(const uint32_t* H, int pos) { return (H[pos >> 1] >> ((pos & 1) << 4)) & 0xFFFF; }
+
+template <int NNU>
+struct FastAcc {
+  double v[NNU];
+  const double* L;  // LUT of nu 0 (nu v at L + v * 2d)
+  int stride;       // 2d
+  int nnu;
+  __device__ __forceinline__ void add(double z, int idx) {
+#pragma unroll
+    for (int t = 0; t < NNU; ++t)
+      if (NNU == 1 || t < nnu) v[t] = fma(z, __ldg(L + t * stride + idx), v[t]);
+  }
+};
+
+// Sort S_ab (negatives in lanes 0-15, positives in lanes 16-31, KM slots
+// each), locate every element in the other row's sorted list, add its term,
+// and count it into the histogram at that position.  hpos: the positions
+// counted (-1: none), for the clean-up.
+template <int KM, int NNU>
+__device__ __forceinline__ bool fast_mids(const double* M, int mneg, int mpos, const FastRows& R, const uint32_t* RW,
+                                          uint32_t* HI, uint32_t* HJ, int sab, int n_neg, int zeros, int lane,
+                                          FastAcc<NNU>& acc, int (&hpos)[4]) {
+  double key[KM];
+  const bool hiB = lane >= 16;
+  const int l16 = lane & 15;
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int e = r * 16 + l16;
+    double v = INFINITY;
+    if (!hiB) {
+      if (e < mneg) v = M[sk(e)];
+    } else {
+      if (e < mpos) v = M[sk(kMCap - 1 - e)];
+    }
+    key[r] = v;
+  }
+  split_detail::warp_bitonic_upto<KM>(key, lane, 16 * KM);
+  const int cnt = hiB ? mpos : mneg;
+  uint32_t mag[KM];  // magnitude codes 2 bits(rz|z|) + inexact
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const double a = fabs(key[r]);
+    const float f = __double2float_rz(a);
+    mag[r] = fkey(f) + ((static_cast<double>(f) != a) ? 1u : 0u);
+  }
+  bool bad = false;
+  const uint32_t mnext0 = __shfl_down_sync(kFull, mag[0], 1);
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int q = l16 * KM + r;
+    const uint32_t mn = (r + 1 < KM) ? mag[r + 1 < KM ? r + 1 : 0] : mnext0;
+    if (q + 1 < cnt && mn == mag[r]) bad = true;  // tie or shared key inside the half
+  }
+  int pos[KM];
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int q = l16 * KM + r;
+    pos[r] = -1;
+    if (q >= cnt) continue;
+    if (hiB) {  // lb: row i's values below m
+      const int lb = row_bound<false>(R.svi, R.ci, mag[r]);
+      if (lb < R.ci && fkey(R.svi[lb]) == mag[r]) bad = true;
+      pos[r] = lb;
+    } else {  // ub: row j's values <= |m|
+      const int ub = row_bound<true>(R.svj, R.cj, mag[r]);
+      if (ub > 0 && fkey(R.svj[ub - 1]) == mag[r]) bad = true;
+      pos[r] = ub;
+    }
+  }
+  if (__any_sync(kFull, bad)) return false;
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int q = l16 * KM + r;
+    hpos[r] = -1;
+    if (q >= cnt) continue;
+    int less;
+    if (hiB) {
+      less = n_neg + zeros + q + pos[r] - removed_before(RW, RW + kRowWords, pos[r], R.ci, sab);
+      if (pos[r] < R.ci) {
+        hist_add(HI, pos[r]);
+        hpos[r] = pos[r];
+      }
+    } else {
+      less = q + (R.cj - pos[r]) - (sab - removed_before(RW + 2 * kRowWords, RW + 3 * kRowWords, pos[r], R.cj, sab));
+      if (pos[r] < R.cj) {
+        hist_add(HJ, pos[r]);
+        hpos[r] = pos[r];
+      }
+    }
+    acc.add(key[r], 2 * less + 1);
+  }
+  return true;
+}
+
+// Terms of the row-only elements of one row: S_a of row i (z = x, base
+// n_neg + zeros, S_ab+ below from the histogram) or S_b of row j (z = -x, the
+// row's larger entries and S_ab- below).
+template <bool ROW_I, int NNU>
+__device__ __forceinline__ void fast_row_terms(const float* sv, int c, const uint32_t* rm, const uint32_t* pre,
+                                               const uint32_t* H, int sab, int mcnt, int base_less, int lane,
+                                               FastAcc<NNU>& acc) {
+  const unsigned lt = (1u << lane) - 1u;
+  int carry = 0;
+  float lastx = -1.f;  // values are >= 0
+  for (int base = 0; base < c; base += 32) {
+    const int k = base + lane;
+    const bool in = k < c;
+    const uint32_t rw = rm[base >> 5];
+    const int removed = (rw >> lane) & 1u;
+    const bool live = in && !removed;
+    const float x = in ? sv[k] : -2.f;
+    // S_ab below: inclusive scan of the histogram over positions <= k
+    int s = in ? hist_get(H, k) : 0;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int o = __shfl_up_sync(kFull, s, dd);
+      if (lane >= dd) s += o;
+    }
+    s += carry;
+    carry = __shfl_sync(kFull, s, 31);
+    // tie group in the row (neighbours through shuffles; lane 31 reads the next chunk's first)
+    float xp = __shfl_up_sync(kFull, x, 1);
+    float xn = __shfl_down_sync(kFull, x, 1);
+    if (lane == 0) xp = lastx;
+    if (lane == 31) xn = (k + 1 < c) ? sv[k + 1] : -3.f;
+    lastx = __shfl_sync(kFull, x, 31);
+    int g0 = k, g1 = k + 1;
+    int rb0 = static_cast<int>(pre[base >> 5]) + __popc(rw & lt);
+    int rb1 = rb0 + removed;
+    if (live && (xp == x || xn == x)) {
+      while (g0 > 0 && sv[g0 - 1] == x) --g0;
+      while (g1 < c && sv[g1] == x) ++g1;
+      rb0 = removed_before(rm, pre, g0, c, sab);
+      rb1 = removed_before(rm, pre, g1, c, sab);
+    }
+    if (live) {
+      const int eq = (g1 - g0) - (rb1 - rb0);
+      const int less = ROW_I ? base_less + (g0 - rb0) + s : (c - g1) - (sab - rb1) + (mcnt - s);
+      acc.add(ROW_I ? static_cast<double>(x) : -static_cast<double>(x), 2 * less + eq);
+    }
+  }
+}
+
+// The whole pair on the fast path; false (warp-uniform) = not handled.
+template <int NNU>
+__device__ __forceinline__ bool fast_pair(const FastRows& R, double* scratch, int d, int lane,
+                                          const double* __restrict__ lut, int nnu, double half_p, bool store,
+                                          double* ot, size_t ostride, int* flag) {
+  uint32_t* RW = reinterpret_cast<uint32_t*>(scratch + kOffB);  // rm_i | pre_i | rm_j | pre_j
+  uint32_t* HI = reinterpret_cast<uint32_t*>(scratch + kOffH);
+  uint32_t* HJ = HI + kHistWords;
+  double* M = scratch + kOffM;
+  const unsigned lt = (1u << lane) - 1u;
+  // ---- row i (ascending): removal words; S_ab values (unordered) into M
+  int mneg = 0, mpos = 0, sab = 0;
+  for (int base = 0; base < R.ci; base += 32) {
+    const int k = base + lane;
+    const bool in = k < R.ci;
+    const int f = in ? R.si[k] : 0;
+    const int w = f >> 5, b = f & 31;
+    const uint32_t mjw = R.mj[w];
+    const bool inj = in && ((mjw >> b) & 1u);
+    const unsigned rm = __ballot_sync(kFull, inj);
+    if (lane == 0) {
+      RW[base >> 5] = rm;
+      RW[kRowWords + (base >> 5)] = static_cast<uint32_t>(sab);
+    }
+    sab += __popc(rm);
+    double z = 0.0;
+    if (inj) z = static_cast<double>(R.svi[k]) - static_cast<double>(R.vj[R.pj[w] + __popc(mjw & ((1u << b) - 1u))]);
+    const unsigned bn = __ballot_sync(kFull, z < 0.0);
+    const unsigned bq = __ballot_sync(kFull, z > 0.0);
+    if (z < 0.0) {
+      const int p = mneg + __popc(bn & lt);
+      if (p < kFastCap) M[sk(p)] = z;
+    } else if (z > 0.0) {
+      const int p = mpos + __popc(bq & lt);
+      if (p < kFastCap) M[sk(kMCap - 1 - p)] = z;
+    }
+    mneg += __popc(bn);
+    mpos += __popc(bq);
+  }
+  if (mneg > kFastCap || mpos > kFastCap) return false;
+  // ---- row j (ascending): removal words only
+  int sabj = 0;
+  for (int base = 0; base < R.cj; base += 32) {
+    const int k = base + lane;
+    const bool in = k < R.cj;
+    const int f = in ? R.sj[k] : 0;
+    const bool ini = in && ((R.mi[f >> 5] >> (f & 31)) & 1u);
+    const unsigned rm = __ballot_sync(kFull, ini);
+    if (lane == 0) {
+      RW[2 * kRowWords + (base >> 5)] = rm;
+      RW[3 * kRowWords + (base >> 5)] = static_cast<uint32_t>(sabj);
+    }
+    sabj += __popc(rm);
+  }
+  __syncwarp();
+  const int n_neg = (R.cj - sab) + mneg, n_pos = (R.ci - sab) + mpos;
+  const int zeros = d - n_neg - n_pos;
+  FastAcc<NNU> acc;
+#pragma unroll
+  for (int t = 0; t < NNU; ++t) acc.v[t] = 0.0;
+  acc.L = lut;
+  acc.stride = 2 * d;
+  acc.nnu = nnu;
+  int hpos[4] = {-1, -1, -1, -1};
+  if (mneg + mpos > 0) {
+    const int Hm = max(16, split_detail::npow2(max(mneg, mpos)));
+    bool ok;
+    switch (Hm / 16) {
+      case 1: ok = fast_mids<1, NNU>(M, mneg, mpos, R, RW, HI, HJ, sab, n_neg, zeros, lane, acc, hpos); break;
+      case 2: ok = fast_mids<2, NNU>(M, mneg, mpos, R, RW, HI, HJ, sab, n_neg, zeros, lane, acc, hpos); break;
+      default: ok = fast_mids<4, NNU>(M, mneg, mpos, R, RW, HI, HJ, sab, n_neg, zeros, lane, acc, hpos); break;
+    }
+    if (!ok) return false;
+    __syncwarp();
+  }
+  fast_row_terms<true, NNU>(R.svi, R.ci, RW, RW + kRowWords, HI, sab, mpos, n_neg + zeros, lane, acc);
+  fast_row_terms<false, NNU>(R.svj, R.cj, RW + 2 * kRowWords, RW + 3 * kRowWords, HJ, sab, mneg, 0, lane, acc);
+  __syncwarp();
+  const bool hiB = lane >= 16;
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    if (hpos[r] >= 0) (hiB ? HI : HJ)[hpos[r] >> 1] = 0u;  // leave the histograms zero
+#pragma unroll
+  for (int t = 0; t < NNU; ++t) {
+    if (NNU > 1 && t >= nnu) break;
+    const double sum = warp_sum(acc.v[t]);
+    const double val = clamp_nonneg(half_p * sum);
+    if (lane == 0 && store) {
+      ot[t * ostride] = val;
+      if (isinf(val)) atomicOr(flag, 1);
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Linear-weight path: nu = 2 or nu = 3.
+//
+// For e = nu - 1 in {1, 2}, G(R) = ((R-1/2)/p)^e - (1-(R-1/2)/p)^e = (2R-1-p)/p
+// exactly, so (Appendix A of SURVEY.md) D = sum_k z_k R_k - (p+1)/2 sum_k z_k,
+// and for any multiset S with midranks r: sum_S z r = sum_S z + PM(S), PM =
+// the sum over unordered pairs of their maximum (ties included).  Splitting z
+// into negatives N = S_b u S_ab-, zeros and positives P = S_a u S_ab+:
+//   D = (1 - h) sum_N z + (1 + |N| + zeros - h) sum_P z + PM(N) + PM(P),  h = (p+1)/2
+// and every term is a per-row constant (s1, tm = PM of the row, suffix sums
+// of its sorted values) corrected by the s features nonzero in BOTH rows
+// (F = S_ab's features): their positions in each row's sorted list, their
+// position-order ranks among F (popc prefix of a bitmask) and prefix sums of
+// their values in that order, plus, per S_ab value, its lower bound in the
+// other row (binary search) and its rank within S_ab+- (one small sort).
+// Per pair the work is O(W + s log p), not O(nnz): no per-element pass.  Ties
+// need no special case (PM(S) is tie-exact).  Every quantity is fp64 from
+// exact fp32 inputs; the reference's pow-based weights agree to round-off.
+// Falls back (false) when s > 64 or a row has more than 256 nonzeros.
+constexpr int kGmdCap = 64;
+
+struct GmdRows {
+  const uint32_t* mi;
+  const uint32_t* mj;
+  const uint16_t* pi;
+  const uint16_t* pj;
+  const float* vi;
+  const float* vj;
+  const float* svi;
+  const float* svj;
+  int ci, cj;
+  int64_t bi, bj;  // row store offsets of rows i, j
+  double s1i, tmi, s1j, tmj;
+};
+
+// #{F positions < pos} from the position bitmask QM (8 words) and its word prefix QP
+__device__ __forceinline__ int gmd_qcount(const uint32_t* QM, const uint32_t* QP, int pos, int c, int s) {
+  if (pos >= c) return s;
+  const int w = pos >> 5;
+  return static_cast<int>(QP[w]) + __popc(QM[w] & ((1u << (pos & 31)) - 1u));
+}
+
+template <int KM>
+__device__ __forceinline__ double gmd_mids(const double* M, int mneg, int mpos, const GmdRows& R,
+                                           const double* __restrict__ suf, const uint32_t* QM, const double* PQi,
+                                           const double* PQj, int s, int lane) {
+  double key[KM];
+  const bool hiB = lane >= 16;
+  const int l16 = lane & 15;
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int e = r * 16 + l16;
+    double v = INFINITY;
+    if (!hiB) {
+      if (e < mneg) v = M[sk(e)];
+    } else {
+      if (e < mpos) v = M[sk(kMCap - 1 - e)];
+    }
+    key[r] = v;
+  }
+  split_detail::warp_bitonic_upto<KM>(key, lane, 16 * KM);
+  const int cnt = hiB ? mpos : mneg;
+  double acc = 0.0;
+#pragma unroll
+  for (int r = 0; r < KM; ++r) {
+    const int q = l16 * KM + r;
+    if (q >= cnt) continue;
+    const double b = key[r];
+    const double a = fabs(b);
+    const float f = __double2float_rz(a);
+    const uint32_t mag = fkey(f) + ((static_cast<double>(f) != a) ? 1u : 0u);
+    if (hiB) {  // b in S_ab+: PM(S_ab+) rank term and the pairs (b, S_a)
+      const int lb = row_bound<false>(R.svi, R.ci, mag);  // #{row-i values < b}
+      const int ql = gmd_qcount(QM, QM + 16, lb, R.ci, s);
+      const double sl = (lb < R.ci) ? __ldg(suf + R.bi + lb) : 0.0;
+      acc += b * static_cast<double>(q + lb - ql) + sl - PQi[s] + PQi[ql];
+    } else {  // b in S_ab-: pairs (b, S_b) are -min(|b|, x)
+      const int L = row_bound<false>(R.svj, R.cj, mag);  // #{row-j values < |b|}
+      const int ql = gmd_qcount(QM + 8, QM + 24, L, R.cj, s);
+      const double sl = (L < R.cj) ? __ldg(suf + R.bj + L) : 0.0;
+      acc += b * static_cast<double>(q) -
+             ((R.s1j - sl) - PQj[ql] + a * static_cast<double>((R.cj - L) - (s - ql)));
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double warp_scan_incl(double v, int lane) {
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const double o = __shfl_up_sync(kFull, v, dd);
+    if (lane >= dd) v += o;
+  }
+  return v;
+}
+
+// D of the pair on the linear-weight path; false (warp-uniform) = not handled.
+__device__ __forceinline__ bool gmd_pair(const GmdRows& R, const uint16_t* __restrict__ pmap,
+                                         const double* __restrict__ suf, double* scratch, int W, int d, int lane,
+                                         double& out) {
+  int* F = reinterpret_cast<int*>(scratch);                  // [64] features nonzero in both rows
+  uint32_t* QM = reinterpret_cast<uint32_t*>(scratch + 32);  // qm_i[8] qm_j[8] qp_i[8] qp_j[8]
+  double* PQi = scratch + 48;                                // [65] prefix sums, position order
+  double* PQj = scratch + 48 + 72;
+  double* M = scratch + kOffM;
+  const unsigned lt = (1u << lane) - 1u;
+  if (R.ci > 256 || R.cj > 256) return false;
+  if (lane < 16) QM[lane] = 0u;
+  // ---- F: AND of the presence masks, compacted in feature order
+  uint32_t m = (lane < W) ? (R.mi[lane] & R.mj[lane]) : 0u;
+  const int c = __popc(m);
+  int incl = c;
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const int o = __shfl_up_sync(kFull, incl, dd);
+    if (lane >= dd) incl += o;
+  }
+  const int s = __shfl_sync(kFull, incl, 31);
+  if (s > kGmdCap) return false;
+  int off = incl - c;
+  while (m) {
+    const int b = __ffs(m) - 1;
+    m &= m - 1u;
+    F[off++] = (lane << 5) | b;
+  }
+  __syncwarp();
+  // ---- F's values and sorted positions in both rows
+  float al[2], be[2];
+  int pI[2], pJ[2];
+  bool live[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int e = lane + 32 * u;
+    live[u] = e < s;
+    al[u] = be[u] = 0.f;
+    pI[u] = pJ[u] = 0;
+    if (live[u]) {
+      const int f = F[e];
+      const int w = f >> 5;
+      const uint32_t lo = (1u << (f & 31)) - 1u;
+      const int ii = R.pi[w] + __popc(R.mi[w] & lo);
+      const int jj = R.pj[w] + __popc(R.mj[w] & lo);
+      al[u] = R.vi[ii];
+      be[u] = R.vj[jj];
+      pI[u] = __ldg(pmap + R.bi + ii);
+      pJ[u] = __ldg(pmap + R.bj + jj);
+      atomicOr(QM + (pI[u] >> 5), 1u << (pI[u] & 31));
+      atomicOr(QM + 8 + (pJ[u] >> 5), 1u << (pJ[u] & 31));
+    }
+  }
+  __syncwarp();
+  {  // word prefixes of the two position masks (groups of 8 lanes)
+    const uint32_t wv = (lane < 16) ? QM[lane] : 0u;
+    const int pc = __popc(wv);
+    int x = pc;
+#pragma unroll
+    for (int dd = 1; dd < 8; dd <<= 1) {
+      const int o = __shfl_up_sync(kFull, x, dd, 8);
+      if ((lane & 7) >= dd) x += o;
+    }
+    if (lane < 16) QM[16 + lane] = static_cast<uint32_t>(x - pc);
+  }
+  __syncwarp();
+  // ---- position-order ranks; values scattered in that order for prefix sums
+  int rI[2], rJ[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    rI[u] = gmd_qcount(QM, QM + 16, pI[u], 256, s);
+    rJ[u] = gmd_qcount(QM + 8, QM + 24, pJ[u], 256, s);
+    if (live[u]) {
+      PQi[1 + rI[u]] = static_cast<double>(al[u]);
+      PQj[1 + rJ[u]] = static_cast<double>(be[u]);
+    }
+  }
+  __syncwarp();
+  {
+    const int t0 = 1 + 2 * lane, t1 = t0 + 1;
+    const double a0 = (t0 <= s) ? PQi[t0] : 0.0, a1 = (t1 <= s) ? PQi[t1] : 0.0;
+    const double b0 = (t0 <= s) ? PQj[t0] : 0.0, b1 = (t1 <= s) ? PQj[t1] : 0.0;
+    const double ia = warp_scan_incl(a0 + a1, lane) - (a0 + a1);
+    const double ib = warp_scan_incl(b0 + b1, lane) - (b0 + b1);
+    if (t0 <= s) {
+      PQi[t0] = ia + a0;
+      PQj[t0] = ib + b0;
+    }
+    if (t1 <= s) {
+      PQi[t1] = ia + a0 + a1;
+      PQj[t1] = ib + b0 + b1;
+    }
+    if (lane == 0) {
+      PQi[0] = 0.0;
+      PQj[0] = 0.0;
+    }
+  }
+  // ---- global counts
+  double z[2];
+  int mneg = 0, mpos = 0;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    z[u] = live[u] ? static_cast<double>(al[u]) - static_cast<double>(be[u]) : 0.0;
+    const unsigned bn = __ballot_sync(kFull, z[u] < 0.0);
+    const unsigned bq = __ballot_sync(kFull, z[u] > 0.0);
+    if (z[u] < 0.0) M[sk(mneg + __popc(bn & lt))] = z[u];
+    if (z[u] > 0.0) M[sk(kMCap - 1 - (mpos + __popc(bq & lt)))] = z[u];
+    mneg += __popc(bn);
+    mpos += __popc(bq);
+  }
+  const int nP = R.ci - s + mpos, nN = R.cj - s + mneg;
+  const int zeros = d - nP - nN;
+  const double h = 0.5 * static_cast<double>(d + 1);
+  const double kp = static_cast<double>(1 + nN + zeros) - h, kn = 1.0 - h;
+  // ---- per-row constants and per-F terms
+  double acc = 0.0;
+  if (lane == 0)
+    acc = kp * R.s1i - kn * R.s1j + R.tmi - (static_cast<double>(R.cj - 1) * R.s1j - R.tmj);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    if (!live[u]) continue;
+    const double a = al[u], b = be[u];
+    const double sufi1 = (pI[u] + 1 < R.ci) ? __ldg(suf + R.bi + pI[u] + 1) : 0.0;
+    const double sufj0 = __ldg(suf + R.bj + pJ[u]);
+    acc += -kp * a + kn * b;
+    acc += a * static_cast<double>(rI[u] - pI[u]) - sufi1;  // PM(S_a) correction
+    acc += (R.s1j - sufj0) + b * static_cast<double>((R.cj - 1 - pJ[u]) - (s - 1 - rJ[u]));  // PM(S_b) correction
+    acc += (z[u] > 0.0) ? kp * z[u] : ((z[u] < 0.0) ? kn * z[u] : 0.0);
+  }
+  __syncwarp();
+  if (mneg + mpos > 0) {
+    const int Hm = max(16, split_detail::npow2(max(mneg, mpos)));
+    switch (Hm / 16) {
+      case 1: acc += gmd_mids<1>(M, mneg, mpos, R, suf, QM, PQi, PQj, s, lane); break;
+      case 2: acc += gmd_mids<2>(M, mneg, mpos, R, suf, QM, PQi, PQj, s, lane); break;
+      default: acc += gmd_mids<4>(M, mneg, mpos, R, suf, QM, PQi, PQj, s, lane); break;
+    }
+  }
+  out = clamp_nonneg(warp_sum(acc));
+  return true;
+}
+
 }  // namespace merge_detail
 
 // 16 warps per CTA on a tile x tile block of pairs (sparse panels + sorted-order index).
@@ -317,13 +870,13 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-  double* scratch = reinterpret_cast<double*>(smem_raw) + warp * kWarpScratch;
+  double* scratch = reinterpret_cast<double*>(smem_raw) + warp * kWarpScratchAll;
   uint32_t* A32 = reinterpret_cast<uint32_t*>(scratch);
   uint32_t* B32 = reinterpret_cast<uint32_t*>(scratch + kOffB);
   double* M = scratch + kOffM;
   double* RA = scratch + kOffRA;
   double* RB = scratch + kOffRB;
-  double* otile = reinterpret_cast<double*>(smem_raw) + nwarps * kWarpScratch;
+  double* otile = reinterpret_cast<double*>(smem_raw) + nwarps * kWarpScratchAll;
   const int tstride = tile + 1;
   unsigned char* pbase = reinterpret_cast<unsigned char*>(otile + static_cast<size_t>(a.nnu) * tile * tstride);
   uint32_t* smask = reinterpret_cast<uint32_t*>(pbase);                       // [2 tile][W]
@@ -339,6 +892,10 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
   __shared__ double s_score[2 * kMaxScoreNu];
   __shared__ double s_red[32 * 8];
   for (int e = threadIdx.x; e < 2 * kMaxScoreNu; e += blockDim.x) s_score[e] = 0.0;
+  {  // fast-path histograms start (and are left) zero
+    uint32_t* H = reinterpret_cast<uint32_t*>(scratch + kOffH);
+    for (int e = lane; e < 2 * kHistWords; e += 32) H[e] = 0u;
+  }
 
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
@@ -388,6 +945,36 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
       double* ot = otile + static_cast<size_t>(r) * tstride + c;
       const size_t ostride = static_cast<size_t>(tile) * tstride;
 
+      bool fastdone = false;
+      if constexpr (std::is_same<T, float>::value) {
+        if (ma.linear) {
+          // global rows of the two panel rows (invalid slots pair row i with itself)
+          const int64_t gi = i0 + ri, gj = (rj < tile) ? i0 + rj : j0 + (rj - tile);
+          const bool oki = gi < a.n, okj = gj < a.n;
+          const GmdRows R{mi, mj, pi, pj, vi, vj, svi, svj, ci, cj,
+                          oki ? __ldg(sa.rowptr + gi) : 0, okj ? __ldg(sa.rowptr + gj) : 0,
+                          oki ? __ldg(ma.s1 + gi) : 0.0, oki ? __ldg(ma.tm + gi) : 0.0,
+                          okj ? __ldg(ma.s1 + gj) : 0.0, okj ? __ldg(ma.tm + gj) : 0.0};
+          double dval = 0.0;
+          fastdone = gmd_pair(R, ma.pmap, ma.suf, scratch, W, d, lane, dval);
+          if (fastdone && valid && lane == 0)
+            for (int v = 0; v < a.nnu; ++v) {
+              ot[v * ostride] = dval;
+              if (isinf(dval)) atomicOr(a.flag, 1);
+            }
+          if (!fastdone && ma.fast_miss && valid && lane == 0) atomicAdd(ma.fast_miss, 1ull);
+          __syncwarp();
+        }
+        if (!fastdone && ma.fast && a.nnu <= kFastNu && ci <= 32 * kRowWords && cj <= 32 * kRowWords) {
+          const FastRows R{mi, mj, pj, vj, si, svi, sj, svj, ci, cj};
+          fastdone = (a.nnu == 1)
+                         ? fast_pair<1>(R, scratch, d, lane, a.lut, 1, half_p, valid, ot, ostride, a.flag)
+                         : fast_pair<kFastNu>(R, scratch, d, lane, a.lut, a.nnu, half_p, valid, ot, ostride, a.flag);
+          if (!fastdone && ma.fast_miss && valid && lane == 0) atomicAdd(ma.fast_miss, 1ull);
+          __syncwarp();
+        }
+      }
+      if (!fastdone) {
       // ---- row i in ascending value order: S_a -> B head (ordered), S_ab -> M (unordered)
       int cp = 0, mneg = 0, mpos = 0;
       for (int base = 0; base < ci; base += 32) {
@@ -517,6 +1104,7 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
           }
         }
       }
+      }  // !fastdone
       __syncwarp();
     }
     __syncthreads();
@@ -527,7 +1115,7 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
 }
 
 inline size_t merge_smem(int tile, int W, int maxnnz, size_t sz, int nnu) {
-  return static_cast<size_t>(merge_detail::kMergeThreads / 32) * merge_detail::kWarpScratch * 8 + static_cast<size_t>(nnu) * tile * (tile + 1) * 8 +
+  return static_cast<size_t>(merge_detail::kMergeThreads / 32) * merge_detail::kWarpScratchAll * 8 + static_cast<size_t>(nnu) * tile * (tile + 1) * 8 +
          ((2 * static_cast<size_t>(tile) * W * 6 + 15) & ~static_cast<size_t>(15)) + (2 * tile + 4) * 4 +
          2 * static_cast<size_t>(tile) * maxnnz * (2 * sz + 2) + 16;
 }

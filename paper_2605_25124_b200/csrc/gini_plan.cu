@@ -22,7 +22,8 @@ void launch_gini_list(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64
                       gmds_dtype ot, cudaStream_t st);
 
 void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, const int64_t* rowptr, const int* rows,
-                     int nrows, int K, uint16_t* sidx, void* svs, cudaStream_t st);
+                     int nrows, int K, uint16_t* sidx, void* svs, uint16_t* pmap, double* suf, double* s1,
+                     double* tm, cudaStream_t st);
 
 namespace {
 
@@ -86,6 +87,9 @@ __global__ void row_fill_kernel(const T* __restrict__ X, int64_t n, int p, int W
 struct RowStore {
   DevBuf<uint16_t> fidx, sidx;
   DevBuf<unsigned char> svs;  // values in ascending order per row (merge path)
+  DevBuf<uint16_t> pmap;      // sorted position of each nonzero (feature order; linear-weight path)
+  DevBuf<double> suf;         // suffix sums of the sorted values (linear-weight path)
+  DevBuf<double> s1, tm;      // per row: sum of values, sum_k v_(k) k
   bool nonneg = false;
   DevBuf<uint32_t> masks;
   DevBuf<uint16_t> prefix;
@@ -143,6 +147,10 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
     // value-sorted feature order per row (the merge kernel's runs); rows bucketed by sort width
     rs.sidx.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
     rs.svs.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])) * dtype_size(xt));
+    rs.pmap.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
+    rs.suf.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
+    rs.s1.alloc(static_cast<size_t>(n));
+    rs.tm.alloc(static_cast<size_t>(n));
     std::vector<std::vector<int>> buckets(6);
     for (int64_t i = 0; i < n; ++i) {
       int K = 1;
@@ -157,7 +165,8 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
       GMDS_CUDA(cudaMemcpyAsync(rows.get(), buckets[bk].data(), buckets[bk].size() * sizeof(int),
                                 cudaMemcpyHostToDevice, st));
       launch_row_sort(rs.vals.get(), xt, rs.fidx.get(), rs.rowptr.get(), rows.get(),
-                      static_cast<int>(buckets[bk].size()), 1 << bk, rs.sidx.get(), rs.svs.get(), st);
+                      static_cast<int>(buckets[bk].size()), 1 << bk, rs.sidx.get(), rs.svs.get(), rs.pmap.get(),
+                      rs.suf.get(), rs.s1.get(), rs.tm.get(), st);
       GMDS_CUDA(cudaStreamSynchronize(st));
     }
   }
@@ -307,6 +316,22 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       ma.s.sparse = 1;
       ma.sidx = rs.sidx.get();
       ma.svs = rs.svs.get();
+      ma.fast = std::getenv("GMDS_MERGE_NOFAST") ? 0 : 1;
+      // nu = 2 and nu = 3 give the same affine weight G(R) = (2R - 1 - p)/p (gmd_pair)
+      ma.linear = 1;
+      for (int v = 0; v < nnu; ++v)
+        if (nus[v] != 2.0 && nus[v] != 3.0) ma.linear = 0;
+      if (std::getenv("GMDS_NO_LINEAR") || score) ma.linear = 0;
+      ma.pmap = rs.pmap.get();
+      ma.suf = rs.suf.get();
+      ma.s1 = rs.s1.get();
+      ma.tm = rs.tm.get();
+      DevBuf<unsigned long long> miss;
+      if (tr.on) {
+        miss.alloc(1);
+        GMDS_CUDA(cudaMemsetAsync(miss.get(), 0, sizeof(unsigned long long), st));
+        ma.fast_miss = miss.get();
+      }
       const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(mt) * mt;
       ma.s.ovf_cap = (p > 512) ? std::min<int64_t>(shard_pairs, int64_t(1) << 20) : 0;
       DevBuf<int64_t> ovf(static_cast<size_t>(std::max<int64_t>(1, 2 * ma.s.ovf_cap)));
@@ -327,6 +352,13 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       });
       ma.s.g = a;
       tr.mark("gini_merge_kernel", st);
+      if (tr.on) {
+        unsigned long long hm = 0;
+        GMDS_CUDA(cudaMemcpyAsync(&hm, miss.get(), sizeof hm, cudaMemcpyDeviceToHost, st));
+        GMDS_CUDA(cudaStreamSynchronize(st));
+        std::fprintf(stderr, "[gmds] merge fast path: %llu of %lld pairs fell back\n", hm,
+                     static_cast<long long>(n * (n - 1) / 2));
+      }
       unsigned long long novf = 0;
       GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
       GMDS_CUDA(cudaStreamSynchronize(st));

@@ -303,3 +303,67 @@ def test_pairwise_nonfinite_input_device_check():
     X[7, 3] = np.inf
     with pytest.raises(G.InvalidInput, match="non-finite input"):
         G.pairwise_gini(X, [2.0])
+
+
+@pytest.mark.parametrize("kind", ["image", "levels", "dense_overlap"])
+def test_merge_fast_path_vs_oracle(kind):
+    # rank-by-counting fast path of the merge kernel (nnu <= 4): ranks from
+    # counts on the pre-sorted rows; row-internal tie groups (clipped 1.0s,
+    # quantised levels), duplicate rows, and |S_ab| above the fast cap (the
+    # pair falls back to the merge path inside the same kernel)
+    rng = np.random.default_rng({"image": 1, "levels": 2, "dense_overlap": 3}[kind])
+    if kind == "image":
+        X = image_like(160, 784, 11)
+        nus = [2.0]
+    elif kind == "levels":  # heavy ties inside rows and across S_a / S_b
+        X = rng.choice(np.float32([0.25, 0.5, 1.0, 2.0]), size=(150, 300)).astype(np.float32)
+        X[rng.random(X.shape) < 0.75] = 0.0
+        nus = [1.5, 2.0, 3.0, 5.0]
+    else:  # ~45% density: many pairs with |S_ab+| or |S_ab-| > 64
+        X = (rng.random((120, 400)) * (rng.random((120, 400)) < 0.45)).astype(np.float32)
+        nus = [1.2, 4.0]
+    X[7] = X[8]
+    Ds = G.pairwise_gini(X, nus)
+    Xd = X.astype(np.float64)
+    for k, nu in enumerate(nus):
+        ref = O.pairwise_matrix(Xd, nu)
+        assert maxnorm_err(Ds[k], ref) <= 1e-12
+    assert Ds[0][7, 8] == 0.0
+
+
+def test_merge_fast_path_matches_merge_path(monkeypatch):
+    # the same matrix with the fast path disabled (GMDS_MERGE_NOFAST): equal to
+    # round-off (different summation order), both equal to the oracle
+    X = image_like(200, 784, 23)
+    a = G.pairwise_matrix(X, 2.0)
+    monkeypatch.setenv("GMDS_MERGE_NOFAST", "1")
+    b = G.pairwise_matrix(X, 2.0)
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.max(b)
+    assert maxnorm_err(a, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["image", "levels", "overlap", "wide"])
+def test_linear_weight_path_vs_oracle(kind, monkeypatch):
+    # nu = 2 and nu = 3: G(R) is affine in R, the merge kernel assembles D from
+    # per-row prefix sums and the features nonzero in both rows (gmd_pair);
+    # checked against the oracle and against the general paths
+    rng = np.random.default_rng({"image": 4, "levels": 5, "overlap": 6, "wide": 7}[kind])
+    if kind == "image":
+        X = image_like(180, 784, 31)
+    elif kind == "levels":  # ties everywhere: within rows, across rows, S_ab values equal to row values
+        X = rng.choice(np.float32([0.25, 0.5, 0.75, 1.0]), size=(150, 200)).astype(np.float32)
+        X[rng.random(X.shape) < 0.7] = 0.0
+    elif kind == "overlap":  # ~45% density: many pairs with more than 64 shared features (fallback)
+        X = (rng.random((120, 300)) * (rng.random((120, 300)) < 0.45)).astype(np.float32)
+    else:  # p = 1000 (W = 32 mask words), a few rows with > 256 nonzeros (fallback)
+        X = image_like(100, 1000, 8)
+        X[:3] = rng.random((3, 1000)).astype(np.float32) * (rng.random((3, 1000)) < 0.4)
+    X[5] = X[9]
+    Xd = X.astype(np.float64)
+    D = G.pairwise_gini(X, [2.0, 3.0])
+    for k, nu in enumerate((2.0, 3.0)):
+        assert maxnorm_err(D[k], O.pairwise_matrix(Xd, nu)) <= 1e-12
+    assert D[0][5, 9] == 0.0
+    monkeypatch.setenv("GMDS_NO_LINEAR", "1")
+    Dg = G.pairwise_gini(X, [2.0])
+    assert np.max(np.abs(D[0] - Dg[0])) <= 1e-12 * np.max(Dg[0])
