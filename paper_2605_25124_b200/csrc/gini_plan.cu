@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "gini_gmd.cuh"
 #include "gini_merge.cuh"
 #include "kernels.cuh"
 #include "lib_internal.h"
@@ -294,6 +295,66 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   }
   // split kernel: split_min_blocks(K) CTAs per SM (its __launch_bounds__) share ~226 KB of smem
   const size_t two_per_sm = (split_detail_min_blocks(p) >= 3 ? 74 : 113) * 1024, one_per_sm = 220 * 1024;
+  bool linear = (score == nullptr) && !std::getenv("GMDS_NO_LINEAR");
+  for (int v = 0; v < nnu; ++v)
+    if (nus[v] != 2.0 && nus[v] != 3.0) linear = false;
+  if (linear && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 &&
+      gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu) <= 227 * 1024) {
+    // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh)
+    const size_t gsm = gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu);
+    a.tile = gmd_detail::kTile;
+    a.nbt = ceil_div(n, a.tile);
+    const int64_t units = a.nbt * (a.nbt + 1) / 2;
+    a.tile_begin = units * shard / nshards;
+    a.tile_end = units * (shard + 1) / nshards;
+    if (a.tile_end <= a.tile_begin) return;
+    GmdArgs ga{};
+    ga.s.g = a;
+    ga.s.masks = rs.masks.get();
+    ga.s.prefix = rs.prefix.get();
+    ga.s.rowptr = rs.rowptr.get();
+    ga.s.vals = rs.vals.get();
+    ga.s.W = rs.W;
+    ga.s.maxnnz = std::max(1, rs.maxnnz);
+    ga.s.sparse = 1;
+    ga.pmap = rs.pmap.get();
+    ga.svs = reinterpret_cast<const float*>(rs.svs.get());
+    ga.suf = rs.suf.get();
+    ga.s1 = rs.s1.get();
+    ga.tm = rs.tm.get();
+    const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(a.tile) * a.tile;
+    ga.s.ovf_cap = std::min<int64_t>(shard_pairs, int64_t(1) << 20);
+    DevBuf<int64_t> ovf(static_cast<size_t>(2 * ga.s.ovf_cap));
+    DevBuf<unsigned long long> ovf_count(1);
+    GMDS_CUDA(cudaMemsetAsync(ovf_count.get(), 0, sizeof(unsigned long long), st));
+    ga.s.ovf_pairs = ovf.get();
+    ga.s.ovf_count = ovf_count.get();
+    chunked(a, [&](GiniTileArgs& g) {
+      ga.s.g = g;
+      const unsigned blk = static_cast<unsigned>(std::min<int64_t>(g.tile_end - g.tile_begin, int64_t(1) << 30));
+      launch_gini_gmd(ga, dD, ot, gsm, blk, st);
+      count_launch();
+      check_launch("gini_gmd_kernel");
+    });
+    ga.s.g = a;
+    tr.mark("gini_gmd_kernel", st);
+    unsigned long long novf = 0;
+    GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    if (tr.on) std::fprintf(stderr, "[gmds] gmd overflow pairs: %llu\n", novf);
+    if (novf == 0) return;
+    if (sink) sink->late_writes = true;
+    if (static_cast<int64_t>(novf) > ga.s.ovf_cap) {
+      sink = nullptr;
+      full_kernel();
+    } else {
+      launch_gini_list<32>(a, dX, xt, ovf.get(), static_cast<int64_t>(novf), dD, ot, st);
+      count_launch();
+      check_launch("gini_list_kernel");
+    }
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
   if (sparse && rs.nonneg && p > 32 && xt == GMDS_F32) {  // merge path (exact u32 keys need fp32 inputs): pre-sorted row runs + one bitonic merge per sign half
     int mt = 32;
     while (mt > 4 && merge_smem(mt, rs.W, std::max(1, rs.maxnnz), sz, nnu) > one_per_sm) mt >>= 1;
