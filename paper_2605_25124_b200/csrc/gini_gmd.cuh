@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
   uint32_t* QM = reinterpret_cast<uint32_t*>(wscr + kOffQM);  // qm_i[8] qm_j[8] qp_i[8] qp_j[8]
   double* PQi = wscr + kOffPQi;
   double* PQj = wscr + kOffPQj;
-  double* BL = wscr + kOffBL;  // [0]: S_ab- values, [kCap]: S_ab+ values
+  double* ZL = wscr + kOffBL;  // z on F, stored twice (F order): circular reads without a wrap
   double* otile = reinterpret_cast<double*>(smem_raw) + kWarps * kWarpWords;  // [nnu][32][33]
   double* rs1 = otile + static_cast<size_t>(a.nnu) * kTile * (kTile + 1);
   double* rtm = rs1 + kRows;
@@ -246,12 +246,12 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
           PQj[1 + rJ[u]] = static_cast<double>(be[u]);
         }
         z[u] = static_cast<double>(al[u]) - static_cast<double>(be[u]);
-        const unsigned bn = __ballot_sync(0xffffffffu, z[u] < 0.0);
-        const unsigned bq = __ballot_sync(0xffffffffu, z[u] > 0.0);
-        if (z[u] < 0.0) BL[mneg + __popc(bn & lt)] = z[u];
-        if (z[u] > 0.0) BL[kCap + mpos + __popc(bq & lt)] = z[u];
-        mneg += __popc(bn);
-        mpos += __popc(bq);
+        if (live) {
+          ZL[lane + 32 * u] = z[u];
+          ZL[lane + 32 * u + s] = z[u];
+        }
+        mneg += __popc(__ballot_sync(0xffffffffu, z[u] < 0.0));
+        mpos += __popc(__ballot_sync(0xffffffffu, z[u] > 0.0));
       }
       __syncwarp();
       {  // prefix sums PQ[k] = sum of the first k values in position order
@@ -283,9 +283,17 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
       double acc = 0.0;
       if (lane == 0) acc = kp * rs1[ri] - kn * s1j + rtm[ri] - (static_cast<double>(cj - 1) * s1j - rtm[rj]);
       const double sumQi = PQi[s];
+      // PM(S_ab+) + PM(S_ab-) = PM(Z) - (|S_ab-| + |Z0|) sum(S_ab+), Z = all s values of
+      // z on F; PM(Z) = (s-1)/2 sum z + 1/2 sum over unordered pairs |z_f - z_g|
+      // (each lane: its values against the next floor((s-1)/2) in circular order,
+      // plus half of the opposite one when s is even: every pair exactly once)
+      const double wneg = static_cast<double>(s - mpos);  // |S_ab-| + |Z0|
+      const int half = (s - 1) >> 1;
+      const bool even = (s & 1) == 0;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        if (lane + 32 * u >= s) continue;
+        const int e = lane + 32 * u;
+        if (e >= s) continue;
         const double av = al[u], bv = be[u];
         // pairs of row i touching F (PM(S_a)) and of row j (minima, PM(S_b))
         const double si1 = (pI[u] + 1 < ci) ? __ldg(sufi + pI[u] + 1) : 0.0;
@@ -293,33 +301,26 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
         acc += av * static_cast<double>(rI[u] - pI[u]) - si1 - kp * av;
         acc += (s1j - sj0) + bv * static_cast<double>((cj - 1 - pJ[u]) - (s - 1 - rJ[u])) + kn * bv;
         const double zz = z[u];
+        // PM(Z) pieces
+        double gsum = 0.0;
+        const double* zr = ZL + e + 1;
+        for (int t = 0; t < half; ++t) gsum += fabs(zz - zr[t]);
+        if (even) gsum += 0.5 * fabs(zz - zr[half]);
+        acc += 0.5 * gsum + 0.5 * static_cast<double>(s - 1) * zz;
         if (zz == 0.0) continue;
-        // zz in S_ab+ / S_ab-: its rank in its sign group (ties: half each) ...
+        // zz's pairs with the other row's row-only values (one search, sign-selected row)
         const bool pos = zz > 0.0;
-        const double* L = BL + (pos ? kCap : 0);
-        const int len = pos ? mpos : mneg;
-        int cl = 0, cle = 0;
-        for (int q = 0; q < len; ++q) {
-          const double o = L[q];
-          cl += (o < zz) ? 1 : 0;
-          cle += (o <= zz) ? 1 : 0;
-        }
-        const double rq = 0.5 * static_cast<double>(cl + cle - 1);
-        // ... and its pairs with the other row's row-only values
         const double mg = fabs(zz);
         const float f = __double2float_rz(mg);
         const uint32_t code = fkey(f) + ((static_cast<double>(f) != mg) ? 1u : 0u);
-        if (pos) {
-          const int lb = lower_count(ssv + ri * stride, ci, code);  // #{row-i values < zz}
-          const int ql = qcount(QM, QM + 16, lb, s);
-          const double sl = (lb < ci) ? __ldg(sufi + lb) : 0.0;
-          acc += kp * zz + zz * (rq + static_cast<double>(lb - ql)) + sl - sumQi + PQi[ql];
-        } else {
-          const int lb = lower_count(ssv + rj * stride, cj, code);  // #{row-j values < |zz|}
-          const int ql = qcount(QM + 8, QM + 24, lb, s);
-          const double sl = (lb < cj) ? __ldg(sufj + lb) : 0.0;
-          acc += kn * zz + zz * rq - ((s1j - sl) - PQj[ql] + mg * static_cast<double>((cj - lb) - (s - ql)));
-        }
+        const int n = pos ? ci : cj;
+        const int lb = lower_count(ssv + (pos ? ri : rj) * stride, n, code);  // #{row values < |zz|}
+        const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
+        const double sl = (lb < n) ? __ldg((pos ? sufi : sufj) + lb) : 0.0;
+        if (pos)
+          acc += (kp - wneg) * zz + zz * static_cast<double>(lb - ql) + sl - sumQi + PQi[ql];
+        else
+          acc += kn * zz - ((s1j - sl) - PQj[ql] + mg * static_cast<double>((cj - lb) - (s - ql)));
       }
 #pragma unroll
       for (int dd = 16; dd > 0; dd >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, dd);
