@@ -44,8 +44,6 @@ namespace gmd_detail {
 
 constexpr int kTile = 32;
 constexpr int kRows = 2 * kTile;
-constexpr int kWarps = 24;
-constexpr int kThreads = kWarps * 32;
 constexpr int kCap = 64;      // max |F| per pair
 constexpr int kMaxC = 256;    // max nonzeros per row
 // per-warp scratch (8-byte words): F[64] ints (32) | QM[32] u32 (16) | PQi[72] | PQj[72] | BL[2][64]
@@ -60,7 +58,7 @@ __device__ __forceinline__ int lower_count(const float* sv, int n, uint32_t t) {
 #pragma unroll
   for (int step = 128; step > 0; step >>= 1) {
     const int idx = pos + step - 1;
-    const bool go = (idx < n) && (fkey(sv[min(idx, kMaxC - 1)]) < t);
+    const bool go = (idx < n) && (fkey(sv[idx]) < t);  // idx <= 254: inside shared memory even past n
     pos += go ? step : 0;
   }
   // the ninth probe (n = 256): position 255
@@ -86,8 +84,8 @@ __device__ __forceinline__ double warp_incl(double v, int lane) {
 
 }  // namespace gmd_detail
 
-template <typename TO>
-__global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdArgs ga, TO* __restrict__ out) {
+template <typename TO, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO* __restrict__ out) {
   using namespace gmd_detail;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const SplitArgs& sa = ga.s;
@@ -97,7 +95,6 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
   const int stride = sa.maxnnz;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
   // ---- shared memory
   double* wscr = reinterpret_cast<double*>(smem_raw) + warp * kWarpWords;
   int* F = reinterpret_cast<int*>(wscr);
@@ -302,10 +299,16 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
         acc += (s1j - sj0) + bv * static_cast<double>((cj - 1 - pJ[u]) - (s - 1 - rJ[u])) + kn * bv;
         const double zz = z[u];
         // PM(Z) pieces
-        double gsum = 0.0;
+        double g0 = 0.0, g1 = 0.0;  // two chains: DADD latency
         const double* zr = ZL + e + 1;
-        for (int t = 0; t < half; ++t) gsum += fabs(zz - zr[t]);
-        if (even) gsum += 0.5 * fabs(zz - zr[half]);
+        int t = 0;
+        for (; t + 1 < half; t += 2) {
+          g0 += fabs(zz - zr[t]);
+          g1 += fabs(zz - zr[t + 1]);
+        }
+        if (t < half) g0 += fabs(zz - zr[t]);
+        if (even) g1 += 0.5 * fabs(zz - zr[half]);
+        const double gsum = g0 + g1;
         acc += 0.5 * gsum + 0.5 * static_cast<double>(s - 1) * zz;
         if (zz == 0.0) continue;
         // zz's pairs with the other row's row-only values (one search, sign-selected row)
@@ -326,7 +329,8 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
       for (int dd = 16; dd > 0; dd >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, dd);
       if (lane == 0) {
         const double val = clamp_nonneg(acc);
-        for (int v = 0; v < a.nnu; ++v) ot[v * kTile * tstride] = val;
+        ot[0] = val;
+        for (int v = 1; v < a.nnu; ++v) ot[v * kTile * tstride] = val;
         if (isinf(val)) atomicOr(a.flag, 1);
       }
       __syncwarp();
@@ -337,13 +341,14 @@ __global__ void __launch_bounds__(gmd_detail::kThreads, 1) gini_gmd_kernel(GmdAr
   }
 }
 
-inline size_t gmd_smem(int W, int maxnnz, int nnu) {
+inline size_t gmd_smem(int W, int maxnnz, int nnu, int nwarps) {
   using namespace gmd_detail;
-  return static_cast<size_t>(kWarps) * kWarpWords * 8 + static_cast<size_t>(nnu) * kTile * (kTile + 1) * 8 +
+  return static_cast<size_t>(nwarps) * kWarpWords * 8 + static_cast<size_t>(nnu) * kTile * (kTile + 1) * 8 +
          kRows * (8 + 8 + 8 + 4) + kRows * W * 4 + ((kRows * W + 1) & ~1) * 2 +
          static_cast<size_t>(kRows) * maxnnz * (4 + 4 + 2) + 16;
 }
 
-void launch_gini_gmd(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, cudaStream_t st);
+void launch_gini_gmd(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
+                     cudaStream_t st);
 
 }  // namespace gmds

@@ -298,10 +298,14 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   bool linear = (score == nullptr) && !std::getenv("GMDS_NO_LINEAR");
   for (int v = 0; v < nnu; ++v)
     if (nus[v] != 2.0 && nus[v] != 3.0) linear = false;
-  if (linear && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 &&
-      gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu) <= 227 * 1024) {
+  // warps per CTA of the linear-weight kernel: the most that fit in shared memory
+  int gmd_warps = 0;
+  for (int nw : {28, 24})  // 28: 72 registers, no spills (217 ms vs 221 at 24; 32 spills: 230 ms)
+    if (!gmd_warps && gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu, nw) <= 227 * 1024) gmd_warps = nw;
+  if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd_warps = std::atoi(e);
+  if (linear && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 && gmd_warps > 0) {
     // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh)
-    const size_t gsm = gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu);
+    const size_t gsm = gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu, gmd_warps);
     a.tile = gmd_detail::kTile;
     a.nbt = ceil_div(n, a.tile);
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
@@ -332,7 +336,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     chunked(a, [&](GiniTileArgs& g) {
       ga.s.g = g;
       const unsigned blk = static_cast<unsigned>(std::min<int64_t>(g.tile_end - g.tile_begin, int64_t(1) << 30));
-      launch_gini_gmd(ga, dD, ot, gsm, blk, st);
+      launch_gini_gmd(ga, dD, ot, gsm, blk, gmd_warps, st);
       count_launch();
       check_launch("gini_gmd_kernel");
     });
