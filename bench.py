@@ -63,7 +63,7 @@ def load_traffic():
         with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
             t = json.load(f)
         g = lambda k: t[k]["dram_read_bytes"] + t[k]["dram_write_bytes"]
-        return g("gini_merge_kernel"), g("stress_tma_kernel_grad")
+        return g("gini_gmd_kernel"), g("stress_tma_kernel_fused")
     except (OSError, KeyError, ValueError):
         return None, None
 
@@ -368,11 +368,11 @@ def run_engine(args, rank, world, dist):
         "gpu_launches": int(dist_launches + stress_launches),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu.value / 1e12, "unit": "Tops/s",
                      "frac": achieved / alu.value, "traffic": traffic_dist, "traffic_unit": "bytes/launch (ncu)",
-                     "kernel": "gini_merge_kernel", "ops_per_pair": ops_pair,
+                     "kernel": "gini_gmd_kernel (nu = 2: linear-weight path)", "ops_per_pair": ops_pair,
                      "peak_source": "measured on this GPU by gmds_probe_alu (FFMA + IADD3/LOP3 lane-op rate)"},
         "stress_roofline": {"bound": "hbm", "achieved": stress_bytes / pass_time / 1e9, "peak": peaks.get("hbm_gbs"),
                             "unit": "GB/s", "frac": stress_bytes / pass_time / 1e9 / peaks.get("hbm_gbs", 6446.6),
-                            "traffic": traffic_stress, "kernel": "stress_tma_kernel (+ reductions, per pass)",
+                            "traffic": traffic_stress, "kernel": "stress_tma_kernel fused (+ reductions, per pass)",
                             "bytes_per_pass": stress_bytes},
         "clocks": clk.summary(),
         "clocks_stress": clk2.summary(),
