@@ -24,6 +24,10 @@
 #include "f32x2.cuh"
 #include "stress_pass.cuh"
 
+#ifndef GMDS_TMA_MINB
+#define GMDS_TMA_MINB(MODE) ((MODE) != 0 ? 2 : 3)
+#endif
+
 namespace gmds {
 
 namespace tma_detail {
@@ -92,7 +96,7 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 // 2 (fused): loss of two trial points + gradient at the first (the predicted
 // Armijo acceptance, so the next iteration usually needs no gradient pass).
 template <int Q, int MODE, int KIND>
-__global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
   constexpr bool GRAD = (MODE != 0);  // gradient accumulation (of configuration 0)
   constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;
@@ -190,6 +194,9 @@ __global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel
       mbar_wait(&bars[stage], static_cast<uint32_t>((h / NS) & 1));
       const float* Ds = ring + stage * kHalfFloats;
       const float* Wb = W ? W + blk * (kPT * kPT) + half * kHalfFloats : nullptr;
+      float2 lhalf[NCM];  // loss of this half, two fp32 lanes per candidate (widened once per half)
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) lhalf[c] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int x = 0; x < kMR; ++x) {
         const int rloc = ti * kMR + x;           // row within the half
@@ -200,14 +207,18 @@ __global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel
         float wv[kMT];
 #pragma unroll
         for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tj * kMT + y] : 1.f;
-        float lossrow[NCM];
-#pragma unroll
-        for (int c = 0; c < NCM; ++c) lossrow[c] = 0.f;
         float yi[NCM][Q];
 #pragma unroll
-        for (int c = 0; c < NCM; ++c)
+        for (int c = 0; c < NCM; ++c) {
+          if constexpr (Q == 2) {
+            const float2 t = (c < nc) ? *reinterpret_cast<const float2*>(&sYi[c][ri][0]) : make_float2(0.f, 0.f);
+            yi[c][0] = t.x;
+            yi[c][1] = t.y;
+          } else {
 #pragma unroll
-          for (int k = 0; k < Q; ++k) yi[c][k] = (c < nc) ? sYi[c][ri][k] : 0.f;
+            for (int k = 0; k < Q; ++k) yi[c][k] = (c < nc) ? sYi[c][ri][k] : 0.f;
+          }
+        }
         // interior blocks: no masks at all; edge blocks (diagonal / last column block) mask per pair
         auto pairs = [&](auto edge_tag) {
           constexpr bool EDGE = decltype(edge_tag)::value;
@@ -236,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel
                 term = keep ? term : 0.f;
                 cc = keep ? cc : 0.f;
               }
-              lossrow[c] += term;
+              lhalf[c].x += term;
               if constexpr (GRAD) {
                 if (c != 0) continue;
 #pragma unroll
@@ -262,7 +273,10 @@ __global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel
             float2 yi2[Q];
 #pragma unroll
             for (int k = 0; k < Q; ++k) yi2[k] = make_float2(yi[c][k], yi[c][k]);
-            float2 lacc = make_float2(0.f, 0.f);
+            float2 lacc = lhalf[c];
+            float2 racc[Q];  // this row's gradient sums over columns (y, y+1)
+#pragma unroll
+            for (int k = 0; k < Q; ++k) racc[k] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int yy = 0; yy < kMT / 2; ++yy) {
               float2 dy2[Q];
@@ -283,19 +297,22 @@ __global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel
                 const float2 u = KR ? f2mul(e, inv) : f2mul(dvp[yy], inv);
 #pragma unroll
                 for (int k = 0; k < Q; ++k) {
-                  if constexpr (KR) {
-                    rowsum[half][x][k] = fmaf(-u.x, dy2[k].x, rowsum[half][x][k]);
-                    rowsum[half][x][k] = fmaf(-u.y, dy2[k].y, rowsum[half][x][k]);
+                  racc[k] = f2fma(u, dy2[k], racc[k]);
+                  if constexpr (KR)
                     colacc2[yy][k] = f2fma(u, dy2[k], colacc2[yy][k]);
-                  } else {
-                    rowsum[half][x][k] = fmaf(u.x, dy2[k].x, rowsum[half][x][k]);
-                    rowsum[half][x][k] = fmaf(u.y, dy2[k].y, rowsum[half][x][k]);
+                  else
                     colacc2[yy][k] = f2sub(colacc2[yy][k], f2mul(u, dy2[k]));
-                  }
                 }
               }
             }
-            lossrow[c] += lacc.x + lacc.y;
+            lhalf[c] = lacc;
+            if constexpr (GRAD) {
+              if (c == 0) {
+#pragma unroll
+                for (int k = 0; k < Q; ++k)  // row += c dy: kruskal c = -u, guttman c = u
+                  rowsum[half][x][k] += KR ? -(racc[k].x + racc[k].y) : (racc[k].x + racc[k].y);
+              }
+            }
           }
         };
         if (edge)
@@ -304,9 +321,9 @@ __global__ void __launch_bounds__(kThreads, MODE != 0 ? 2 : 3) stress_tma_kernel
           pairs_packed();
         else
           pairs(std::false_type{});
-#pragma unroll
-        for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lossrow[c]);
       }
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lhalf[c].x) + static_cast<double>(lhalf[c].y);
       if constexpr (GRAD) {
         if (half == 1) {
 #pragma unroll
