@@ -269,6 +269,61 @@ Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, doubl
   return r;
 }
 
+GdState Engine::device_gd(int kind, double delta, double f, double step, int it, int pred, int max_iters,
+                          double rel_tol, std::vector<double>& history) {
+  if (!sq2.get()) {
+    sq2.alloc(2 * kSqBlocks);
+    gdst.alloc(2);
+  }
+  if (hist.n < static_cast<size_t>(max_iters) + 1) hist.alloc(static_cast<size_t>(max_iters) + 1);
+  if (!gnext.get()) gnext.alloc(static_cast<size_t>(n * Q));
+  const double s0 = pred == 0 ? step : step * 0.5, s1 = pred == 0 ? step * 0.5 : step;
+  // prime: the trial pair of iteration `it` and its fused pass (as fused_trials, without the round trip)
+  const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
+                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sq2.get(), scal.get(), st);
+  PassArgs b = args(kind, delta);
+  b.Y[0] = cand[0].get();
+  b.Y[1] = cand[1].get();
+  b.ncand = 2;
+  launch_pass_fused_f32(b, Q, st);
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get());
+  ++passes;
+  GdState S{};
+  S.f = f;
+  S.step = step;
+  S.it = it;
+  S.pred = pred;
+  GMDS_CUDA(cudaMemcpyAsync(gdst.get(), &S, sizeof S, cudaMemcpyHostToDevice, st));
+  int par = 0;
+  int issued = it;
+  for (;;) {
+    const int batch = std::max(1, std::min(16, max_iters - issued));
+    for (int k = 0; k < batch; ++k) {
+      launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + par * kSqBlocks, nsq,
+                     sq2.get() + (par ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
+                     cand[1].get(), gnext.get(), graw.get(), n * Q, hist.get(), max_iters, rel_tol, st);
+      par ^= 1;
+      b.halt = &gdst.get()[par].stop;
+      launch_pass_fused_f32(b, Q, st);
+      launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get(),
+                         b.halt);
+    }
+    issued += batch;
+    GMDS_CUDA(cudaMemcpyAsync(&S, gdst.get() + par, sizeof S, cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    if (S.stop != 0) break;
+  }
+  // passes: the prime plus one per decision that continued (all accepted ones but a final stop)
+  passes += (S.it - it) - (S.stop == 1 ? 1 : 0);
+  if (S.it > it) {
+    std::vector<double> h(static_cast<size_t>(S.it - it));
+    GMDS_CUDA(cudaMemcpyAsync(h.data(), hist.get() + it + 1, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    history.insert(history.end(), h.begin(), h.end());
+  }
+  return S;
+}
+
 double Engine::scale_grad(double scale) {
   launch_scale_sqnorm(graw.get(), n * Q, scale, scal.get() + 4, sqpart.get(), st);
   double gsq = 0.0;
@@ -425,10 +480,37 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
   const bool spec = E.fused_ok() && !std::getenv("GMDS_NO_SPECULATION");
   bool have_grad = false;  // graw holds the raw gradient at Y (speculative mode)
   int pred = 0;            // 0: step accepted last time, 1: step/2
+  // Device-resident loop (fp32 storage): iterations whose predicted trial is
+  // accepted run without a host round trip (gd_step_kernel); GMDS_HOST_GD=1
+  // keeps every decision on the host (same arithmetic, same trajectory).
+  const bool devloop = spec && !std::getenv("GMDS_HOST_GD");
   for (; it < max_iters; ++it) {
     Engine::GradTrials gt;
     int slot_of[2] = {0, 1};  // slot of (step, step/2) in gt.trial / E.cand
-    if (spec) {
+    bool decided_on_device = false;
+    if (devloop && have_grad) {
+      const GdState S = E.device_gd(kind, rp.delta, f, step, it, pred, max_iters, rel_tol, r.history);
+      it = S.it;
+      f = S.f;
+      step = S.step;
+      pred = S.pred;
+      if (S.stop == 1) {
+        stalled = S.stalled != 0;
+        break;
+      }
+      // stop 2: iteration `it` is decided here, from the device's sums
+      gt.raw = 0.0;
+      gt.gsq = S.gsq;
+      gt.trial[0] = S.t0;
+      gt.trial[1] = S.t1;
+      if (pred == 1) {
+        slot_of[0] = 1;
+        slot_of[1] = 0;
+      }
+      decided_on_device = true;
+    }
+    if (decided_on_device) {
+    } else if (spec) {
       if (!have_grad) {
         const double raw0 = E.grad_raw(kind, rp.delta, E.Y.get());
         if (it == 0) {

@@ -54,6 +54,15 @@ struct Engine {
   GradTrials fused_trials(int kind, double delta, double s0, double s1);
   DevBuf<double> gnext;
   DevBuf<double> gpart;  // two-level row reduction scratch
+  // Device-resident gradient descent (gd_step_kernel): from a state where graw
+  // holds the raw gradient at Y and losspart column 0 the raw loss at Y, run
+  // iterations on the device until one finishes the fit (stop 1) or needs the
+  // host (stop 2: that iteration's trial losses and |g|^2 are in the state).
+  // Appends the accepted losses to history.
+  GdState device_gd(int kind, double delta, double f, double step, int it, int pred, int max_iters, double rel_tol,
+                    std::vector<double>& history);
+  DevBuf<double> sq2, hist;
+  DevBuf<GdState> gdst;
   double loss_of(int kind, double raw) const;
 };
 

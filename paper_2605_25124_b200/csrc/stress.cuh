@@ -29,6 +29,14 @@ struct PassArgs {
   double* losspart;         // [nchunks][kMaxCand] (rows kernel: [n][kMaxCand])
   int64_t cand_stride_row;  // elements between candidates' rowpart images (fused trial passes)
   int64_t cand_stride_col;  // elements between candidates' colpart images
+  const int* halt;          // device flag: nonzero -> the pass is a no-op (device-resident loops)
+};
+
+// Device-resident gradient descent state (double-buffered by iteration parity)
+struct GdState {
+  double f, step;
+  double t0, t1, gsq;  // the last decided pass: raw trial losses (slot order), |g|^2
+  int it, pred, stop, stalled;  // stop: 0 running, 1 finished, 2 iteration handed to the host
 };
 
 struct Steps {
@@ -39,7 +47,12 @@ struct Steps {
 void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage, cudaStream_t st);
 // gpart (reduce_rows_scratch(nb, q) doubles): the two-level reduction; nullptr: one-level
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
-                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart = nullptr);
+                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart = nullptr,
+                        const int* halt = nullptr);
+void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
+                    int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
+                    double* cand1, const double* gnext, double* graw, int64_t m, double* history, int max_iters,
+                    double rel_tol, cudaStream_t st);
 size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass

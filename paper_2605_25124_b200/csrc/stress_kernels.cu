@@ -88,7 +88,8 @@ __global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const dou
 constexpr int kRedGroups = 8;
 __global__ void reduce_groups_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart,
                                      const int64_t* __restrict__ strip_first, int64_t nb, int Q,
-                                     double* __restrict__ gpart) {
+                                     double* __restrict__ gpart, const int* __restrict__ halt) {
+  if (halt && *halt) return;
   const int64_t R = blockIdx.x / kRedGroups;
   const int s = blockIdx.x % kRedGroups;
   const int64_t c0 = strip_first[R], nrow = strip_first[R + 1] - c0;
@@ -103,7 +104,9 @@ __global__ void reduce_groups_kernel(const double* __restrict__ rowpart, const d
   }
   gpart[(R * kRedGroups + s) * run + e] = acc;
 }
-__global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int Q, double* __restrict__ out) {
+__global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int Q, double* __restrict__ out,
+                               const int* __restrict__ halt) {
+  if (halt && *halt) return;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n * Q) return;
   const int64_t r = idx / Q, R = r / kPT;
@@ -158,36 +161,59 @@ __global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double sc
 // (embed.cpp:179-181 for Kruskal; 2/sum(D) for Sammon; 1 otherwise), scales
 // its slice of g, writes the two trial points Y - s0 g and Y - s1 g, and leaves
 // a per-block partial of |g|^2 (summed in order on the host).
-__global__ void finish_grad_kernel(const double* __restrict__ losspart, int64_t nparts, int stride, int kind,
-                                   double sum_sq, double sum, double* __restrict__ g, const double* __restrict__ Y,
-                                   int64_t m, double s0, double s1, double* __restrict__ T0, double* __restrict__ T1,
-                                   double* __restrict__ sqpart, double* __restrict__ raw_out) {
-  __shared__ double red[256];
-  double r = 0.0;
-  for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) r += losspart[k * stride];
-  red[threadIdx.x] = r;
+// Strided partial sums over VT virtual threads then a pairwise tree -- the
+// exact order of a VT-thread CTA doing `for k = t; k < count; k += VT`
+// followed by `red[t] += red[t + w]` (VT = 256: finish_grad_kernel; VT =
+// 1024: sum_parts_kernel), computed by a 256-thread CTA: every caller of
+// the same (part, count, stride, slot, VT) gets the same bits.
+template <int VT>
+__device__ double tree_sum(const double* __restrict__ part, int64_t count, int stride, int slot, double* red) {
+  constexpr int per = VT / 256;
+#pragma unroll
+  for (int u = 0; u < per; ++u) {
+    const int t = threadIdx.x + 256 * u;
+    double r = 0.0;
+    for (int64_t k = t; k < count; k += VT) r += part[k * stride + slot];
+    red[t] = r;
+  }
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+  for (int w = VT / 2; w > 0; w >>= 1) {
+#pragma unroll
+    for (int u = 0; u < per; ++u) {
+      const int t = threadIdx.x + 256 * u;
+      if (t < w) red[t] += red[t + w];
+    }
     __syncthreads();
   }
-  const double raw = red[0];
+  const double v = red[0];
   __syncthreads();
-  double scale = 1.0;
+  return v;
+}
+
+// the kind's gradient scale at a raw loss (embed.cpp:179-181 Kruskal, 2/sum(D) Sammon, 1 otherwise)
+__device__ __forceinline__ double grad_scale(int kind, double raw, double sum_sq, double sum) {
   if (kind == kKruskal) {
     const double ks = sqrt(raw / sum_sq);
-    scale = (ks <= 0.0) ? 0.0 : 1.0 / (ks * sum_sq);
-  } else if (kind == kSammon) {
-    scale = 2.0 * (1.0 / sum);
+    return (ks <= 0.0) ? 0.0 : 1.0 / (ks * sum_sq);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *raw_out = raw;
+  if (kind == kSammon) return 2.0 * (1.0 / sum);
+  return 1.0;
+}
+
+// g *= scale over this grid's slice, trial points T0/T1 = Y - s g, |g|^2 block partial.
+// Y and T0 may alias (the device loop's accepted point): each element is read then written
+// by one thread.
+__device__ void finish_body(double scale, double* __restrict__ g, const double* Y, int64_t m, double s0,
+                            double s1, double* T0, double* __restrict__ T1, double* __restrict__ sqpart,
+                            double* red, double* Ycopy = nullptr, const double* gsrc = nullptr) {
   double sq = 0.0;
   for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double v = g[k] * scale;
+    const double v = (gsrc ? gsrc[k] : g[k]) * scale;
     g[k] = v;
     sq += v * v;
     const double y = Y[k];
+    if (Ycopy) Ycopy[k] = y;
     T0[k] = y - s0 * v;
     T1[k] = y - s1 * v;
   }
@@ -198,6 +224,107 @@ __global__ void finish_grad_kernel(const double* __restrict__ losspart, int64_t 
     __syncthreads();
   }
   if (threadIdx.x == 0) sqpart[blockIdx.x] = red[0];
+}
+
+__global__ void finish_grad_kernel(const double* __restrict__ losspart, int64_t nparts, int stride, int kind,
+                                   double sum_sq, double sum, double* __restrict__ g, const double* __restrict__ Y,
+                                   int64_t m, double s0, double s1, double* __restrict__ T0, double* __restrict__ T1,
+                                   double* __restrict__ sqpart, double* __restrict__ raw_out) {
+  __shared__ double red[256];
+  const double raw = tree_sum<256>(losspart, nparts, stride, 0, red);
+  const double scale = grad_scale(kind, raw, sum_sq, sum);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *raw_out = raw;
+  finish_body(scale, g, Y, m, s0, s1, T0, T1, sqpart, red);
+}
+
+// Device-resident gradient descent (fp32 storage, fused passes): one launch
+// per iteration decides the previous fused pass exactly as the host loop
+// (fit.cu gradient_descent: Armijo in the reference's order, embed.cpp:236-
+// 262) and, in the common case -- the trial in slot 0 accepted, so its
+// gradient is already in gnext -- moves Y to it, records the history, and
+// forms the next trial pair.  Every CTA evaluates the same decision on the
+// same bits (no grid sync); the state is double-buffered by iteration
+// parity.  Anything else (slot 1 accepted, no trial accepted, |g|^2 <= 0)
+// hands the iteration back to the host (stop = 2) untouched.
+__global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ losspart, int64_t nparts,
+                               int stride, const double* __restrict__ sqprev, int nsq, double* __restrict__ sqnext,
+                               int kind, double sum_sq, double sum, double* __restrict__ Y, double* cand0,
+                               double* __restrict__ cand1, const double* __restrict__ gnext,
+                               double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
+                               double rel_tol) {
+  __shared__ double red[1024];
+  __shared__ double sgsq;
+  const GdState S = st[par];
+  GdState* N = st + (par ^ 1);
+  const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  if (S.stop) {
+    if (lead) *N = S;
+    return;
+  }
+  // the same sums the host path reads: trial losses as sum_parts_kernel, |g|^2 in order
+  const double t0 = tree_sum<1024>(losspart, nparts, stride, 0, red);
+  const double t1 = tree_sum<1024>(losspart, nparts, stride, 1, red);
+  if (threadIdx.x == 0) {
+    double gq = 0.0;
+    for (int b = 0; b < nsq; ++b) gq += sqprev[b];
+    sgsq = gq;
+  }
+  __syncthreads();
+  const double gsq = sgsq;
+  GdState R = S;
+  R.t0 = t0;
+  R.t1 = t1;
+  R.gsq = gsq;
+  auto loss_of = [&](double raw) {
+    if (kind == kKruskal) return sqrt(__ddiv_rn(raw, sum_sq));
+    if (kind == kSammon) return __dmul_rn(__ddiv_rn(1.0, sum), raw);
+    return raw;
+  };
+  int acc_c = -1;
+  double f_new = S.f, sc_acc = 0.0;
+  if (gsq > 0.0) {
+    for (int c = 0; c < 2; ++c) {  // step, then step/2 (the reference's order)
+      const double sc = (c == 0) ? S.step : __dmul_rn(S.step, 0.5);
+      const int slot = (S.pred == 0) ? c : 1 - c;
+      const double fc = loss_of(slot == 0 ? t0 : t1);
+      if (fc <= __dsub_rn(S.f, __dmul_rn(__dmul_rn(1e-4, sc), gsq))) {
+        acc_c = c;
+        f_new = fc;
+        sc_acc = sc;
+        break;
+      }
+    }
+  }
+  if (acc_c < 0 || ((S.pred == 0) ? acc_c : 1 - acc_c) != 0) {  // host takes this iteration
+    R.stop = 2;
+    if (lead) *N = R;
+    return;
+  }
+  const double decrease = __ddiv_rn(__dsub_rn(S.f, f_new), fmax(S.f, 1e-300));
+  R.f = f_new;
+  R.it = S.it + 1;
+  R.step = __dmul_rn(sc_acc, 2.0);
+  if (decrease < rel_tol) {
+    R.stop = 1;
+    R.stalled = 1;
+  } else if (R.it >= max_iters) {
+    R.stop = 1;
+  }
+  if (lead) {
+    history[R.it] = f_new;
+    *N = R;
+  }
+  // Y <- cand0 (the accepted point); graw <- scaled gradient there; next trial pair
+  const double scale = grad_scale(kind, tree_sum<256>(losspart, nparts, stride, 0, red), sum_sq, sum);
+  const double s0 = (S.pred == 0) ? R.step : __dmul_rn(R.step, 0.5);
+  const double s1 = (S.pred == 0) ? __dmul_rn(R.step, 0.5) : R.step;
+  if (R.stop) {  // final point only
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      Y[k] = cand0[k];
+    return;
+  }
+  finish_body(scale, graw, cand0, m, s0, s1, cand0, cand1, sqnext, red, Y, gnext);
 }
 
 // out_c = Y - step_c * G for each candidate (trial = coords - step * grad, embed.cpp:243).
@@ -249,13 +376,13 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
 }
 
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
-                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart) {
+                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart, const int* halt) {
   if (gpart) {
     reduce_groups_kernel<<<static_cast<unsigned>(nb * kRedGroups), kPT * q, 0, st>>>(rowpart, colpart, strip_first,
-                                                                                    nb, q, gpart);
+                                                                                    nb, q, gpart, halt);
     count_launch();
     check_launch("reduce_groups_kernel");
-    combine_kernel<<<static_cast<unsigned>(ceil_div(n * q, 256)), 256, 0, st>>>(gpart, n, q, out);
+    combine_kernel<<<static_cast<unsigned>(ceil_div(n * q, 256)), 256, 0, st>>>(gpart, n, q, out, halt);
     count_launch();
     check_launch("combine_kernel");
     return;
@@ -278,6 +405,16 @@ int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int k
   count_launch();
   check_launch("finish_grad_kernel");
   return blocks;
+}
+
+void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
+                    int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
+                    double* cand1, const double* gnext, double* graw, int64_t m, double* history, int max_iters,
+                    double rel_tol, cudaStream_t st) {
+  gd_step_kernel<<<nsq, 256, 0, st>>>(st2, par, losspart, nparts, stride, sqprev, nsq, sqnext, kind, sum_sq, sum, Y,
+                                      cand0, cand1, gnext, graw, m, history, max_iters, rel_tol);
+  count_launch();
+  check_launch("gd_step_kernel");
 }
 
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st) {

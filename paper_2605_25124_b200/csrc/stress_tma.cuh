@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kern
   __shared__ float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
+  if (a.halt && *a.halt) return;
   const int tid = threadIdx.x;
   const int ti = tid / kTG, tj = tid % kTG;
   const int64_t chunk = blockIdx.x;

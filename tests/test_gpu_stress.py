@@ -355,6 +355,28 @@ def test_speculative_trial_gradient_identical(monkeypatch, kind, q):
     assert np.max(np.abs(h - ho) / ho) <= TRAJ
 
 
+@pytest.mark.parametrize("kind,rel_tol,iters", [("kruskal", 1e-300, 60), ("kruskal", 1e-4, 500),
+                                                ("sammon", 1e-300, 37), ("huber", 1e-5, 300)])
+def test_device_resident_descent_identical(monkeypatch, kind, rel_tol, iters):
+    # gd_step_kernel decides accepted iterations on the device (no host round
+    # trip) with the host loop's arithmetic: same history, coordinates,
+    # iteration count and converged flag as GMDS_HOST_GD=1, through the
+    # max_iters and rel_tol exits and the hand-backs to the host
+    rng = np.random.default_rng(21)
+    n = 2400
+    X = rng.standard_normal((n, 5)) * np.linspace(2.0, 0.5, 5)
+    D = G.pairwise_matrix(X, 2.0)
+    Y0 = rng.normal(0.0, 0.1, (n, 2))
+    hd = 0.5 * float(np.median(D)) if kind == "huber" else None
+    a = G.minimize_stress(D, 2, kind, huber_delta=hd, max_iters=iters, rel_tol=rel_tol, Y0=Y0, storage=G.F32)
+    monkeypatch.setenv("GMDS_HOST_GD", "1")
+    b = G.minimize_stress(D, 2, kind, huber_delta=hd, max_iters=iters, rel_tol=rel_tol, Y0=Y0, storage=G.F32)
+    assert a["iterations"] == b["iterations"] and a["converged"] == b["converged"]
+    assert np.array_equal(np.array(a["stress_history"]), np.array(b["stress_history"]))
+    assert np.array_equal(a["coords"], b["coords"])
+    assert a["passes"] == b["passes"]
+
+
 def test_tune_batched_eigensolver_matches(monkeypatch):
     # tune_nu's classical cells of a fold go through one batched eigensolver call;
     # per-cell dense solves give the same mean stresses
