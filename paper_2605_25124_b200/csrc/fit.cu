@@ -159,7 +159,7 @@ double Engine::grad_raw(int kind, double delta, const double* Yd) {
   a.ncand = 1;
   launch_stress_pass(a, Q, true, D->storage, st);
   if (!rows_mode)
-    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get());
+    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get(), nullptr, f32parts());
   else
     GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
@@ -198,10 +198,11 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
   a.chunk_I = chunk_I.get() + c0;
   a.chunk_J0 = chunk_J0.get() + c0;
   a.nchunks = c1 - c0;
-  a.rowpart = rowpart.get() + c0 * kPT * Q;
+  a.rowpart = f32parts() ? reinterpret_cast<double*>(reinterpret_cast<float*>(rowpart.get()) + c0 * kPT * Q)
+                        : rowpart.get() + c0 * kPT * Q;
   a.losspart = losspart.get() + c0 * kMaxCand;
   if (a.nchunks > 0) launch_stress_pass(a, Q, true, D->storage, st);
-  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get());
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get(), nullptr, f32parts());
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
   double out = 0.0;
   GMDS_CUDA(cudaMemcpyAsync(&out, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -217,7 +218,7 @@ Engine::GradTrials Engine::grad_and_trials(int kind, double delta, double s0, do
   a.ncand = 1;
   launch_stress_pass(a, Q, true, D->storage, st);
   if (!rows_mode)
-    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get());
+    launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, graw.get(), st, gpart.get(), nullptr, f32parts());
   else
     GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
   const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
@@ -252,7 +253,7 @@ Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, doubl
   b.Y[1] = cand[1].get();
   b.ncand = 2;
   launch_pass_fused_f32(b, Q, st);
-  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get());
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get(), nullptr, f32parts());
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 2, scal.get() + 1, st);
   double h[3];
   std::vector<double> sq(static_cast<size_t>(nsq));
@@ -286,7 +287,10 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   b.Y[1] = cand[1].get();
   b.ncand = 2;
   launch_pass_fused_f32(b, Q, st);
-  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get());
+  double* pre = scal.get() + 5;  // the pass's loss sums (reduction launch's extra CTA; q >= 2)
+  const bool have_pre = kPT * Q >= 256;
+  launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(), nullptr,
+                     f32parts(), losspart.get(), nchunks, kMaxCand, have_pre ? pre : nullptr);
   ++passes;
   GdState S{};
   S.f = f;
@@ -301,12 +305,13 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
     for (int k = 0; k < batch; ++k) {
       launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + par * kSqBlocks, nsq,
                      sq2.get() + (par ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
-                     cand[1].get(), gnext.get(), graw.get(), n * Q, hist.get(), max_iters, rel_tol, st);
+                     cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
+                     rel_tol, have_pre ? pre : nullptr, st);
       par ^= 1;
       b.halt = &gdst.get()[par].stop;
       launch_pass_fused_f32(b, Q, st);
-      launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get(),
-                         b.halt);
+      launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(),
+                         b.halt, f32parts(), losspart.get(), nchunks, kMaxCand, have_pre ? pre : nullptr);
     }
     issued += batch;
     GMDS_CUDA(cudaMemcpyAsync(&S, gdst.get() + par, sizeof S, cudaMemcpyDeviceToHost, st));

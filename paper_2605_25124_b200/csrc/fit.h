@@ -51,6 +51,8 @@ struct Engine {
   // trial losses plus the raw gradient at cand[0] (into gnext; losspart column
   // 0 then holds the raw loss at cand[0]).
   bool fused_ok() const { return D->storage == GMDS_F32 && !rows_mode; }
+  // the tiled passes over fp32 storage (TMA kernels) leave fp32 row/column partials
+  bool f32parts() const { return D->storage == GMDS_F32 && !rows_mode; }
   GradTrials fused_trials(int kind, double delta, double s0, double s1);
   DevBuf<double> gnext;
   DevBuf<double> gpart;  // two-level row reduction scratch

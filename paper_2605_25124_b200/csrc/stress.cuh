@@ -24,8 +24,8 @@ struct PassArgs {
   const int64_t* chunk_J0;  // [nchunks]
   int64_t chunk_len;
   int64_t nchunks;
-  double* rowpart;          // [nchunks][kPT][Q]  (rows kernel: [n][q] final)
-  double* colpart;          // [nblk][kPT][Q]
+  double* rowpart;          // [nchunks][kPT][Q]  (rows kernel: [n][q] final; TMA passes: fp32 partials)
+  double* colpart;          // [nblk][kPT][Q]     (TMA passes: fp32 partials)
   double* losspart;         // [nchunks][kMaxCand] (rows kernel: [n][kMaxCand])
   int64_t cand_stride_row;  // elements between candidates' rowpart images (fused trial passes)
   int64_t cand_stride_col;  // elements between candidates' colpart images
@@ -48,11 +48,12 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
 // gpart (reduce_rows_scratch(nb, q) doubles): the two-level reduction; nullptr: one-level
 void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
                         int64_t nb, int q, double* out, cudaStream_t st, double* gpart = nullptr,
-                        const int* halt = nullptr);
+                        const int* halt = nullptr, bool f32parts = false, const double* losspart = nullptr,
+                        int64_t nparts = 0, int lstride = 0, double* sums = nullptr);
 void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
-                    double* cand1, const double* gnext, double* graw, int64_t m, double* history, int max_iters,
-                    double rel_tol, cudaStream_t st);
+                    double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
+                    double* history, int max_iters, double rel_tol, const double* pre, cudaStream_t st);
 size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass

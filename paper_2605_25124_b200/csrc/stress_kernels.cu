@@ -58,7 +58,58 @@ __global__ void stress_rows_kernel(PassArgs a, int q, int grad) {
 // Stage 2: out[r][k] = sum over strip-R chunks of rowpart + sum over I <= R of colpart(I, R).
 // Eight lanes per output (strided over the partial list), combined by a fixed
 // xor-tree: deterministic, and eight times the loads in flight.
-__global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+// Strided partial sums over VT virtual threads then a pairwise tree -- the
+// exact order of a VT-thread CTA doing `for k = t; k < count; k += VT`
+// followed by `red[t] += red[t + w]` (VT = 256: finish_grad_kernel; VT =
+// 1024: sum_parts_kernel), computed by a 256-thread CTA: every caller of
+// the same (part, count, stride, slot, VT) gets the same bits.
+// (Any blockDim >= 256: threads beyond 256 only take part in the barriers.)
+template <int VT>
+__device__ double tree_sum(const double* __restrict__ part, int64_t count, int stride, int slot, double* red) {
+  constexpr int per = VT / 256;
+  const bool act = threadIdx.x < 256;
+  if (act) {
+#pragma unroll
+    for (int u = 0; u < per; ++u) {
+      const int t = threadIdx.x + 256 * u;
+      double r = 0.0;
+      for (int64_t k = t; k < count; k += VT) r += part[k * stride + slot];
+      red[t] = r;
+    }
+  }
+  __syncthreads();
+  for (int w = VT / 2; w > 0; w >>= 1) {
+    if (act) {
+#pragma unroll
+      for (int u = 0; u < per; ++u) {
+        const int t = threadIdx.x + 256 * u;
+        if (t < w) red[t] += red[t + w];
+      }
+    }
+    __syncthreads();
+  }
+  const double v = red[0];
+  __syncthreads();
+  return v;
+}
+
+// The device loop's three loss sums of a fused pass (trial slots 0 and 1 as
+// sum_parts_kernel, slot 0 as finish_grad_kernel), by one extra CTA of the
+// reduction launch that follows the pass: out[0..2].
+__device__ void gd_pass_sums(const double* __restrict__ losspart, int64_t nparts, int stride, double* out) {
+  __shared__ double red[1024];
+  const double t0 = tree_sum<1024>(losspart, nparts, stride, 0, red);
+  const double t1 = tree_sum<1024>(losspart, nparts, stride, 1, red);
+  const double r0 = tree_sum<256>(losspart, nparts, stride, 0, red);
+  if (threadIdx.x == 0) {
+    out[0] = t0;
+    out[1] = t1;
+    out[2] = r0;
+  }
+}
+
+template <typename TP>
+__global__ void reduce_rows_kernel(const TP* __restrict__ rowpart, const TP* __restrict__ colpart,
                                    const int64_t* __restrict__ strip_first, int64_t n, int64_t nb, int Q,
                                    double* __restrict__ out) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -71,8 +122,8 @@ __global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const dou
     const int k = static_cast<int>(e % Q);
     const int64_t R = r / kPT, rr = r % kPT;
     const int64_t c0 = strip_first[R], c1 = strip_first[R + 1];
-    for (int64_t c = c0 + sub; c < c1; c += 8) s += rowpart[(c * kPT + rr) * Q + k];
-    for (int64_t I = sub; I <= R; I += 8) s += colpart[(blk_index(I, R, nb) * kPT + rr) * Q + k];
+    for (int64_t c = c0 + sub; c < c1; c += 8) s += static_cast<double>(rowpart[(c * kPT + rr) * Q + k]);
+    for (int64_t I = sub; I <= R; I += 8) s += static_cast<double>(colpart[(blk_index(I, R, nb) * kPT + rr) * Q + k]);
   }
   s += __shfl_xor_sync(0xffffffffu, s, 4);
   s += __shfl_xor_sync(0xffffffffu, s, 2);
@@ -85,11 +136,19 @@ __global__ void reduce_rows_kernel(const double* __restrict__ rowpart, const dou
 // partials of blocks (I, R), I <= R) for all 128 x Q entries at once -- every
 // term is a contiguous 128 x Q run, read coalesced -- and combine_kernel adds
 // the kRedGroups group sums of each entry in order.  Fixed order throughout.
+// TP: the partials' type (fp32 from the TMA passes, fp64 from the fp64 pass).
 constexpr int kRedGroups = 8;
-__global__ void reduce_groups_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart,
+template <typename TP>
+__global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* __restrict__ colpart,
                                      const int64_t* __restrict__ strip_first, int64_t nb, int Q,
-                                     double* __restrict__ gpart, const int* __restrict__ halt) {
+                                     double* __restrict__ gpart, const int* __restrict__ halt,
+                                     const double* __restrict__ losspart, int64_t nparts, int lstride,
+                                     double* __restrict__ sums) {
   if (halt && *halt) return;
+  if (blockIdx.x == nb * kRedGroups) {  // the extra CTA (device loop): the pass's loss sums
+    gd_pass_sums(losspart, nparts, lstride, sums);
+    return;
+  }
   const int64_t R = blockIdx.x / kRedGroups;
   const int s = blockIdx.x % kRedGroups;
   const int64_t c0 = strip_first[R], nrow = strip_first[R + 1] - c0;
@@ -98,9 +157,20 @@ __global__ void reduce_groups_kernel(const double* __restrict__ rowpart, const d
   const int e = threadIdx.x;  // (rr, k), < 128 Q
   const int64_t run = static_cast<int64_t>(kPT) * Q;
   double acc = 0.0;
-  for (int64_t t = t0; t < t1; ++t) {
-    const double* src = (t < nrow) ? rowpart + (c0 + t) * run : colpart + blk_index(t - nrow, R, nb) * run;
-    acc += src[e];
+  int64_t t = t0;
+  for (; t + 4 <= t1; t += 4) {  // four loads in flight, added in order
+    TP v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t tt = t + u;
+      v[u] = ((tt < nrow) ? rowpart + (c0 + tt) * run : colpart + blk_index(tt - nrow, R, nb) * run)[e];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc += static_cast<double>(v[u]);
+  }
+  for (; t < t1; ++t) {
+    const TP* src = (t < nrow) ? rowpart + (c0 + t) * run : colpart + blk_index(t - nrow, R, nb) * run;
+    acc += static_cast<double>(src[e]);
   }
   gpart[(R * kRedGroups + s) * run + e] = acc;
 }
@@ -161,35 +231,6 @@ __global__ void scale_sqnorm_kernel(double* __restrict__ g, int64_t m, double sc
 // (embed.cpp:179-181 for Kruskal; 2/sum(D) for Sammon; 1 otherwise), scales
 // its slice of g, writes the two trial points Y - s0 g and Y - s1 g, and leaves
 // a per-block partial of |g|^2 (summed in order on the host).
-// Strided partial sums over VT virtual threads then a pairwise tree -- the
-// exact order of a VT-thread CTA doing `for k = t; k < count; k += VT`
-// followed by `red[t] += red[t + w]` (VT = 256: finish_grad_kernel; VT =
-// 1024: sum_parts_kernel), computed by a 256-thread CTA: every caller of
-// the same (part, count, stride, slot, VT) gets the same bits.
-template <int VT>
-__device__ double tree_sum(const double* __restrict__ part, int64_t count, int stride, int slot, double* red) {
-  constexpr int per = VT / 256;
-#pragma unroll
-  for (int u = 0; u < per; ++u) {
-    const int t = threadIdx.x + 256 * u;
-    double r = 0.0;
-    for (int64_t k = t; k < count; k += VT) r += part[k * stride + slot];
-    red[t] = r;
-  }
-  __syncthreads();
-  for (int w = VT / 2; w > 0; w >>= 1) {
-#pragma unroll
-    for (int u = 0; u < per; ++u) {
-      const int t = threadIdx.x + 256 * u;
-      if (t < w) red[t] += red[t + w];
-    }
-    __syncthreads();
-  }
-  const double v = red[0];
-  __syncthreads();
-  return v;
-}
-
 // the kind's gradient scale at a raw loss (embed.cpp:179-181 Kruskal, 2/sum(D) Sammon, 1 otherwise)
 __device__ __forceinline__ double grad_scale(int kind, double raw, double sum_sq, double sum) {
   if (kind == kKruskal) {
@@ -249,9 +290,10 @@ __global__ void finish_grad_kernel(const double* __restrict__ losspart, int64_t 
 __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ losspart, int64_t nparts,
                                int stride, const double* __restrict__ sqprev, int nsq, double* __restrict__ sqnext,
                                int kind, double sum_sq, double sum, double* __restrict__ Y, double* cand0,
-                               double* __restrict__ cand1, const double* __restrict__ gnext,
+                               double* __restrict__ cand1, double* __restrict__ gnext,
+                               const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
-                               double rel_tol) {
+                               double rel_tol, const double* __restrict__ pre) {
   __shared__ double red[1024];
   __shared__ double sgsq;
   const GdState S = st[par];
@@ -262,11 +304,16 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     return;
   }
   // the same sums the host path reads: trial losses as sum_parts_kernel, |g|^2 in order
-  const double t0 = tree_sum<1024>(losspart, nparts, stride, 0, red);
-  const double t1 = tree_sum<1024>(losspart, nparts, stride, 1, red);
+  // the pass's loss sums: from the reduction launch's extra CTA when it ran, else here (same order)
+  const double t0 = pre ? pre[0] : tree_sum<1024>(losspart, nparts, stride, 0, red);
+  const double t1 = pre ? pre[1] : tree_sum<1024>(losspart, nparts, stride, 1, red);
+  // |g|^2 = the finish partials added in order (as the host does); staged through
+  // shared memory so the serial adds do not wait on 148 serial L2 loads
+  for (int b = threadIdx.x; b < nsq; b += blockDim.x) red[b] = sqprev[b];
+  __syncthreads();
   if (threadIdx.x == 0) {
     double gq = 0.0;
-    for (int b = 0; b < nsq; ++b) gq += sqprev[b];
+    for (int b = 0; b < nsq; ++b) gq += red[b];
     sgsq = gq;
   }
   __syncthreads();
@@ -295,9 +342,23 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
       }
     }
   }
+  // the raw gradient at cand0 (combine_kernel's sums, in its order) -> gnext
+  auto combine = [&]() {
+    const int64_t run = static_cast<int64_t>(kPT) * Q;
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      const int64_t r = k / Q, Rr = r / kPT;
+      const int64_t e = (r % kPT) * Q + k % Q;
+      double a = 0.0;
+#pragma unroll
+      for (int g = 0; g < kRedGroups; ++g) a += gpart[(Rr * kRedGroups + g) * run + e];
+      gnext[k] = a;
+    }
+  };
   if (acc_c < 0 || ((S.pred == 0) ? acc_c : 1 - acc_c) != 0) {  // host takes this iteration
     R.stop = 2;
     if (lead) *N = R;
+    combine();
     return;
   }
   const double decrease = __ddiv_rn(__dsub_rn(S.f, f_new), fmax(S.f, 1e-300));
@@ -315,7 +376,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     *N = R;
   }
   // Y <- cand0 (the accepted point); graw <- scaled gradient there; next trial pair
-  const double scale = grad_scale(kind, tree_sum<256>(losspart, nparts, stride, 0, red), sum_sq, sum);
+  const double scale = grad_scale(kind, pre ? pre[2] : tree_sum<256>(losspart, nparts, stride, 0, red), sum_sq, sum);
   const double s0 = (S.pred == 0) ? R.step : __dmul_rn(R.step, 0.5);
   const double s1 = (S.pred == 0) ? __dmul_rn(R.step, 0.5) : R.step;
   if (R.stop) {  // final point only
@@ -324,6 +385,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
       Y[k] = cand0[k];
     return;
   }
+  combine();  // each thread its own elements: read back below by the same thread
   finish_body(scale, graw, cand0, m, s0, s1, cand0, cand1, sqnext, red, Y, gnext);
 }
 
@@ -375,23 +437,37 @@ void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage,
   check_launch("stress_rows_kernel");
 }
 
-void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
-                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart, const int* halt) {
+template <typename TP>
+static void reduce_rows_t(const TP* rowpart, const TP* colpart, const int64_t* strip_first, int64_t n, int64_t nb,
+                          int q, double* out, cudaStream_t st, double* gpart, const int* halt,
+                          const double* losspart, int64_t nparts, int lstride, double* sums) {
   if (gpart) {
-    reduce_groups_kernel<<<static_cast<unsigned>(nb * kRedGroups), kPT * q, 0, st>>>(rowpart, colpart, strip_first,
-                                                                                    nb, q, gpart, halt);
+    const bool extra = sums != nullptr && kPT * q >= 256;
+    reduce_groups_kernel<TP><<<static_cast<unsigned>(nb * kRedGroups + (extra ? 1 : 0)), kPT * q, 0, st>>>(
+        rowpart, colpart, strip_first, nb, q, gpart, halt, losspart, nparts, lstride, extra ? sums : nullptr);
     count_launch();
     check_launch("reduce_groups_kernel");
+    if (!out) return;  // the caller adds the groups itself (gd_step_kernel)
     combine_kernel<<<static_cast<unsigned>(ceil_div(n * q, 256)), 256, 0, st>>>(gpart, n, q, out, halt);
     count_launch();
     check_launch("combine_kernel");
     return;
   }
   const int64_t m = n * q * 8;
-  reduce_rows_kernel<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, st>>>(rowpart, colpart, strip_first, n, nb,
-                                                                             q, out);
+  reduce_rows_kernel<TP><<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, st>>>(rowpart, colpart, strip_first, n,
+                                                                                 nb, q, out);
   count_launch();
   check_launch("reduce_rows_kernel");
+}
+
+void launch_reduce_rows(const double* rowpart, const double* colpart, const int64_t* strip_first, int64_t n,
+                        int64_t nb, int q, double* out, cudaStream_t st, double* gpart, const int* halt,
+                        bool f32parts, const double* losspart, int64_t nparts, int lstride, double* sums) {
+  if (f32parts)
+    reduce_rows_t(reinterpret_cast<const float*>(rowpart), reinterpret_cast<const float*>(colpart), strip_first, n,
+                  nb, q, out, st, gpart, halt, losspart, nparts, lstride, sums);
+  else
+    reduce_rows_t(rowpart, colpart, strip_first, n, nb, q, out, st, gpart, halt, losspart, nparts, lstride, sums);
 }
 
 size_t reduce_rows_scratch(int64_t nb, int q) { return static_cast<size_t>(nb) * kRedGroups * kPT * q; }
@@ -409,10 +485,10 @@ int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int k
 
 void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
-                    double* cand1, const double* gnext, double* graw, int64_t m, double* history, int max_iters,
-                    double rel_tol, cudaStream_t st) {
+                    double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
+                    double* history, int max_iters, double rel_tol, const double* pre, cudaStream_t st) {
   gd_step_kernel<<<nsq, 256, 0, st>>>(st2, par, losspart, nparts, stride, sqprev, nsq, sqnext, kind, sum_sq, sum, Y,
-                                      cand0, cand1, gnext, graw, m, history, max_iters, rel_tol);
+                                      cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre);
   count_launch();
   check_launch("gd_step_kernel");
 }

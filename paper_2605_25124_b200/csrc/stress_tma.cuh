@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kern
         float s = 0.f;
 #pragma unroll
         for (int t = 0; t < kTG; ++t) s += sRed[(k * kTG + t) * kPT + col];
-        a.colpart[(blk * kPT + col) * Q + k] = static_cast<double>(s);
+        reinterpret_cast<float*>(a.colpart)[(blk * kPT + col) * Q + k] = s;  // fp32 partials (exact as summed)
       }
     }
   }
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kern
           float v = rowsum[hh][x][k];
 #pragma unroll
           for (int m = 8; m > 0; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-          if (tj == 0) a.rowpart[(chunk * kPT + hh * kHalfRows + ti * kMR + x) * Q + k] = static_cast<double>(v);
+          if (tj == 0) reinterpret_cast<float*>(a.rowpart)[(chunk * kPT + hh * kHalfRows + ti * kMR + x) * Q + k] = v;
         }
   }
 #pragma unroll
