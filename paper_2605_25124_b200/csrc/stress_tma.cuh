@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kern
   constexpr int NS = GRAD ? kStagesGrad : kStages;
   float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
   __shared__ __align__(8) uint64_t bars[NS];
-  __shared__ float sYi[NCM][kPT][Q];
-  __shared__ float sYj[2][NCM][kPT][Q];  // [block parity][cand][yslot(r)][k]: double-buffered
+  __shared__ __align__(16) float sYi[NCM][kPT][Q];
+  __shared__ __align__(16) float sYj[2][NCM][kPT][Q];  // [block parity][cand][yslot(r)][k]: double-buffered
   __shared__ float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
@@ -158,6 +158,15 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kern
         for (int k = 0; k < Q; ++k) rowsum[hh][x][k] = 0.f;
   }
   float2 yj2[NCM][kMT / 2][Q];  // this thread's 8 columns as (y, y+1) pairs, loaded once per block
+  // Q = 2: thread (c = tid / 128, r = tid % 128) stages point r of candidate c
+  // as one 16-byte load, prefetched a block ahead into registers
+  const int sc = tid >> 7, sr = tid & (kPT - 1);
+  auto col_load = [&](int64_t J) {
+    const int64_t j = J * kPT + sr;
+    return (sc < nc && j < a.n) ? reinterpret_cast<const double2*>(a.Y[sc])[j] : make_double2(0.0, 0.0);
+  };
+  double2 ycol = make_double2(0.0, 0.0);
+  if constexpr (Q == 2) ycol = col_load(J0);
 
   // Barriers per block: one after the column coordinates are staged (their
   // buffer alternates, so no barrier is needed before writing it), one per
@@ -165,20 +174,37 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kern
   for (int b = 0; b < nblocks; ++b) {
     const int64_t J = J0 + b;
     const int yb = b & 1;
-    for (int e = tid; e < nc * kPT * Q; e += kThreads) {
-      const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
-      const int64_t j = J * kPT + r;
-      sYj[yb][c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+    if constexpr (Q == 2) {
+      if (sc < NCM)
+        *reinterpret_cast<float2*>(&sYj[yb][sc][yslot(sr)][0]) =
+            make_float2(static_cast<float>(ycol.x), static_cast<float>(ycol.y));
+      if (b + 1 < nblocks) ycol = col_load(J + 1);
+    } else {
+      for (int e = tid; e < nc * kPT * Q; e += kThreads) {
+        const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
+        const int64_t j = J * kPT + r;
+        sYj[yb][c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < NCM; ++c)
 #pragma unroll
-      for (int y = 0; y < kMT; y += 2)
+      for (int y = 0; y < kMT; y += 2) {
+        if constexpr (Q == 2) {
+          const float2 p0 = (c < nc) ? *reinterpret_cast<const float2*>(&sYj[yb][c][y * kTG + tj][0])
+                                     : make_float2(0.f, 0.f);
+          const float2 p1 = (c < nc) ? *reinterpret_cast<const float2*>(&sYj[yb][c][(y + 1) * kTG + tj][0])
+                                     : make_float2(0.f, 0.f);
+          yj2[c][y / 2][0] = make_float2(p0.x, p1.x);
+          yj2[c][y / 2][1] = make_float2(p0.y, p1.y);
+        } else {
 #pragma unroll
-        for (int k = 0; k < Q; ++k)
-          yj2[c][y / 2][k] = (c < nc) ? make_float2(sYj[yb][c][y * kTG + tj][k], sYj[yb][c][(y + 1) * kTG + tj][k])
-                                      : make_float2(0.f, 0.f);
+          for (int k = 0; k < Q; ++k)
+            yj2[c][y / 2][k] = (c < nc) ? make_float2(sYj[yb][c][y * kTG + tj][k], sYj[yb][c][(y + 1) * kTG + tj][k])
+                                        : make_float2(0.f, 0.f);
+        }
+      }
     float2 colacc2[GRAD ? kMT / 2 : 1][Q];  // column sums of columns (y, y+1)
     if constexpr (GRAD) {
 #pragma unroll
