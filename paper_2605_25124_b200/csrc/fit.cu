@@ -37,7 +37,15 @@ namespace gmds {
 
 namespace {
 
-constexpr int64_t kChunk = 4;
+// blocks per CTA of a tiled pass (one block row); GMDS_STRESS_CHUNK overrides (tuning)
+int64_t chunk_blocks() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("GMDS_STRESS_CHUNK");
+    const int64_t c = e ? std::atoll(e) : 4;
+    return c > 0 ? c : 4;
+  }();
+  return v;
+}
 constexpr double kTiny = 1e-300;  // embed.cpp:13
 
 int padded_q(int q) { return q <= 4 ? q : q; }
@@ -69,7 +77,7 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
     std::vector<int64_t> cI, cJ, sf;
     for (int64_t I = 0; I < nb; ++I) {
       sf.push_back(static_cast<int64_t>(cI.size()));
-      for (int64_t J0 = I; J0 < nb; J0 += kChunk) {
+      for (int64_t J0 = I; J0 < nb; J0 += chunk_blocks()) {
         cI.push_back(I);
         cJ.push_back(J0);
       }
@@ -129,7 +137,7 @@ PassArgs Engine::args(int kind, double delta) const {
   a.huber_delta = delta;
   a.chunk_I = chunk_I.get();
   a.chunk_J0 = chunk_J0.get();
-  a.chunk_len = kChunk;
+  a.chunk_len = chunk_blocks();
   a.nchunks = nchunks;
   a.rowpart = rowpart.get();
   a.colpart = colpart.get();
@@ -175,7 +183,7 @@ double Engine::grad_raw(int kind, double delta, const double* Yd) {
 // summed across ranks by an all-reduce.
 double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shard, int nshards) {
   if (rows_mode) fail(GMDS_INVALID_INPUT, "stress_partial: sharded passes support q <= 4");
-  // chunk c covers (blocks) kChunk... weight = number of blocks; split the prefix sum evenly
+  // chunk c covers up to chunk_blocks() blocks... weight = number of blocks; split the prefix sum evenly
   std::vector<int64_t> cI(static_cast<size_t>(nchunks)), cJ(static_cast<size_t>(nchunks));
   GMDS_CUDA(cudaMemcpyAsync(cI.data(), chunk_I.get(), nchunks * 8, cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaMemcpyAsync(cJ.data(), chunk_J0.get(), nchunks * 8, cudaMemcpyDeviceToHost, st));
@@ -184,7 +192,7 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
   int64_t acc = 0, c0 = nchunks, c1 = nchunks;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t before = acc;
-    acc += std::min<int64_t>(kChunk, nb - cJ[c]);
+    acc += std::min<int64_t>(chunk_blocks(), nb - cJ[c]);
     if (c0 == nchunks && before * nshards >= nblk * shard) c0 = c;
     if (c1 == nchunks && before * nshards >= nblk * (shard + 1)) c1 = c;
   }
