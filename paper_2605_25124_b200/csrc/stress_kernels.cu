@@ -96,16 +96,12 @@ __device__ double tree_sum(const double* __restrict__ part, int64_t count, int s
 // The device loop's three loss sums of a fused pass (trial slots 0 and 1 as
 // sum_parts_kernel, slot 0 as finish_grad_kernel), by one extra CTA of the
 // reduction launch that follows the pass: out[0..2].
-__device__ void gd_pass_sums(const double* __restrict__ losspart, int64_t nparts, int stride, double* out) {
+__device__ void gd_pass_sums(const double* __restrict__ losspart, int64_t nparts, int stride, double* out,
+                             int which) {  // one sum per CTA: 0, 1 = trial slots, 2 = slot 0 (finish order)
   __shared__ double red[1024];
-  const double t0 = tree_sum<1024>(losspart, nparts, stride, 0, red);
-  const double t1 = tree_sum<1024>(losspart, nparts, stride, 1, red);
-  const double r0 = tree_sum<256>(losspart, nparts, stride, 0, red);
-  if (threadIdx.x == 0) {
-    out[0] = t0;
-    out[1] = t1;
-    out[2] = r0;
-  }
+  const double v = (which == 2) ? tree_sum<256>(losspart, nparts, stride, 0, red)
+                                : tree_sum<1024>(losspart, nparts, stride, which, red);
+  if (threadIdx.x == 0) out[which] = v;
 }
 
 template <typename TP>
@@ -145,8 +141,8 @@ __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* _
                                      const double* __restrict__ losspart, int64_t nparts, int lstride,
                                      double* __restrict__ sums) {
   if (halt && *halt) return;
-  if (blockIdx.x == nb * kRedGroups) {  // the extra CTA (device loop): the pass's loss sums
-    gd_pass_sums(losspart, nparts, lstride, sums);
+  if (blockIdx.x >= nb * kRedGroups) {  // the extra CTAs (device loop): the pass's loss sums
+    gd_pass_sums(losspart, nparts, lstride, sums, static_cast<int>(blockIdx.x - nb * kRedGroups));
     return;
   }
   const int64_t R = blockIdx.x / kRedGroups;
@@ -443,7 +439,7 @@ static void reduce_rows_t(const TP* rowpart, const TP* colpart, const int64_t* s
                           const double* losspart, int64_t nparts, int lstride, double* sums) {
   if (gpart) {
     const bool extra = sums != nullptr && kPT * q >= 256;
-    reduce_groups_kernel<TP><<<static_cast<unsigned>(nb * kRedGroups + (extra ? 1 : 0)), kPT * q, 0, st>>>(
+    reduce_groups_kernel<TP><<<static_cast<unsigned>(nb * kRedGroups + (extra ? 3 : 0)), kPT * q, 0, st>>>(
         rowpart, colpart, strip_first, nb, q, gpart, halt, losspart, nparts, lstride, extra ? sums : nullptr);
     count_launch();
     check_launch("reduce_groups_kernel");
