@@ -25,7 +25,7 @@ struct MergeArgs {
   SplitArgs s;
   const uint16_t* sidx;  // per row, its nonzero features sorted by value (rowptr layout)
   const void* svs;       // per row, its nonzero values sorted ascending (rowptr layout)
-  int fast;              // try the rank-by-counting path first (GMDS_MERGE_NOFAST=1 disables)
+  int fast;              // try the rank-by-counting path first (GMDS_MERGE_FAST=1 enables)
   int linear;            // every nu is 2 or 3: the linear-weight path (gmd_pair)
   const uint16_t* pmap;  // row store: sorted position of each nonzero (feature order)
   const double* suf;     // row store: suffix sums of the sorted values

@@ -381,7 +381,9 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       ma.s.sparse = 1;
       ma.sidx = rs.sidx.get();
       ma.svs = rs.svs.get();
-      ma.fast = std::getenv("GMDS_MERGE_NOFAST") ? 0 : 1;
+      // rank-by-counting first: exact, but measured slower than the merge path on the
+      // metric data (0.83 vs 0.72 s), so opt-in (GMDS_MERGE_FAST=1)
+      ma.fast = std::getenv("GMDS_MERGE_FAST") ? 1 : 0;
       // nu = 2 and nu = 3 give the same affine weight G(R) = (2R - 1 - p)/p (gmd_pair)
       ma.linear = 1;
       for (int v = 0; v < nnu; ++v)

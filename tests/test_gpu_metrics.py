@@ -306,7 +306,7 @@ def test_pairwise_nonfinite_input_device_check():
 
 
 @pytest.mark.parametrize("kind", ["image", "levels", "dense_overlap"])
-def test_merge_fast_path_vs_oracle(kind):
+def test_merge_fast_path_vs_oracle(kind, monkeypatch):
     # rank-by-counting fast path of the merge kernel (nnu <= 4): ranks from
     # counts on the pre-sorted rows; row-internal tie groups (clipped 1.0s,
     # quantised levels), duplicate rows, and |S_ab| above the fast cap (the
@@ -323,6 +323,7 @@ def test_merge_fast_path_vs_oracle(kind):
         X = (rng.random((120, 400)) * (rng.random((120, 400)) < 0.45)).astype(np.float32)
         nus = [1.2, 4.0]
     X[7] = X[8]
+    monkeypatch.setenv("GMDS_MERGE_FAST", "1")
     Ds = G.pairwise_gini(X, nus)
     Xd = X.astype(np.float64)
     for k, nu in enumerate(nus):
@@ -332,14 +333,14 @@ def test_merge_fast_path_vs_oracle(kind):
 
 
 def test_merge_fast_path_matches_merge_path(monkeypatch):
-    # the same matrix with the fast path disabled (GMDS_MERGE_NOFAST): equal to
-    # round-off (different summation order), both equal to the oracle
+    # the same matrix with and without the counting path (GMDS_MERGE_FAST): equal
+    # to round-off (different summation order), both equal to the oracle
     X = image_like(200, 784, 23)
-    a = G.pairwise_matrix(X, 2.0)
-    monkeypatch.setenv("GMDS_MERGE_NOFAST", "1")
-    b = G.pairwise_matrix(X, 2.0)
+    b = G.pairwise_matrix(X, 2.5)
+    monkeypatch.setenv("GMDS_MERGE_FAST", "1")
+    a = G.pairwise_matrix(X, 2.5)
     assert np.max(np.abs(a - b)) <= 1e-12 * np.max(b)
-    assert maxnorm_err(a, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
+    assert maxnorm_err(a, O.pairwise_matrix(X.astype(np.float64), 2.5)) <= 1e-12
 
 
 @pytest.mark.parametrize("kind", ["image", "levels", "overlap", "wide"])
@@ -367,3 +368,22 @@ def test_linear_weight_path_vs_oracle(kind, monkeypatch):
     monkeypatch.setenv("GMDS_NO_LINEAR", "1")
     Dg = G.pairwise_gini(X, [2.0])
     assert np.max(np.abs(D[0] - Dg[0])) <= 1e-12 * np.max(Dg[0])
+
+
+@pytest.mark.parametrize("nshards", [2, 3, 7])
+def test_linear_weight_kernel_sharded_matches_full(nshards):
+    # tile shards of the linear-weight kernel (multi-GPU split of the distance
+    # step): the union of the shards' writes is the full matrix, bit for bit
+    torch = pytest.importorskip("torch")
+    X = image_like(333, 300, 41)
+    dX = torch.from_numpy(X).cuda()
+    pe = G.packed_elems(333)
+    full = torch.zeros(pe, dtype=torch.float32, device="cuda")
+    G.pairwise_gini_device(dX.data_ptr(), G.F32, 333, 300, [2.0], G.F32, True, full.data_ptr())
+    sh = torch.zeros_like(full)
+    for s in range(nshards):
+        G.pairwise_gini_device(dX.data_ptr(), G.F32, 333, 300, [2.0], G.F32, True, sh.data_ptr(), s, nshards)
+    torch.cuda.synchronize()
+    assert torch.equal(full, sh)
+    D = G.pairwise_matrix(X, 2.0)
+    assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
