@@ -25,7 +25,10 @@
 #include "stress_pass.cuh"
 
 #ifndef GMDS_TMA_MINB
-#define GMDS_TMA_MINB(MODE) ((MODE) != 0 ? 2 : 3)
+// CTAs per SM: 3 for loss passes, 2 for gradient passes (128 registers).  At
+// Q >= 3 the gradient passes spill (448 B at Q = 3) yet stay faster than one
+// CTA per SM without spills (n = 20000: 24.2 vs 28.5 ms per 50 iterations)
+#define GMDS_TMA_MINB(MODE, Q) ((MODE) == 0 ? 3 : 2)
 #endif
 
 namespace gmds {
@@ -96,7 +99,7 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 // 2 (fused): loss of two trial points + gradient at the first (the predicted
 // Armijo acceptance, so the next iteration usually needs no gradient pass).
 template <int Q, int MODE, int KIND>
-__global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE)) stress_tma_kernel(PassArgs a) {
+__global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
   constexpr bool GRAD = (MODE != 0);  // gradient accumulation (of configuration 0)
   constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--p", type=int, default=784)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--q", type=int, default=2)
     a = ap.parse_args()
     import torch
 
@@ -39,10 +40,10 @@ def main():
             print(f"distance n={a.n} p={a.p}: {time.perf_counter() - t0:.4f} s", flush=True)
     if a.mode in ("stress", "both"):
         Dm = G.dmat_gini_device(dX.data_ptr(), G.F32, a.n, a.p, 2.0, G.F32)
-        Y0 = np.random.default_rng(1).normal(0, 0.1, (a.n, 2))
+        Y0 = np.random.default_rng(1).normal(0, 0.1, (a.n, a.q))
         for _ in range(a.reps):
             t0 = time.perf_counter()
-            r = G.minimize_stress(Dm, 2, "kruskal", max_iters=a.iters, rel_tol=1e-300, Y0=Y0)
+            r = G.minimize_stress(Dm, a.q, "kruskal", max_iters=a.iters, rel_tol=1e-300, Y0=Y0)
             print(f"stress n={a.n}: {a.iters} iters {time.perf_counter() - t0:.4f} s passes={r['passes']}", flush=True)
 
 
