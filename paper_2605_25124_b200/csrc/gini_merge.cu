@@ -6,9 +6,17 @@ namespace gmds {
 
 #define GMDS_MERGE_ONE(T, TO)                                                                                \
   do {                                                                                                       \
-    GMDS_CUDA(cudaFuncSetAttribute(gini_merge_kernel<T, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                   static_cast<int>(smem)));                                                 \
-    gini_merge_kernel<T, TO><<<blocks, merge_detail::kMergeThreads, smem, st>>>(ma, static_cast<const T*>(dX), static_cast<TO*>(dout)); \
+    if (ma.fast) {                                                                                           \
+      GMDS_CUDA(cudaFuncSetAttribute(gini_merge_kernel<T, TO, true>,                                         \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));  \
+      gini_merge_kernel<T, TO, true><<<blocks, merge_detail::kMergeThreads, smem, st>>>(                     \
+          ma, static_cast<const T*>(dX), static_cast<TO*>(dout));                                            \
+    } else {                                                                                                 \
+      GMDS_CUDA(cudaFuncSetAttribute(gini_merge_kernel<T, TO, false>,                                        \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));  \
+      gini_merge_kernel<T, TO, false><<<blocks, merge_detail::kMergeThreads, smem, st>>>(                    \
+          ma, static_cast<const T*>(dX), static_cast<TO*>(dout));                                            \
+    }                                                                                                        \
   } while (0)
 
 void launch_gini_merge(const MergeArgs& ma, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, size_t smem,

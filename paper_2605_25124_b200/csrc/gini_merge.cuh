@@ -26,11 +26,6 @@ struct MergeArgs {
   const uint16_t* sidx;  // per row, its nonzero features sorted by value (rowptr layout)
   const void* svs;       // per row, its nonzero values sorted ascending (rowptr layout)
   int fast;              // try the rank-by-counting path first (GMDS_MERGE_FAST=1 enables)
-  int linear;            // every nu is 2 or 3: the linear-weight path (gmd_pair)
-  const uint16_t* pmap;  // row store: sorted position of each nonzero (feature order)
-  const double* suf;     // row store: suffix sums of the sorted values
-  const double* s1;      // per row: sum of its values
-  const double* tm;      // per row: sum_k v_(k) k
   unsigned long long* fast_miss;  // optional: pairs the fast path handed to the merge path
 };
 
@@ -614,250 +609,12 @@ __device__ __forceinline__ bool fast_pair(const FastRows& R, double* scratch, in
   return true;
 }
 
-// ---------------------------------------------------------------------------
-// Linear-weight path: nu = 2 or nu = 3.
-//
-// For e = nu - 1 in {1, 2}, G(R) = ((R-1/2)/p)^e - (1-(R-1/2)/p)^e = (2R-1-p)/p
-// exactly, so (Appendix A of SURVEY.md) D = sum_k z_k R_k - (p+1)/2 sum_k z_k,
-// and for any multiset S with midranks r: sum_S z r = sum_S z + PM(S), PM =
-// the sum over unordered pairs of their maximum (ties included).  Splitting z
-// into negatives N = S_b u S_ab-, zeros and positives P = S_a u S_ab+:
-//   D = (1 - h) sum_N z + (1 + |N| + zeros - h) sum_P z + PM(N) + PM(P),  h = (p+1)/2
-// and every term is a per-row constant (s1, tm = PM of the row, suffix sums
-// of its sorted values) corrected by the s features nonzero in BOTH rows
-// (F = S_ab's features): their positions in each row's sorted list, their
-// position-order ranks among F (popc prefix of a bitmask) and prefix sums of
-// their values in that order, plus, per S_ab value, its lower bound in the
-// other row (binary search) and its rank within S_ab+- (one small sort).
-// Per pair the work is O(W + s log p), not O(nnz): no per-element pass.  Ties
-// need no special case (PM(S) is tie-exact).  Every quantity is fp64 from
-// exact fp32 inputs; the reference's pow-based weights agree to round-off.
-// Falls back (false) when s > 64 or a row has more than 256 nonzeros.
-constexpr int kGmdCap = 64;
-
-struct GmdRows {
-  const uint32_t* mi;
-  const uint32_t* mj;
-  const uint16_t* pi;
-  const uint16_t* pj;
-  const float* vi;
-  const float* vj;
-  const float* svi;
-  const float* svj;
-  int ci, cj;
-  int64_t bi, bj;  // row store offsets of rows i, j
-  double s1i, tmi, s1j, tmj;
-};
-
-// #{F positions < pos} from the position bitmask QM (8 words) and its word prefix QP
-__device__ __forceinline__ int gmd_qcount(const uint32_t* QM, const uint32_t* QP, int pos, int c, int s) {
-  if (pos >= c) return s;
-  const int w = pos >> 5;
-  return static_cast<int>(QP[w]) + __popc(QM[w] & ((1u << (pos & 31)) - 1u));
-}
-
-template <int KM>
-__device__ __forceinline__ double gmd_mids(const double* M, int mneg, int mpos, const GmdRows& R,
-                                           const double* __restrict__ suf, const uint32_t* QM, const double* PQi,
-                                           const double* PQj, int s, int lane) {
-  double key[KM];
-  const bool hiB = lane >= 16;
-  const int l16 = lane & 15;
-#pragma unroll
-  for (int r = 0; r < KM; ++r) {
-    const int e = r * 16 + l16;
-    double v = INFINITY;
-    if (!hiB) {
-      if (e < mneg) v = M[sk(e)];
-    } else {
-      if (e < mpos) v = M[sk(kMCap - 1 - e)];
-    }
-    key[r] = v;
-  }
-  split_detail::warp_bitonic_upto<KM>(key, lane, 16 * KM);
-  const int cnt = hiB ? mpos : mneg;
-  double acc = 0.0;
-#pragma unroll
-  for (int r = 0; r < KM; ++r) {
-    const int q = l16 * KM + r;
-    if (q >= cnt) continue;
-    const double b = key[r];
-    const double a = fabs(b);
-    const float f = __double2float_rz(a);
-    const uint32_t mag = fkey(f) + ((static_cast<double>(f) != a) ? 1u : 0u);
-    if (hiB) {  // b in S_ab+: PM(S_ab+) rank term and the pairs (b, S_a)
-      const int lb = row_bound<false>(R.svi, R.ci, mag);  // #{row-i values < b}
-      const int ql = gmd_qcount(QM, QM + 16, lb, R.ci, s);
-      const double sl = (lb < R.ci) ? __ldg(suf + R.bi + lb) : 0.0;
-      acc += b * static_cast<double>(q + lb - ql) + sl - PQi[s] + PQi[ql];
-    } else {  // b in S_ab-: pairs (b, S_b) are -min(|b|, x)
-      const int L = row_bound<false>(R.svj, R.cj, mag);  // #{row-j values < |b|}
-      const int ql = gmd_qcount(QM + 8, QM + 24, L, R.cj, s);
-      const double sl = (L < R.cj) ? __ldg(suf + R.bj + L) : 0.0;
-      acc += b * static_cast<double>(q) -
-             ((R.s1j - sl) - PQj[ql] + a * static_cast<double>((R.cj - L) - (s - ql)));
-    }
-  }
-  return acc;
-}
-
-__device__ __forceinline__ double warp_scan_incl(double v, int lane) {
-#pragma unroll
-  for (int dd = 1; dd < 32; dd <<= 1) {
-    const double o = __shfl_up_sync(kFull, v, dd);
-    if (lane >= dd) v += o;
-  }
-  return v;
-}
-
-// D of the pair on the linear-weight path; false (warp-uniform) = not handled.
-__device__ __forceinline__ bool gmd_pair(const GmdRows& R, const uint16_t* __restrict__ pmap,
-                                         const double* __restrict__ suf, double* scratch, int W, int d, int lane,
-                                         double& out) {
-  int* F = reinterpret_cast<int*>(scratch);                  // [64] features nonzero in both rows
-  uint32_t* QM = reinterpret_cast<uint32_t*>(scratch + 32);  // qm_i[8] qm_j[8] qp_i[8] qp_j[8]
-  double* PQi = scratch + 48;                                // [65] prefix sums, position order
-  double* PQj = scratch + 48 + 72;
-  double* M = scratch + kOffM;
-  const unsigned lt = (1u << lane) - 1u;
-  if (R.ci > 256 || R.cj > 256) return false;
-  if (lane < 16) QM[lane] = 0u;
-  // ---- F: AND of the presence masks, compacted in feature order
-  uint32_t m = (lane < W) ? (R.mi[lane] & R.mj[lane]) : 0u;
-  const int c = __popc(m);
-  int incl = c;
-#pragma unroll
-  for (int dd = 1; dd < 32; dd <<= 1) {
-    const int o = __shfl_up_sync(kFull, incl, dd);
-    if (lane >= dd) incl += o;
-  }
-  const int s = __shfl_sync(kFull, incl, 31);
-  if (s > kGmdCap) return false;
-  int off = incl - c;
-  while (m) {
-    const int b = __ffs(m) - 1;
-    m &= m - 1u;
-    F[off++] = (lane << 5) | b;
-  }
-  __syncwarp();
-  // ---- F's values and sorted positions in both rows
-  float al[2], be[2];
-  int pI[2], pJ[2];
-  bool live[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int e = lane + 32 * u;
-    live[u] = e < s;
-    al[u] = be[u] = 0.f;
-    pI[u] = pJ[u] = 0;
-    if (live[u]) {
-      const int f = F[e];
-      const int w = f >> 5;
-      const uint32_t lo = (1u << (f & 31)) - 1u;
-      const int ii = R.pi[w] + __popc(R.mi[w] & lo);
-      const int jj = R.pj[w] + __popc(R.mj[w] & lo);
-      al[u] = R.vi[ii];
-      be[u] = R.vj[jj];
-      pI[u] = __ldg(pmap + R.bi + ii);
-      pJ[u] = __ldg(pmap + R.bj + jj);
-      atomicOr(QM + (pI[u] >> 5), 1u << (pI[u] & 31));
-      atomicOr(QM + 8 + (pJ[u] >> 5), 1u << (pJ[u] & 31));
-    }
-  }
-  __syncwarp();
-  {  // word prefixes of the two position masks (groups of 8 lanes)
-    const uint32_t wv = (lane < 16) ? QM[lane] : 0u;
-    const int pc = __popc(wv);
-    int x = pc;
-#pragma unroll
-    for (int dd = 1; dd < 8; dd <<= 1) {
-      const int o = __shfl_up_sync(kFull, x, dd, 8);
-      if ((lane & 7) >= dd) x += o;
-    }
-    if (lane < 16) QM[16 + lane] = static_cast<uint32_t>(x - pc);
-  }
-  __syncwarp();
-  // ---- position-order ranks; values scattered in that order for prefix sums
-  int rI[2], rJ[2];
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    rI[u] = gmd_qcount(QM, QM + 16, pI[u], 256, s);
-    rJ[u] = gmd_qcount(QM + 8, QM + 24, pJ[u], 256, s);
-    if (live[u]) {
-      PQi[1 + rI[u]] = static_cast<double>(al[u]);
-      PQj[1 + rJ[u]] = static_cast<double>(be[u]);
-    }
-  }
-  __syncwarp();
-  {
-    const int t0 = 1 + 2 * lane, t1 = t0 + 1;
-    const double a0 = (t0 <= s) ? PQi[t0] : 0.0, a1 = (t1 <= s) ? PQi[t1] : 0.0;
-    const double b0 = (t0 <= s) ? PQj[t0] : 0.0, b1 = (t1 <= s) ? PQj[t1] : 0.0;
-    const double ia = warp_scan_incl(a0 + a1, lane) - (a0 + a1);
-    const double ib = warp_scan_incl(b0 + b1, lane) - (b0 + b1);
-    if (t0 <= s) {
-      PQi[t0] = ia + a0;
-      PQj[t0] = ib + b0;
-    }
-    if (t1 <= s) {
-      PQi[t1] = ia + a0 + a1;
-      PQj[t1] = ib + b0 + b1;
-    }
-    if (lane == 0) {
-      PQi[0] = 0.0;
-      PQj[0] = 0.0;
-    }
-  }
-  // ---- global counts
-  double z[2];
-  int mneg = 0, mpos = 0;
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    z[u] = live[u] ? static_cast<double>(al[u]) - static_cast<double>(be[u]) : 0.0;
-    const unsigned bn = __ballot_sync(kFull, z[u] < 0.0);
-    const unsigned bq = __ballot_sync(kFull, z[u] > 0.0);
-    if (z[u] < 0.0) M[sk(mneg + __popc(bn & lt))] = z[u];
-    if (z[u] > 0.0) M[sk(kMCap - 1 - (mpos + __popc(bq & lt)))] = z[u];
-    mneg += __popc(bn);
-    mpos += __popc(bq);
-  }
-  const int nP = R.ci - s + mpos, nN = R.cj - s + mneg;
-  const int zeros = d - nP - nN;
-  const double h = 0.5 * static_cast<double>(d + 1);
-  const double kp = static_cast<double>(1 + nN + zeros) - h, kn = 1.0 - h;
-  // ---- per-row constants and per-F terms
-  double acc = 0.0;
-  if (lane == 0)
-    acc = kp * R.s1i - kn * R.s1j + R.tmi - (static_cast<double>(R.cj - 1) * R.s1j - R.tmj);
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    if (!live[u]) continue;
-    const double a = al[u], b = be[u];
-    const double sufi1 = (pI[u] + 1 < R.ci) ? __ldg(suf + R.bi + pI[u] + 1) : 0.0;
-    const double sufj0 = __ldg(suf + R.bj + pJ[u]);
-    acc += -kp * a + kn * b;
-    acc += a * static_cast<double>(rI[u] - pI[u]) - sufi1;  // PM(S_a) correction
-    acc += (R.s1j - sufj0) + b * static_cast<double>((R.cj - 1 - pJ[u]) - (s - 1 - rJ[u]));  // PM(S_b) correction
-    acc += (z[u] > 0.0) ? kp * z[u] : ((z[u] < 0.0) ? kn * z[u] : 0.0);
-  }
-  __syncwarp();
-  if (mneg + mpos > 0) {
-    const int Hm = max(16, split_detail::npow2(max(mneg, mpos)));
-    switch (Hm / 16) {
-      case 1: acc += gmd_mids<1>(M, mneg, mpos, R, suf, QM, PQi, PQj, s, lane); break;
-      case 2: acc += gmd_mids<2>(M, mneg, mpos, R, suf, QM, PQi, PQj, s, lane); break;
-      default: acc += gmd_mids<4>(M, mneg, mpos, R, suf, QM, PQi, PQj, s, lane); break;
-    }
-  }
-  out = clamp_nonneg(warp_sum(acc));
-  return true;
-}
-
 }  // namespace merge_detail
 
 // 16 warps per CTA on a tile x tile block of pairs (sparse panels + sorted-order index).
-template <typename T, typename TO>
+template <typename T, typename TO, bool FAST>
 __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_kernel(MergeArgs ma, const T* __restrict__ X, TO* __restrict__ out) {
+  // FAST: the rank-by-counting path is compiled in (its registers would otherwise spill the merge path)
   using namespace merge_detail;
   using namespace split_detail;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -946,26 +703,8 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
       const size_t ostride = static_cast<size_t>(tile) * tstride;
 
       bool fastdone = false;
-      if constexpr (std::is_same<T, float>::value) {
-        if (ma.linear) {
-          // global rows of the two panel rows (invalid slots pair row i with itself)
-          const int64_t gi = i0 + ri, gj = (rj < tile) ? i0 + rj : j0 + (rj - tile);
-          const bool oki = gi < a.n, okj = gj < a.n;
-          const GmdRows R{mi, mj, pi, pj, vi, vj, svi, svj, ci, cj,
-                          oki ? __ldg(sa.rowptr + gi) : 0, okj ? __ldg(sa.rowptr + gj) : 0,
-                          oki ? __ldg(ma.s1 + gi) : 0.0, oki ? __ldg(ma.tm + gi) : 0.0,
-                          okj ? __ldg(ma.s1 + gj) : 0.0, okj ? __ldg(ma.tm + gj) : 0.0};
-          double dval = 0.0;
-          fastdone = gmd_pair(R, ma.pmap, ma.suf, scratch, W, d, lane, dval);
-          if (fastdone && valid && lane == 0)
-            for (int v = 0; v < a.nnu; ++v) {
-              ot[v * ostride] = dval;
-              if (isinf(dval)) atomicOr(a.flag, 1);
-            }
-          if (!fastdone && ma.fast_miss && valid && lane == 0) atomicAdd(ma.fast_miss, 1ull);
-          __syncwarp();
-        }
-        if (!fastdone && ma.fast && a.nnu <= kFastNu && ci <= 32 * kRowWords && cj <= 32 * kRowWords) {
+      if constexpr (FAST && std::is_same<T, float>::value) {
+        if (ma.fast && a.nnu <= kFastNu && ci <= 32 * kRowWords && cj <= 32 * kRowWords) {
           const FastRows R{mi, mj, pj, vj, si, svi, sj, svj, ci, cj};
           fastdone = (a.nnu == 1)
                          ? fast_pair<1>(R, scratch, d, lane, a.lut, 1, half_p, valid, ot, ostride, a.flag)

@@ -384,15 +384,6 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       // rank-by-counting first: exact, but measured slower than the merge path on the
       // metric data (0.83 vs 0.72 s), so opt-in (GMDS_MERGE_FAST=1)
       ma.fast = std::getenv("GMDS_MERGE_FAST") ? 1 : 0;
-      // nu = 2 and nu = 3 give the same affine weight G(R) = (2R - 1 - p)/p (gmd_pair)
-      ma.linear = 1;
-      for (int v = 0; v < nnu; ++v)
-        if (nus[v] != 2.0 && nus[v] != 3.0) ma.linear = 0;
-      if (std::getenv("GMDS_NO_LINEAR") || score) ma.linear = 0;
-      ma.pmap = rs.pmap.get();
-      ma.suf = rs.suf.get();
-      ma.s1 = rs.s1.get();
-      ma.tm = rs.tm.get();
       DevBuf<unsigned long long> miss;
       if (tr.on) {
         miss.alloc(1);
