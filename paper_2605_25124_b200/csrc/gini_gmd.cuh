@@ -24,7 +24,8 @@
 // Nothing is O(nnz) per pair.  All sums are fp64 from exact fp32 inputs; the
 // reference's pow-based weights agree to round-off (tests: <= 1e-12
 // max-normalised vs the compiled reference).  Pairs with s > 64 or a row with
-// more than 256 nonzeros go to the overflow list (exact full-sort kernel).
+// more nonzeros than the panel stride (<= 256, sized to shared memory) go to
+// the overflow list (exact full-sort kernel).
 #pragma once
 
 #include "gini_split.cuh"
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
   const GiniTileArgs& a = sa.g;
   const int d = a.d;
   const int W = sa.W;
-  const int stride = sa.maxnnz;
+  const int stride = sa.maxnnz;  // panel stride (<= kMaxC): rows with more nonzeros overflow
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   // ---- shared memory
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
         if (lane >= dd) incl += o;
       }
       const int s = __shfl_sync(0xffffffffu, incl, 31);
-      if (s > kCap || ci > kMaxC || cj > kMaxC) {  // overflow list: the exact full-sort kernel
+      if (s > kCap || ci > stride || cj > stride) {  // overflow list: the exact full-sort kernel
         if (lane == 0) {
           const unsigned long long slot = atomicAdd(sa.ovf_count, 1ull);
           if (static_cast<int64_t>(slot) < sa.ovf_cap) {

@@ -299,13 +299,22 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   for (int v = 0; v < nnu; ++v)
     if (nus[v] != 2.0 && nus[v] != 3.0) linear = false;
   // warps per CTA of the linear-weight kernel: the most that fit in shared memory
+  // and the panel stride (nonzeros per staged row): rows with more nonzeros than the
+  // stride go to the overflow list, so a few dense rows do not push every pair
+  // off this kernel
   int gmd_warps = 0;
+  int gmd_stride = std::min(std::max(1, rs.maxnnz), gmd_detail::kMaxC);
   for (int nw : {28, 24})  // 28: 72 registers, no spills (217 ms vs 221 at 24; 32 spills: 230 ms)
-    if (!gmd_warps && gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu, nw) <= 227 * 1024) gmd_warps = nw;
+    if (!gmd_warps && gmd_smem(rs.W, gmd_stride, nnu, nw) <= 227 * 1024) gmd_warps = nw;
+  if (!gmd_warps) {
+    gmd_warps = 24;
+    while (gmd_stride > 32 && gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > 227 * 1024) gmd_stride -= 8;
+    if (gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > 227 * 1024) gmd_warps = 0;
+  }
   if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd_warps = std::atoi(e);
   if (linear && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 && gmd_warps > 0) {
     // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh)
-    const size_t gsm = gmd_smem(rs.W, std::max(1, rs.maxnnz), nnu, gmd_warps);
+    const size_t gsm = gmd_smem(rs.W, gmd_stride, nnu, gmd_warps);
     a.tile = gmd_detail::kTile;
     a.nbt = ceil_div(n, a.tile);
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
@@ -319,7 +328,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     ga.s.rowptr = rs.rowptr.get();
     ga.s.vals = rs.vals.get();
     ga.s.W = rs.W;
-    ga.s.maxnnz = std::max(1, rs.maxnnz);
+    ga.s.maxnnz = gmd_stride;  // panel stride; longer rows overflow
     ga.s.sparse = 1;
     ga.pmap = rs.pmap.get();
     ga.svs = reinterpret_cast<const float*>(rs.svs.get());

@@ -387,3 +387,15 @@ def test_linear_weight_kernel_sharded_matches_full(nshards):
     assert torch.equal(full, sh)
     D = G.pairwise_matrix(X, 2.0)
     assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
+
+
+def test_linear_weight_kernel_dense_rows_overflow():
+    # a few dense rows (600 of 784 features) would make the panels too large for
+    # shared memory: the kernel caps its panel stride and sends those rows' pairs
+    # to the exact overflow list instead of leaving the linear-weight path
+    X = image_like(140, 784, 51)
+    rng = np.random.default_rng(52)
+    for r in (3, 77):
+        X[r] = (rng.random(784) * (rng.random(784) < 0.77)).astype(np.float32)
+    D = G.pairwise_matrix(X, 2.0)
+    assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
