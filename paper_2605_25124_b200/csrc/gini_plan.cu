@@ -201,15 +201,17 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       launch(ga);
       return;
     }
+    // Chunks of about equal work, each covering at most nbt/24 block rows: the
+    // rows left to copy after the last launch (the tail the caller waits for)
+    // stay a few percent of the matrix even though late block rows hold few tiles.
     const int64_t nbt = ga.nbt, b0 = ga.tile_begin, b1 = ga.tile_end;
     auto start = [nbt](int64_t r) { return r * nbt - (r * (r - 1)) / 2; };
+    const int64_t max_rows = std::max<int64_t>(1, nbt / 24);
     int64_t R = 0;
-    for (int c = 1; c <= sink->chunks; ++c) {
-      const int64_t target = b0 + (b1 - b0) * c / sink->chunks;
+    for (int c = 1; R < nbt; ++c) {
+      const int64_t target = b0 + (b1 - b0) * std::min(c, sink->chunks) / sink->chunks;
       int64_t R1 = R;
-      while (R1 < nbt && start(R1 + 1) <= target) ++R1;
-      if (c == sink->chunks) R1 = nbt;
-      if (R1 == R) continue;
+      while (R1 < nbt && R1 - R < max_rows && (R1 == R || start(R1 + 1) <= target)) ++R1;
       ga.tile_begin = start(R);
       ga.tile_end = start(R1);
       launch(ga);
