@@ -37,14 +37,16 @@ namespace gmds {
 
 namespace {
 
-// blocks per CTA of a tiled pass (one block row); GMDS_STRESS_CHUNK overrides (tuning)
-int64_t chunk_blocks() {
-  static const int64_t v = [] {
-    const char* e = std::getenv("GMDS_STRESS_CHUNK");
-    const int64_t c = e ? std::atoll(e) : 4;
-    return c > 0 ? c : 4;
-  }();
-  return v;
+// Blocks per CTA of a tiled pass (one block row): 4 at large n (measured best
+// at n = 20000), fewer when that would leave the pass short of ~8 CTAs per SM
+// (n = 5000: 820 blocks -> 1 per CTA); GMDS_STRESS_CHUNK overrides (tuning).
+int64_t chunk_blocks(int64_t nb) {
+  if (const char* e = std::getenv("GMDS_STRESS_CHUNK")) {
+    const int64_t c = std::atoll(e);
+    if (c > 0) return c;
+  }
+  const int64_t nblk = nb * (nb + 1) / 2;
+  return std::max<int64_t>(1, std::min<int64_t>(4, nblk / (148 * 8)));
 }
 constexpr double kTiny = 1e-300;  // embed.cpp:13
 
@@ -74,10 +76,11 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
   Q = padded_q(q);
   rows_mode = (q > 4);
   if (!rows_mode) {
+    chunk_len = chunk_blocks(nb);
     std::vector<int64_t> cI, cJ, sf;
     for (int64_t I = 0; I < nb; ++I) {
       sf.push_back(static_cast<int64_t>(cI.size()));
-      for (int64_t J0 = I; J0 < nb; J0 += chunk_blocks()) {
+      for (int64_t J0 = I; J0 < nb; J0 += chunk_len) {
         cI.push_back(I);
         cJ.push_back(J0);
       }
@@ -137,7 +140,7 @@ PassArgs Engine::args(int kind, double delta) const {
   a.huber_delta = delta;
   a.chunk_I = chunk_I.get();
   a.chunk_J0 = chunk_J0.get();
-  a.chunk_len = chunk_blocks();
+  a.chunk_len = chunk_len;
   a.nchunks = nchunks;
   a.rowpart = rowpart.get();
   a.colpart = colpart.get();
@@ -183,7 +186,7 @@ double Engine::grad_raw(int kind, double delta, const double* Yd) {
 // summed across ranks by an all-reduce.
 double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shard, int nshards) {
   if (rows_mode) fail(GMDS_INVALID_INPUT, "stress_partial: sharded passes support q <= 4");
-  // chunk c covers up to chunk_blocks() blocks... weight = number of blocks; split the prefix sum evenly
+  // chunk c covers up to chunk_len blocks... weight = number of blocks; split the prefix sum evenly
   std::vector<int64_t> cI(static_cast<size_t>(nchunks)), cJ(static_cast<size_t>(nchunks));
   GMDS_CUDA(cudaMemcpyAsync(cI.data(), chunk_I.get(), nchunks * 8, cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaMemcpyAsync(cJ.data(), chunk_J0.get(), nchunks * 8, cudaMemcpyDeviceToHost, st));
@@ -192,7 +195,7 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
   int64_t acc = 0, c0 = nchunks, c1 = nchunks;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t before = acc;
-    acc += std::min<int64_t>(chunk_blocks(), nb - cJ[c]);
+    acc += std::min<int64_t>(chunk_len, nb - cJ[c]);
     if (c0 == nchunks && before * nshards >= nblk * shard) c0 = c;
     if (c1 == nchunks && before * nshards >= nblk * (shard + 1)) c1 = c;
   }
