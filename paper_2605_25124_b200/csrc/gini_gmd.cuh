@@ -20,7 +20,10 @@
 //   * F's position-order ranks in each row (popc prefix of a position mask)
 //     and prefix sums of F's values in that order,
 //   * per S_ab value: its lower bound in the other row's sorted values
-//     (binary search) and its rank within S_ab+ or S_ab- (counting loop).
+//     (branch-free binary search), and
+//   * PM(S_ab+) + PM(S_ab-) = PM(Z) - (|S_ab-| + |Z0|) sum(S_ab+), with Z the
+//     s values of z on F and PM(Z) = (s-1)/2 sum z + 1/2 sum_{f<g} |z_f - z_g|
+//     (each lane sums its values against the next half of F, circularly).
 // Nothing is O(nnz) per pair.  All sums are fp64 from exact fp32 inputs; the
 // reference's pow-based weights agree to round-off (tests: <= 1e-12
 // max-normalised vs the compiled reference).  Pairs with s > 64 or a row with
