@@ -77,6 +77,10 @@ __device__ __forceinline__ int qcount(const uint32_t* QM, const uint32_t* QP, in
   return static_cast<int>(QP[w]) + __popc(QM[w] & ((1u << (pos & 31)) - 1u));
 }
 
+// per-warp histograms of u16 counters packed two per u32 word
+__device__ __forceinline__ void hist_add(uint32_t* H, int pos) { atomicAdd(H + (pos >> 1), 1u << ((pos & 1) << 4)); }
+__device__ __forceinline__ int hist_get(const uint32_t* H, int pos) { return (H[pos >> 1] >> ((pos & 1) << 4)) & 0xFFFF; }
+
 __device__ __forceinline__ double warp_incl(double v, int lane) {
 #pragma unroll
   for (int dd = 1; dd < 32; dd <<= 1) {
@@ -345,6 +349,305 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
   }
 }
 
+// ---------------------------------------------------------------------------
+// General-nu kernel on the same panels (nu not in {2, 3}, nnu <= 4): every
+// element's midrank is a count, and the weight comes from the LUT
+// (gini_tile.cuh: L[2 #less + #equal], p/2 sum z L).  With F, its sorted
+// positions and the position masks as in the linear kernel:
+//   x in S_a at row-i position k (tie group [g0, g1)):
+//     #less  = n_neg + zeros + (g0 - f_i(g0)) + #{b in S_ab+ : lb_b <= k}
+//     #equal = (g1 - g0) - (f_i(g1) - f_i(g0))
+//   -x in S_b at row-j position k:
+//     #less  = (cj - g1) - (s - f_j(g1)) + |S_ab-| - #{b in S_ab- : lb_b <= k}
+//   b in S_ab+- : #less from its rank in its sign group (counting loop over
+//     the group, fp64) and its lower bound lb_b in the other row,
+// where f_r(pos) = #{F positions < pos} (popc prefix of the position mask)
+// and the S_ab counts come from a per-warp histogram over row positions read
+// back with a warp scan per 32-element chunk.  One pass over each row's
+// nonzeros, no sort and no merge network.  Pairs whose S_ab values tie
+// anything (each other, or a value of the other row) go to the exact
+// overflow list, as do s > 64 and rows longer than the panel stride.
+template <typename TO, int kWarps, int NNU>
+__global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO* __restrict__ out) {
+  using namespace gmd_detail;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const SplitArgs& sa = ga.s;
+  const GiniTileArgs& a = sa.g;
+  const int d = a.d;
+  const int W = sa.W;
+  const int stride = sa.maxnnz;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  double* wscr = reinterpret_cast<double*>(smem_raw) + warp * kWarpWords;
+  int* F = reinterpret_cast<int*>(wscr);
+  uint32_t* QM = reinterpret_cast<uint32_t*>(wscr + kOffQM);  // qm_i[8] qm_j[8] qp_i[8] qp_j[8]
+  double* BL = wscr + kOffPQi;                                // [0, 64): S_ab- values, [64, 128): S_ab+
+  uint32_t* HI = reinterpret_cast<uint32_t*>(wscr + kOffPQi + 2 * kCap);  // 256 u16 counters
+  uint32_t* HJ = HI + 128;
+  double* otile = reinterpret_cast<double*>(smem_raw) + kWarps * kWarpWords;  // [nnu][32][33]
+  double* rs1 = otile + static_cast<size_t>(a.nnu) * kTile * (kTile + 1);
+  double* rtm = rs1 + kRows;
+  int64_t* rbase = reinterpret_cast<int64_t*>(rtm + kRows);
+  int* rcnt = reinterpret_cast<int*>(rbase + kRows);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(rcnt + kRows);  // [64][W]
+  uint16_t* spre = reinterpret_cast<uint16_t*>(smask + kRows * W);
+  float* svals = reinterpret_cast<float*>(spre + ((kRows * W + 1) & ~1));  // [64][stride]
+  float* ssv = svals + kRows * stride;                                       // [64][stride]
+  uint16_t* spm = reinterpret_cast<uint16_t*>(ssv + kRows * stride);         // [64][stride]
+  const float* gv = static_cast<const float*>(sa.vals);
+  const double half_p = 0.5 * static_cast<double>(d);
+  const int tstride = kTile + 1;
+  const int nnu = (NNU == 1) ? 1 : a.nnu;
+  const int lstride = 2 * d;
+  __shared__ double s_score[2 * kMaxScoreNu];
+  __shared__ double s_red[32 * 8];
+  for (int e = threadIdx.x; e < 2 * kMaxScoreNu; e += blockDim.x) s_score[e] = 0.0;
+  for (int e = lane; e < 256; e += 32) HI[e] = 0u;  // HI and HJ: left zero after every pair
+
+  for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
+    int64_t I, J;
+    decode_tile(t, a.nbt, I, J);
+    const int64_t i0 = I * kTile, j0 = J * kTile;
+    for (int e = threadIdx.x; e < kRows * W; e += blockDim.x) {
+      const int r = e / W, w = e - (e / W) * W;
+      const int64_t row = (r < kTile) ? i0 + r : j0 + (r - kTile);
+      smask[e] = (row < a.n) ? sa.masks[row * W + w] : 0u;
+      spre[e] = (row < a.n) ? sa.prefix[row * W + w] : uint16_t(0);
+    }
+    for (int r = warp; r < kRows; r += kWarps) {
+      const int64_t row = (r < kTile) ? i0 + r : j0 + (r - kTile);
+      int cnt = 0;
+      if (row < a.n) {
+        const int64_t b = sa.rowptr[row];
+        cnt = static_cast<int>(sa.rowptr[row + 1] - b);
+        for (int k = lane; k < cnt && k < stride; k += 32) {
+          svals[r * stride + k] = gv[b + k];
+          ssv[r * stride + k] = ga.svs[b + k];
+          spm[r * stride + k] = ga.pmap[b + k];
+        }
+      }
+      if (lane == 0) rcnt[r] = cnt;
+    }
+    __syncthreads();
+
+    for (int k0 = warp; k0 < kTile * kTile; k0 += kWarps) {
+      const int r = k0 >> 5, c = k0 & 31;
+      const int64_t gi = i0 + r, gj = j0 + c;
+      if (!(gj < a.n && gi < gj)) continue;
+      const int ri = r, rj = kTile + c;
+      const int ci = rcnt[ri], cj = rcnt[rj];
+      const uint32_t* mi = smask + ri * W;
+      const uint32_t* mj = smask + rj * W;
+      double* ot = otile + r * tstride + c;
+      auto overflow = [&]() {
+        if (lane == 0) {
+          const unsigned long long slot = atomicAdd(sa.ovf_count, 1ull);
+          if (static_cast<int64_t>(slot) < sa.ovf_cap) {
+            sa.ovf_pairs[2 * slot] = gi;
+            sa.ovf_pairs[2 * slot + 1] = gj;
+          }
+          for (int v = 0; v < nnu; ++v) ot[v * kTile * tstride] = -1.0;
+        }
+      };
+      // ---- F = features nonzero in both rows
+      if (lane < 16) QM[lane] = 0u;
+      uint32_t m = (lane < W) ? (mi[lane] & mj[lane]) : 0u;
+      const int cm = __popc(m);
+      int incl = cm;
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, dd);
+        if (lane >= dd) incl += o;
+      }
+      const int s = __shfl_sync(0xffffffffu, incl, 31);
+      if (s > kCap || ci > stride || cj > stride) {
+        overflow();
+        continue;
+      }
+      {
+        int off = incl - cm;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1u;
+          F[off++] = (lane << 5) | b;
+        }
+      }
+      __syncwarp();
+      const uint16_t* pim = spre + ri * W;
+      const uint16_t* pjm = spre + rj * W;
+      const float* vi = svals + ri * stride;
+      const float* vj = svals + rj * stride;
+      const float* svi = ssv + ri * stride;
+      const float* svj = ssv + rj * stride;
+      // ---- F's values and sorted positions in both rows; position masks
+      double z[2];
+      int lbp[2];  // histogram position of this lane's S_ab values (-1: none)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = lane + 32 * u;
+        z[u] = 0.0;
+        lbp[u] = -1;
+        if (e < s) {
+          const int f = F[e];
+          const int w = f >> 5;
+          const uint32_t lo = (1u << (f & 31)) - 1u;
+          const int ii = pim[w] + __popc(mi[w] & lo);
+          const int jj = pjm[w] + __popc(mj[w] & lo);
+          z[u] = static_cast<double>(vi[ii]) - static_cast<double>(vj[jj]);
+          const int pI = spm[ri * stride + ii], pJ = spm[rj * stride + jj];
+          atomicOr(QM + (pI >> 5), 1u << (pI & 31));
+          atomicOr(QM + 8 + (pJ >> 5), 1u << (pJ & 31));
+        }
+      }
+      int mneg = 0, mpos = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const unsigned bn = __ballot_sync(0xffffffffu, z[u] < 0.0);
+        const unsigned bq = __ballot_sync(0xffffffffu, z[u] > 0.0);
+        if (z[u] < 0.0) BL[mneg + __popc(bn & lt)] = z[u];
+        if (z[u] > 0.0) BL[kCap + mpos + __popc(bq & lt)] = z[u];
+        mneg += __popc(bn);
+        mpos += __popc(bq);
+      }
+      __syncwarp();
+      {  // word prefixes of the two masks (groups of 8 lanes)
+        const uint32_t wv = (lane < 16) ? QM[lane] : 0u;
+        const int pc = __popc(wv);
+        int x = pc;
+#pragma unroll
+        for (int dd = 1; dd < 8; dd <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, x, dd, 8);
+          if ((lane & 7) >= dd) x += o;
+        }
+        if (lane < 16) QM[16 + lane] = static_cast<uint32_t>(x - pc);
+      }
+      __syncwarp();
+      const int n_neg = (cj - s) + mneg, n_pos = (ci - s) + mpos;
+      const int zeros = d - n_neg - n_pos;
+      // ---- S_ab values: rank in their sign group, lower bound in the other row
+      bool bad = false;
+      int bidx[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        bidx[u] = -1;
+        const double zz = z[u];
+        if (zz == 0.0) continue;
+        const bool pos = zz > 0.0;
+        const double* L = BL + (pos ? kCap : 0);
+        const int len = pos ? mpos : mneg;
+        int cl = 0, ce = 0;
+        for (int q = 0; q < len; ++q) {
+          const double o = L[q];
+          cl += (o < zz) ? 1 : 0;
+          ce += (o == zz) ? 1 : 0;
+        }
+        if (ce != 1) bad = true;  // two equal S_ab values
+        const double mg = fabs(zz);
+        const float f = __double2float_rz(mg);
+        const uint32_t code = fkey(f) + ((static_cast<double>(f) != mg) ? 1u : 0u);
+        const int n = pos ? ci : cj;
+        const float* sv = pos ? svi : svj;
+        const int lb = lower_count(sv, n, code);
+        if (lb < n && fkey(sv[lb]) == code) bad = true;  // equal to a value of the other row
+        const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
+        const int less = pos ? n_neg + zeros + cl + (lb - ql) : cl + (cj - lb) - (s - ql);
+        bidx[u] = 2 * less + 1;
+        lbp[u] = (lb < n) ? (pos ? lb : 256 + lb) : -1;
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+        overflow();
+        continue;
+      }
+      double acc[NNU];
+#pragma unroll
+      for (int v = 0; v < NNU; ++v) acc[v] = 0.0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (lbp[u] >= 0) hist_add(HI, lbp[u]);  // HJ == HI + 128: position 256 + lb
+        if (bidx[u] >= 0) {
+#pragma unroll
+          for (int v = 0; v < NNU; ++v)
+            if (NNU == 1 || v < nnu) acc[v] = fma(z[u], __ldg(a.lut + v * lstride + bidx[u]), acc[v]);
+        }
+      }
+      __syncwarp();
+      // ---- one pass over each row's nonzeros (S_a of row i, S_b of row j)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const bool RI = side == 0;
+        const int cnt = RI ? ci : cj;
+        const float* sv = RI ? svi : svj;
+        const uint32_t* qm = QM + (RI ? 0 : 8);
+        const uint32_t* qp = QM + (RI ? 16 : 24);
+        const uint32_t* H = RI ? HI : HJ;
+        int carry = 0;
+        float lastx = -1.f;
+        for (int base = 0; base < cnt; base += 32) {
+          const int k = base + lane;
+          const bool in = k < cnt;
+          const uint32_t qw = qm[base >> 5];
+          const int rem = (qw >> lane) & 1u;
+          const bool live = in && !rem;
+          const float x = in ? sv[k] : -2.f;
+          int hs = in ? hist_get(H, k) : 0;
+#pragma unroll
+          for (int dd = 1; dd < 32; dd <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, hs, dd);
+            if (lane >= dd) hs += o;
+          }
+          hs += carry;
+          carry = __shfl_sync(0xffffffffu, hs, 31);
+          float xp = __shfl_up_sync(0xffffffffu, x, 1);
+          float xn = __shfl_down_sync(0xffffffffu, x, 1);
+          if (lane == 0) xp = lastx;
+          if (lane == 31) xn = (k + 1 < cnt) ? sv[k + 1] : -3.f;
+          lastx = __shfl_sync(0xffffffffu, x, 31);
+          int g0 = k, g1 = k + 1;
+          int rb0 = static_cast<int>(qp[base >> 5]) + __popc(qw & lt);
+          int rb1 = rb0 + rem;
+          if (live && (xp == x || xn == x)) {  // tie group in the row (clipped values, repeats)
+            while (g0 > 0 && sv[g0 - 1] == x) --g0;
+            while (g1 < cnt && sv[g1] == x) ++g1;
+            rb0 = qcount(qm, qp, g0, s);
+            rb1 = qcount(qm, qp, g1, s);
+          }
+          if (live) {
+            const int eq = (g1 - g0) - (rb1 - rb0);
+            const int less = RI ? n_neg + zeros + (g0 - rb0) + hs : (cnt - g1) - (s - rb1) + (mneg - hs);
+            const int idx = 2 * less + eq;
+            const double zv = RI ? static_cast<double>(x) : -static_cast<double>(x);
+#pragma unroll
+            for (int v = 0; v < NNU; ++v)
+              if (NNU == 1 || v < nnu) acc[v] = fma(zv, __ldg(a.lut + v * lstride + idx), acc[v]);
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (lbp[u] >= 0) HI[lbp[u] >> 1] = 0u;  // leave the histograms zero
+#pragma unroll
+      for (int v = 0; v < NNU; ++v) {
+        if (NNU > 1 && v >= nnu) break;
+        double sum = acc[v];
+#pragma unroll
+        for (int dd = 16; dd > 0; dd >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, dd);
+        if (lane == 0) {
+          const double val = clamp_nonneg(half_p * sum);
+          ot[v * kTile * tstride] = val;
+          if (isinf(val)) atomicOr(a.flag, 1);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    tile_epilogue<TO>(a, otile, kTile, tstride, i0, j0, out, s_score, s_red);
+    __syncthreads();
+  }
+  score_flush(a, s_score);
+}
+
 inline size_t gmd_smem(int W, int maxnnz, int nnu, int nwarps) {
   using namespace gmd_detail;
   return static_cast<size_t>(nwarps) * kWarpWords * 8 + static_cast<size_t>(nnu) * kTile * (kTile + 1) * 8 +
@@ -353,6 +656,8 @@ inline size_t gmd_smem(int W, int maxnnz, int nnu, int nwarps) {
 }
 
 void launch_gini_gmd(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
+                     cudaStream_t st);
+void launch_gini_gen(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
                      cudaStream_t st);
 
 }  // namespace gmds

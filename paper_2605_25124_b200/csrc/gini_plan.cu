@@ -314,8 +314,11 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     if (gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > 227 * 1024) gmd_warps = 0;
   }
   if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd_warps = std::atoi(e);
-  if (linear && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 && gmd_warps > 0) {
-    // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh)
+  // other nu (at most 4 per launch, store mode): the general counting kernel on the same panels
+  const bool general = !linear && score == nullptr && nnu <= 4 && !std::getenv("GMDS_NO_GEN");
+  if ((linear || general) && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 && gmd_warps > 0) {
+    // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh);
+    // other nu: midranks counted from the same structures, one LUT pass (gini_gen_kernel)
     const size_t gsm = gmd_smem(rs.W, gmd_stride, nnu, gmd_warps);
     a.tile = gmd_detail::kTile;
     a.nbt = ceil_div(n, a.tile);
@@ -347,12 +350,15 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     chunked(a, [&](GiniTileArgs& g) {
       ga.s.g = g;
       const unsigned blk = static_cast<unsigned>(std::min<int64_t>(g.tile_end - g.tile_begin, int64_t(1) << 30));
-      launch_gini_gmd(ga, dD, ot, gsm, blk, gmd_warps, st);
+      if (linear)
+        launch_gini_gmd(ga, dD, ot, gsm, blk, gmd_warps, st);
+      else
+        launch_gini_gen(ga, dD, ot, gsm, blk, gmd_warps, st);
       count_launch();
-      check_launch("gini_gmd_kernel");
+      check_launch(linear ? "gini_gmd_kernel" : "gini_gen_kernel");
     });
     ga.s.g = a;
-    tr.mark("gini_gmd_kernel", st);
+    tr.mark(linear ? "gini_gmd_kernel" : "gini_gen_kernel", st);
     unsigned long long novf = 0;
     GMDS_CUDA(cudaMemcpyAsync(&novf, ovf_count.get(), sizeof novf, cudaMemcpyDeviceToHost, st));
     GMDS_CUDA(cudaStreamSynchronize(st));

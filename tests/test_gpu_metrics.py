@@ -399,3 +399,36 @@ def test_linear_weight_kernel_dense_rows_overflow():
         X[r] = (rng.random(784) * (rng.random(784) < 0.77)).astype(np.float32)
     D = G.pairwise_matrix(X, 2.0)
     assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", ["image", "levels", "mixed", "wide"])
+def test_general_counting_kernel_vs_oracle(kind, monkeypatch):
+    # other nu (<= 4 per launch) on sparse non-negative fp32 data: midranks counted
+    # from the shared-feature structures (gini_gen_kernel), ties in rows handled,
+    # ties between S_ab values and row values sent to the exact overflow kernel;
+    # checked against the oracle and against the merge kernel (GMDS_NO_GEN)
+    rng = np.random.default_rng({"image": 61, "levels": 62, "mixed": 63, "wide": 64}[kind])
+    if kind == "image":
+        X = image_like(170, 784, 65)
+        nus = [2.5]
+    elif kind == "levels":  # quantised values: many S_ab values equal row values (overflow path)
+        X = rng.choice(np.float32([0.25, 0.5, 0.75, 1.0]), size=(150, 200)).astype(np.float32)
+        X[rng.random(X.shape) < 0.7] = 0.0
+        nus = [1.3, 4.0]
+    elif kind == "mixed":
+        X = image_like(160, 300, 66)
+        X[::7] = np.round(X[::7] * 4) / 4  # some quantised rows
+        nus = [1.1, 1.7, 5.0, 8.0]
+    else:
+        X = image_like(100, 1000, 67)
+        X[:2] = rng.random((2, 1000)).astype(np.float32) * (rng.random((2, 1000)) < 0.4)
+        nus = [6.0]
+    X[5] = X[9]
+    Xd = X.astype(np.float64)
+    D = G.pairwise_gini(X, nus)
+    for k, nu in enumerate(nus):
+        assert maxnorm_err(D[k], O.pairwise_matrix(Xd, nu)) <= 1e-12
+    assert D[0][5, 9] == 0.0
+    monkeypatch.setenv("GMDS_NO_GEN", "1")
+    Dm = G.pairwise_gini(X, nus)
+    assert np.max(np.abs(D - Dm)) <= 1e-12 * np.max(np.abs(Dm))
