@@ -42,6 +42,7 @@ struct GmdArgs {
   const double* suf;     // suffix sums of the sorted values per row
   const double* s1;      // per row: sum of values
   const double* tm;      // per row: sum_k v_(k) k
+  const uint32_t* tiew;  // per row, 8 words: bit g = (v_(g) == v_(g+1)) (general kernel's tie groups)
 };
 
 namespace gmd_detail {
@@ -395,6 +396,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
   float* svals = reinterpret_cast<float*>(spre + ((kRows * W + 1) & ~1));  // [64][stride]
   float* ssv = svals + kRows * stride;                                       // [64][stride]
   uint16_t* spm = reinterpret_cast<uint16_t*>(ssv + kRows * stride);         // [64][stride]
+  uint32_t* stie = reinterpret_cast<uint32_t*>(spm + ((kRows * stride + 1) & ~1));  // [64][8]
   const float* gv = static_cast<const float*>(sa.vals);
   const double half_p = 0.5 * static_cast<double>(d);
   const int tstride = kTile + 1;
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
         }
       }
       if (lane == 0) rcnt[r] = cnt;
+      if (lane < 8) stie[r * 8 + lane] = (row < a.n) ? ga.tiew[row * 8 + lane] : 0u;
     }
     __syncthreads();
 
@@ -582,7 +585,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
         const uint32_t* qp = QM + (RI ? 16 : 24);
         const uint32_t* H = RI ? HI : HJ;
         int carry = 0;
-        float lastx = -1.f;
         for (int base = 0; base < cnt; base += 32) {
           const int k = base + lane;
           const bool in = k < cnt;
@@ -598,17 +600,35 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
           }
           hs += carry;
           carry = __shfl_sync(0xffffffffu, hs, 31);
-          float xp = __shfl_up_sync(0xffffffffu, x, 1);
-          float xn = __shfl_down_sync(0xffffffffu, x, 1);
-          if (lane == 0) xp = lastx;
-          if (lane == 31) xn = (k + 1 < cnt) ? sv[k + 1] : -3.f;
-          lastx = __shfl_sync(0xffffffffu, x, 31);
           int g0 = k, g1 = k + 1;
           int rb0 = static_cast<int>(qp[base >> 5]) + __popc(qw & lt);
           int rb1 = rb0 + rem;
-          if (live && (xp == x || xn == x)) {  // tie group in the row (clipped values, repeats)
-            while (g0 > 0 && sv[g0 - 1] == x) --g0;
-            while (g1 < cnt && sv[g1] == x) ++g1;
+          // tie groups in the row (clipped values, repeats) from the row's tie bits:
+          // group bounds by bit scans; only a group crossing a 32-entry chunk walks the row
+          const int prow = RI ? ri : rj;
+          const uint32_t tw = stie[prow * 8 + (base >> 5)];
+          const uint32_t pbit = (base > 0) ? (stie[prow * 8 + (base >> 5) - 1] >> 31) : 0u;
+          const bool tied = live && ((lane > 0 ? (tw >> (lane - 1)) & 1u : pbit) || ((tw >> lane) & 1u));
+          if (tied) {
+            const uint32_t below = ~tw & lt;                    // positions t < lane with v_t != v_(t+1)
+            const uint32_t above = ~tw & (0xffffffffu << lane);  // positions t >= lane with v_t != v_(t+1)
+            bool cross = false;
+            if (below) {
+              g0 = base + 32 - __clz(below);
+            } else {
+              g0 = base;
+              cross = pbit != 0;
+            }
+            if (above) {
+              g1 = base + __ffs(above);
+            } else {
+              g1 = base + 32;
+              cross = true;
+            }
+            if (cross) {
+              while (g0 > 0 && sv[g0 - 1] == x) --g0;
+              while (g1 < cnt && sv[g1] == x) ++g1;
+            }
             rb0 = qcount(qm, qp, g0, s);
             rb1 = qcount(qm, qp, g1, s);
           }
@@ -652,7 +672,7 @@ inline size_t gmd_smem(int W, int maxnnz, int nnu, int nwarps) {
   using namespace gmd_detail;
   return static_cast<size_t>(nwarps) * kWarpWords * 8 + static_cast<size_t>(nnu) * kTile * (kTile + 1) * 8 +
          kRows * (8 + 8 + 8 + 4) + kRows * W * 4 + ((kRows * W + 1) & ~1) * 2 +
-         static_cast<size_t>(kRows) * maxnnz * (4 + 4 + 2) + 16;
+         static_cast<size_t>(kRows) * maxnnz * (4 + 4 + 2) + 4 + kRows * 8 * 4 + 16;  // + tie words
 }
 
 void launch_gini_gmd(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,

@@ -37,7 +37,8 @@ template <int K, typename T>
 __global__ void row_sort_kernel(const T* __restrict__ vals, const uint16_t* __restrict__ fidx,
                                 const int64_t* __restrict__ rowptr, const int* __restrict__ rows, int nrows,
                                 uint16_t* __restrict__ sidx, T* __restrict__ svs, uint16_t* __restrict__ pmap,
-                                double* __restrict__ suf, double* __restrict__ s1, double* __restrict__ tm) {
+                                double* __restrict__ suf, double* __restrict__ s1, double* __restrict__ tm,
+                                uint32_t* __restrict__ tiew) {
   const int lane = threadIdx.x & 31;
   for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nrows; q += (gridDim.x * blockDim.x) >> 5) {
     const int64_t row = rows[q];
@@ -90,21 +91,36 @@ __global__ void row_sort_kernel(const T* __restrict__ vals, const uint16_t* __re
         s1[row] = incl;  // lane 0: the whole row
         tm[row] = tsum;
       }
+      if constexpr (K <= 8) {  // tie words (rows of <= 256 nonzeros): bit g = (v_(g) == v_(g+1))
+        const double nxt0 = __shfl_down_sync(0xffffffffu, key[0], 1);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int g = lane * K + r;
+          const double nx = (r + 1 < K) ? key[r + 1 < K ? r + 1 : 0] : nxt0;
+          if (g + 1 < cnt && key[r] == nx) mine |= 1u << r;
+        }
+        uint32_t word = mine << ((lane * K) & 31);  // 32 / K lanes per word
+#pragma unroll
+        for (int dd = 1; dd < 32 / K; dd <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, dd);
+        const int w = (lane * K) >> 5;
+        if (((lane * K) & 31) == 0 && w < 8) tiew[row * 8 + w] = word;
+      }
     }
   }
 }
 
 void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, const int64_t* rowptr, const int* rows,
                      int nrows, int K, uint16_t* sidx, void* svs, uint16_t* pmap, double* suf, double* s1,
-                     double* tm, cudaStream_t st) {
+                     double* tm, uint32_t* tiew, cudaStream_t st) {
   if (nrows <= 0) return;
   const unsigned blocks = static_cast<unsigned>(std::max(1, std::min((nrows + 7) / 8, 148 * 8)));
 #define GMDS_RS(KK)                                                                                                \
   case KK:                                                                                                         \
     if (xt == GMDS_F32)                                                                                            \
-      row_sort_kernel<KK, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(vals), fidx, rowptr, rows, nrows, sidx, static_cast<float*>(svs), pmap, suf, s1, tm); \
+      row_sort_kernel<KK, float><<<blocks, 256, 0, st>>>(static_cast<const float*>(vals), fidx, rowptr, rows, nrows, sidx, static_cast<float*>(svs), pmap, suf, s1, tm, tiew); \
     else                                                                                                           \
-      row_sort_kernel<KK, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(vals), fidx, rowptr, rows, nrows, sidx, static_cast<double*>(svs), pmap, suf, s1, tm); \
+      row_sort_kernel<KK, double><<<blocks, 256, 0, st>>>(static_cast<const double*>(vals), fidx, rowptr, rows, nrows, sidx, static_cast<double*>(svs), pmap, suf, s1, tm, tiew); \
     break;
   switch (K) {
     GMDS_RS(1) GMDS_RS(2) GMDS_RS(4) GMDS_RS(8) GMDS_RS(16) GMDS_RS(32)

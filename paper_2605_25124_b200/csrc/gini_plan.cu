@@ -24,7 +24,7 @@ void launch_gini_list(GiniTileArgs a, const void* dX, gmds_dtype xt, const int64
 
 void launch_row_sort(const void* vals, gmds_dtype xt, const uint16_t* fidx, const int64_t* rowptr, const int* rows,
                      int nrows, int K, uint16_t* sidx, void* svs, uint16_t* pmap, double* suf, double* s1,
-                     double* tm, cudaStream_t st);
+                     double* tm, uint32_t* tiew, cudaStream_t st);
 
 namespace {
 
@@ -91,6 +91,7 @@ struct RowStore {
   DevBuf<uint16_t> pmap;      // sorted position of each nonzero (feature order; linear-weight path)
   DevBuf<double> suf;         // suffix sums of the sorted values (linear-weight path)
   DevBuf<double> s1, tm;      // per row: sum of values, sum_k v_(k) k
+  DevBuf<uint32_t> tiew;      // per row, 8 words: bit g = (v_(g) == v_(g+1)) (rows of <= 256 nonzeros)
   bool nonneg = false;
   DevBuf<uint32_t> masks;
   DevBuf<uint16_t> prefix;
@@ -152,6 +153,8 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
     rs.suf.alloc(static_cast<size_t>(std::max<int64_t>(1, rp[n])));
     rs.s1.alloc(static_cast<size_t>(n));
     rs.tm.alloc(static_cast<size_t>(n));
+    rs.tiew.alloc(static_cast<size_t>(n) * 8);
+    GMDS_CUDA(cudaMemsetAsync(rs.tiew.get(), 0, static_cast<size_t>(n) * 8 * sizeof(uint32_t), st));
     std::vector<std::vector<int>> buckets(6);
     for (int64_t i = 0; i < n; ++i) {
       int K = 1;
@@ -167,7 +170,7 @@ RowStore build_rows(const void* dX, gmds_dtype xt, int64_t n, int p, cudaStream_
                                 cudaMemcpyHostToDevice, st));
       launch_row_sort(rs.vals.get(), xt, rs.fidx.get(), rs.rowptr.get(), rows.get(),
                       static_cast<int>(buckets[bk].size()), 1 << bk, rs.sidx.get(), rs.svs.get(), rs.pmap.get(),
-                      rs.suf.get(), rs.s1.get(), rs.tm.get(), st);
+                      rs.suf.get(), rs.s1.get(), rs.tm.get(), rs.tiew.get(), st);
       GMDS_CUDA(cudaStreamSynchronize(st));
     }
   }
@@ -306,12 +309,13 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   // off this kernel
   int gmd_warps = 0;
   int gmd_stride = std::min(std::max(1, rs.maxnnz), gmd_detail::kMaxC);
+  const size_t gmd_budget = 227 * 1024 - 4096;  // dynamic shared memory; the general kernel has 3 KB static
   for (int nw : {28, 24})  // 28: 72 registers, no spills (217 ms vs 221 at 24; 32 spills: 230 ms)
-    if (!gmd_warps && gmd_smem(rs.W, gmd_stride, nnu, nw) <= 227 * 1024) gmd_warps = nw;
+    if (!gmd_warps && gmd_smem(rs.W, gmd_stride, nnu, nw) <= gmd_budget) gmd_warps = nw;
   if (!gmd_warps) {
     gmd_warps = 24;
-    while (gmd_stride > 32 && gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > 227 * 1024) gmd_stride -= 8;
-    if (gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > 227 * 1024) gmd_warps = 0;
+    while (gmd_stride > 32 && gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > gmd_budget) gmd_stride -= 8;
+    if (gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > gmd_budget) gmd_warps = 0;
   }
   if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd_warps = std::atoi(e);
   // other nu (at most 4 per launch, store mode): the general counting kernel on the same panels
@@ -340,6 +344,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     ga.suf = rs.suf.get();
     ga.s1 = rs.s1.get();
     ga.tm = rs.tm.get();
+    ga.tiew = rs.tiew.get();
     const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(a.tile) * a.tile;
     ga.s.ovf_cap = std::min<int64_t>(shard_pairs, int64_t(1) << 20);
     DevBuf<int64_t> ovf(static_cast<size_t>(2 * ga.s.ovf_cap));
