@@ -592,14 +592,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
           const int rem = (qw >> lane) & 1u;
           const bool live = in && !rem;
           const float x = in ? sv[k] : -2.f;
-          int hs = in ? hist_get(H, k) : 0;
+          // S_ab values counted at positions <= k: a popc of the chunk's occupied
+          // positions, or a warp scan when a position holds more than one
+          const int hc = in ? hist_get(H, k) : 0;
+          const unsigned occ = __ballot_sync(0xffffffffu, hc > 0);
+          int hs;
+          if (__any_sync(0xffffffffu, hc > 1)) {
+            hs = hc;
 #pragma unroll
-          for (int dd = 1; dd < 32; dd <<= 1) {
-            const int o = __shfl_up_sync(0xffffffffu, hs, dd);
-            if (lane >= dd) hs += o;
+            for (int dd = 1; dd < 32; dd <<= 1) {
+              const int o = __shfl_up_sync(0xffffffffu, hs, dd);
+              if (lane >= dd) hs += o;
+            }
+            hs += carry;
+            carry = __shfl_sync(0xffffffffu, hs, 31);
+          } else {
+            hs = carry + __popc(occ & (lt | (1u << lane)));
+            carry += __popc(occ);
           }
-          hs += carry;
-          carry = __shfl_sync(0xffffffffu, hs, 31);
           int g0 = k, g1 = k + 1;
           int rb0 = static_cast<int>(qp[base >> 5]) + __popc(qw & lt);
           int rb1 = rb0 + rem;
