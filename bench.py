@@ -39,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N, P, Q, NU = 20000, 784, 2, 2.0
+NU_GENERAL = 2.5  # a weight outside the linear case (nu in {2, 3}), reported beside the headline
 STRESS_ITERS = 50
 SEED = 2605
 
@@ -280,6 +281,24 @@ def run_engine(args, rank, world, dist):
     print(f"[bench] distance step times (ms): {[round(t * 1e3, 2) for t in times]}", file=sys.stderr, flush=True)
     t_dist = max_over_ranks(dist, float(np.mean(times)))
 
+    # ---- the same step at a nu outside {2, 3} (general-weight kernel), reported beside `value`
+    def general_step():
+        G.pairwise_gini_device(dX.data_ptr(), G.F32, N, P, [NU_GENERAL], G.F32, True, dD.data_ptr(), rank, world,
+                               stream.cuda_stream)
+
+    general_step()
+    gtimes = []
+    for _ in range(2):
+        flush.zero_()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        general_step()
+        e1.record(stream)
+        e1.synchronize()
+        gtimes.append(e0.elapsed_time(e1) / 1e3)
+    t_general = max_over_ranks(dist, float(np.mean(gtimes)))
+
     # ---- stress: S Kruskal iterations on the packed matrix of this step.  One GPU: the
     # device-controlled fit.  Several ranks: the tile-sharded fit, one NCCL all-reduce of
     # [loss | gradient] per pass (paper_2605_25124_b200/distributed.py).
@@ -368,6 +387,8 @@ def run_engine(args, rank, world, dist):
                    "distance step; the packed D (800 MB) exceeds L2 for the stress passes",
                    "parallelism": f"pair tiles sharded over {world} GPU(s)"},
         "distance_ms": t_dist * 1e3,
+        "distance_general_nu": {"nu": NU_GENERAL, "ms": t_general * 1e3, "pairs_per_s": npairs / t_general,
+                                "kernel": "gini_gen_kernel (midranks counted, one LUT pass)"},
         "stress_iters_per_sec": iters_per_sec,
         "stress_ms_per_iter": 1e3 / iters_per_sec,
         "stress_passes_per_iter": spasses / max(1, siters),
