@@ -227,6 +227,10 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       float2 lhalf[NCM];  // loss of this half, two fp32 lanes per candidate (widened once per half)
 #pragma unroll
       for (int c = 0; c < NCM; ++c) lhalf[c] = make_float2(0.f, 0.f);
+      // the row loop, instantiated per block kind (edge / packed / generic) so the
+      // interior-block version is a branch-free, fully unrolled loop over the rows
+      auto row_loop = [&](auto mode_tag) {
+      constexpr int MODE_ROWS = decltype(mode_tag)::value;  // 0 packed, 1 edge, 2 generic
 #pragma unroll
       for (int x = 0; x < kMR; ++x) {
         const int rloc = ti * kMR + x;           // row within the half
@@ -345,13 +349,20 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             }
           }
         };
-        if (edge)
+        if constexpr (MODE_ROWS == 1)
           pairs(std::true_type{});
-        else if ((KIND == kKruskal || KIND == kGuttman) && !Wb)
+        else if constexpr (MODE_ROWS == 0)
           pairs_packed();
         else
           pairs(std::false_type{});
       }
+      };
+      if (edge)
+        row_loop(std::integral_constant<int, 1>{});
+      else if ((KIND == kKruskal || KIND == kGuttman) && !Wb)
+        row_loop(std::integral_constant<int, 0>{});
+      else
+        row_loop(std::integral_constant<int, 2>{});
 #pragma unroll
       for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lhalf[c].x) + static_cast<double>(lhalf[c].y);
       if constexpr (GRAD) {
