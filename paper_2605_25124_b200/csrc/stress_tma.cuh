@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   const int64_t J1 = min(J0 + a.chunk_len, a.nb);
   const int nblocks = static_cast<int>(J1 - J0);
   const int nhalves = 2 * nblocks;
-  const int nc = (MODE == 1) ? 1 : a.ncand;
+  const int nc = (MODE == 1) ? 1 : (MODE == 2 ? kTmaCand : a.ncand);  // fused passes always carry both trials
   const float* __restrict__ D = static_cast<const float*>(a.D);
   const float* __restrict__ W = static_cast<const float*>(a.W);
   const float delta = static_cast<float>(a.huber_delta);
