@@ -41,6 +41,15 @@ constexpr int kHalfRows = 64;
 constexpr int kHalfFloats = kHalfRows * kPT;  // 8192 floats = 32 KB
 constexpr int kMR = 4;                        // micro-tile rows per half (ti*4 + x)
 constexpr int kTmaCand = 2;                   // trial points per loss pass (y_j kept in registers)
+// Thread column tj owns columns 4tj..4tj+3 and 64+4tj..64+4tj+3 of a block: each
+// 16-byte shared-memory read of a D row by 8 consecutive threads covers 128
+// contiguous bytes (no bank conflicts; 8 contiguous columns per thread gave 2-way).
+__device__ __forceinline__ int tcol(int tj, int y) { return (y < 4) ? 4 * tj + y : 64 + 4 * tj + (y - 4); }
+// slot of column r in the staged column coordinates: thread tj reads slot y * kTG + tj
+__device__ __forceinline__ int tslot(int r) {
+  const int hi = r >> 6, rr = r & 63;
+  return (4 * hi + (rr & 3)) * kTG + (rr >> 2);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -108,7 +117,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
   __shared__ __align__(8) uint64_t bars[NS];
   __shared__ __align__(16) float sYi[NCM][kPT][Q];
-  __shared__ __align__(16) float sYj[2][NCM][kPT][Q];  // [block parity][cand][yslot(r)][k]: double-buffered
+  __shared__ __align__(16) float sYj[2][NCM][kPT][Q];  // [block parity][cand][tslot(r)][k]: double-buffered
   __shared__ float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
@@ -179,14 +188,14 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     const int yb = b & 1;
     if constexpr (Q == 2) {
       if (sc < NCM)
-        *reinterpret_cast<float2*>(&sYj[yb][sc][yslot(sr)][0]) =
+        *reinterpret_cast<float2*>(&sYj[yb][sc][tslot(sr)][0]) =
             make_float2(static_cast<float>(ycol.x), static_cast<float>(ycol.y));
       if (b + 1 < nblocks) ycol = col_load(J + 1);
     } else {
       for (int e = tid; e < nc * kPT * Q; e += kThreads) {
         const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
         const int64_t j = J * kPT + r;
-        sYj[yb][c][yslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+        sYj[yb][c][tslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
       }
     }
     __syncthreads();
@@ -235,12 +244,12 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       for (int x = 0; x < kMR; ++x) {
         const int rloc = ti * kMR + x;           // row within the half
         const int ri = half * kHalfRows + rloc;  // row within the block
-        const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT);
-        const float4 v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + tj * kMT + 4);
+        const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + 4 * tj);
+        const float4 v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + 64 + 4 * tj);
         const float dv[kMT] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
         float wv[kMT];
 #pragma unroll
-        for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tj * kMT + y] : 1.f;
+        for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tcol(tj, y)] : 1.f;
         float yi[NCM][Q];
 #pragma unroll
         for (int c = 0; c < NCM; ++c) {
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
           constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
           for (int y = 0; y < kMT; ++y) {
-            const int rj = tj * kMT + y;
+            const int rj = tcol(tj, y);
             bool keep = true;
             if constexpr (EDGE) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
             const float Dv = dv[y];
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
           for (int k = 0; k < Q; ++k)
 #pragma unroll
             for (int y = 0; y < kMT; ++y)
-              sRed[(k * kTG + ti) * kPT + tj * kMT + y] = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
+              sRed[(k * kTG + ti) * kPT + tcol(tj, y)] = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
         }
       }
       __syncthreads();  // stage `half` is free (and, after half 1, the column partials are in sRed)
