@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   __shared__ __align__(8) uint64_t bars[NS];
   __shared__ __align__(16) float sYi[NCM][kPT][Q];
   __shared__ __align__(16) float sYj[2][NCM][kPT][Q];  // [block parity][cand][tslot(r)][k]: double-buffered
-  __shared__ float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
+  __shared__ __align__(16) float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   if (a.halt && *a.halt) return;
@@ -377,10 +377,13 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       if constexpr (GRAD) {
         if (half == 1) {
 #pragma unroll
-          for (int k = 0; k < Q; ++k)
-#pragma unroll
-            for (int y = 0; y < kMT; ++y)
-              sRed[(k * kTG + ti) * kPT + tcol(tj, y)] = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
+          for (int k = 0; k < Q; ++k) {  // columns 4tj..+3 and 64+4tj..+3: two 16-byte stores
+            float* dst = sRed + (k * kTG + ti) * kPT;
+            *reinterpret_cast<float4*>(dst + 4 * tj) =
+                make_float4(colacc2[0][k].x, colacc2[0][k].y, colacc2[1][k].x, colacc2[1][k].y);
+            *reinterpret_cast<float4*>(dst + 64 + 4 * tj) =
+                make_float4(colacc2[2][k].x, colacc2[2][k].y, colacc2[3][k].x, colacc2[3][k].y);
+          }
         }
       }
       __syncthreads();  // stage `half` is free (and, after half 1, the column partials are in sRed)
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     }
     if constexpr (GRAD) {  // column partials of block J: 16 ti-threads per column, fixed order
       for (int e = tid; e < kPT * Q; e += kThreads) {
-        const int col = e / Q, k = e % Q;
+        const int col = e % kPT, k = e / kPT;  // a warp reads 32 consecutive columns of one k
         float s = 0.f;
 #pragma unroll
         for (int t = 0; t < kTG; ++t) s += sRed[(k * kTG + t) * kPT + col];
