@@ -150,10 +150,19 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   if (tid == 0)
     for (int h = 0; h < min(NS, nhalves); ++h) issue(h);
 
-  for (int e = tid; e < nc * kPT * Q; e += kThreads) {
-    const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
+  if constexpr (Q == 2) {  // one 16-byte load per (candidate, row)
+    const int c = tid >> 7, r = tid & (kPT - 1);
     const int64_t i = I * kPT + r;
-    sYi[c][r][k] = (i < a.n) ? static_cast<float>(a.Y[c][i * Q + k]) : 0.f;
+    if (c < NCM) {
+      const double2 v = (c < nc && i < a.n) ? reinterpret_cast<const double2*>(a.Y[c])[i] : make_double2(0.0, 0.0);
+      *reinterpret_cast<float2*>(&sYi[c][r][0]) = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
+    }
+  } else {
+    for (int e = tid; e < nc * kPT * Q; e += kThreads) {
+      const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
+      const int64_t i = I * kPT + r;
+      sYi[c][r][k] = (i < a.n) ? static_cast<float>(a.Y[c][i * Q + k]) : 0.f;
+    }
   }
   double lossacc[NCM];
 #pragma unroll
