@@ -49,6 +49,7 @@ int64_t chunk_blocks(int64_t nb) {
   return std::max<int64_t>(1, std::min<int64_t>(4, nblk / (148 * 8)));
 }
 constexpr double kTiny = 1e-300;  // embed.cpp:13
+constexpr double kPreciseRel = 1e-6;  // fp32-storage loss changes below this are re-evaluated in fp64
 
 int padded_q(int q) { return q <= 4 ? q : q; }
 
@@ -155,6 +156,19 @@ std::vector<double> Engine::loss_raw(int kind, double delta, const double* const
   for (int c = 0; c < nc; ++c) a.Y[c] = Ys[c];
   a.ncand = nc;
   launch_stress_pass(a, Q, false, D->storage, st);
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
+  std::vector<double> out(static_cast<size_t>(nc));
+  GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  ++passes;
+  return out;
+}
+
+std::vector<double> Engine::loss_raw_precise(int kind, double delta, const double* const* Ys, int nc) {
+  PassArgs a = args(kind, delta);
+  for (int c = 0; c < nc; ++c) a.Y[c] = Ys[c];
+  a.ncand = nc;
+  launch_pass_precise(a, Q, st);
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
   std::vector<double> out(static_cast<size_t>(nc));
   GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -282,7 +296,7 @@ Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, doubl
 }
 
 GdState Engine::device_gd(int kind, double delta, double f, double step, int it, int pred, int max_iters,
-                          double rel_tol, std::vector<double>& history) {
+                          double rel_tol, std::vector<double>& history, double precise_rel) {
   if (!sq2.get()) {
     sq2.alloc(2 * kSqBlocks);
     gdst.alloc(2);
@@ -317,7 +331,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + par * kSqBlocks, nsq,
                      sq2.get() + (par ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
                      cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
-                     rel_tol, have_pre ? pre : nullptr, st);
+                     rel_tol, have_pre ? pre : nullptr, precise_rel, st);
       par ^= 1;
       b.halt = &gdst.get()[par].stop;
       launch_pass_fused_f32(b, Q, st);
@@ -500,12 +514,14 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
   // accepted run without a host round trip (gd_step_kernel); GMDS_HOST_GD=1
   // keeps every decision on the host (same arithmetic, same trajectory).
   const bool devloop = spec && !std::getenv("GMDS_HOST_GD");
+  const bool precise_ok = !std::getenv("GMDS_NO_PRECISE");
   for (; it < max_iters; ++it) {
     Engine::GradTrials gt;
     int slot_of[2] = {0, 1};  // slot of (step, step/2) in gt.trial / E.cand
     bool decided_on_device = false;
     if (devloop && have_grad) {
-      const GdState S = E.device_gd(kind, rp.delta, f, step, it, pred, max_iters, rel_tol, r.history);
+      const GdState S = E.device_gd(kind, rp.delta, f, step, it, pred, max_iters, rel_tol, r.history,
+                                    precise_ok ? kPreciseRel : 0.0);
       it = S.it;
       f = S.f;
       step = S.step;
@@ -550,6 +566,22 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     if (grad_sq <= 0.0) {
       stalled = true;
       break;
+    }
+    // fp32 storage resolves a change of the loss only above ~1e-7 relative (one pair's
+    // e = D - dist changes by less than its ulp).  When both trials are within
+    // kPreciseRel of f, the decision is taken on fp64-arithmetic losses of Y and both
+    // trial points (one extra pass): the reference's first iterations, whose losses
+    // change by ~1e-13, are then followed instead of stalling on equal fp32 sums.
+    if (E.D->storage == GMDS_F32 && precise_ok) {
+      const double tol = kPreciseRel * std::abs(f);
+      if (std::abs(E.loss_of(kind, gt.trial[0]) - f) <= tol && std::abs(E.loss_of(kind, gt.trial[1]) - f) <= tol) {
+        const double* Ys[3] = {E.Y.get(), E.cand[0].get(), E.cand[1].get()};
+        const std::vector<double> raws = E.loss_raw_precise(kind, rp.delta, Ys, 3);
+        f = E.loss_of(kind, raws[0]);
+        if (!r.history.empty()) r.history.back() = f;  // the loss at Y, now in fp64 arithmetic
+        gt.trial[0] = raws[1];
+        gt.trial[1] = raws[2];
+      }
     }
     double f_new = f;
     bool accepted = false;

@@ -32,6 +32,8 @@ struct Engine {
   PassArgs args(int kind, double delta) const;
   // raw loss sums at up to kMaxCand configurations (one pass)
   std::vector<double> loss_raw(int kind, double delta, const double* const* Ys, int nc);
+  // the same in fp64 arithmetic over fp32 storage (stress_pass_kernel<.., float, .., double>)
+  std::vector<double> loss_raw_precise(int kind, double delta, const double* const* Ys, int nc);
   // raw gradient sums into graw, returns the raw loss at Yd (one pass)
   double grad_raw(int kind, double delta, const double* Yd);
   // raw sums over one shard's chunks (sharded fits; summed across ranks)
@@ -63,7 +65,7 @@ struct Engine {
   // host (stop 2: that iteration's trial losses and |g|^2 are in the state).
   // Appends the accepted losses to history.
   GdState device_gd(int kind, double delta, double f, double step, int it, int pred, int max_iters, double rel_tol,
-                    std::vector<double>& history);
+                    std::vector<double>& history, double precise_rel);
   DevBuf<double> sq2, hist;
   DevBuf<GdState> gdst;
   double loss_of(int kind, double raw) const;

@@ -53,11 +53,14 @@ void launch_reduce_rows(const double* rowpart, const double* colpart, const int6
 void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
-                    double* history, int max_iters, double rel_tol, const double* pre, cudaStream_t st);
+                    double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
+                    cudaStream_t st);
 size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass
 void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st);
+// fp32 storage, fp64 arithmetic: loss of up to kMaxCand points
+void launch_pass_precise(const PassArgs& a, int Q, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 // raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;

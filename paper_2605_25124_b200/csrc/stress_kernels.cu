@@ -289,7 +289,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                double* __restrict__ cand1, double* __restrict__ gnext,
                                const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
-                               double rel_tol, const double* __restrict__ pre) {
+                               double rel_tol, const double* __restrict__ pre, double precise_rel) {
   __shared__ double red[1024];
   __shared__ double sgsq;
   const GdState S = st[par];
@@ -325,7 +325,10 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   };
   int acc_c = -1;
   double f_new = S.f, sc_acc = 0.0;
-  if (gsq > 0.0) {
+  // both trials within fp32 storage's resolution of f: the host re-evaluates them in fp64
+  const double tol = precise_rel * fabs(S.f);
+  const bool unresolved = precise_rel > 0.0 && fabs(loss_of(t0) - S.f) <= tol && fabs(loss_of(t1) - S.f) <= tol;
+  if (gsq > 0.0 && !unresolved) {
     for (int c = 0; c < 2; ++c) {  // step, then step/2 (the reference's order)
       const double sc = (c == 0) ? S.step : __dmul_rn(S.step, 0.5);
       const int slot = (S.pred == 0) ? c : 1 - c;
@@ -482,9 +485,11 @@ int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int k
 void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
-                    double* history, int max_iters, double rel_tol, const double* pre, cudaStream_t st) {
+                    double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
+                    cudaStream_t st) {
   gd_step_kernel<<<nsq, 256, 0, st>>>(st2, par, losspart, nparts, stride, sqprev, nsq, sqnext, kind, sum_sq, sum, Y,
-                                      cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre);
+                                      cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
+                                      precise_rel);
   count_launch();
   check_launch("gd_step_kernel");
 }

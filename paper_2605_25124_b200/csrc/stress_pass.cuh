@@ -107,9 +107,11 @@ __device__ __forceinline__ int yslot(int r) { return (r % kMT) * kTG + r / kMT; 
 using namespace stress_detail;
 
 // ---------------------------------------------------------------------------
-template <int Q, typename TD, bool GRAD, int KIND>
+// MT: arithmetic type (fp64 for fp64 storage; fp32 storage takes fp32 math in the
+// TMA kernels and fp64 math in the "precise" loss pass that resolves tiny changes)
+template <int Q, typename TD, bool GRAD, int KIND, typename MT = typename MathOf<TD>::type>
 __global__ void __launch_bounds__(kThreads) stress_pass_kernel(PassArgs a) {
-  using M = typename MathOf<TD>::type;
+  using M = MT;
   constexpr int NCM = GRAD ? 1 : kMaxCand;
   __shared__ M sYi[NCM][kPT][Q];
   __shared__ M sYj[NCM][kPT][Q];  // [yslot(r)]
@@ -291,5 +293,17 @@ void launch_pass_td(const PassArgs& a, int Q, cudaStream_t st);
       default: fail(GMDS_ERROR, "stress pass: unsupported padded dimension");               \
     }                                                                                       \
   }
+
+// fp32 storage, fp64 arithmetic, loss only (Engine::loss_raw_precise)
+#define GMDS_PRECISE_KIND(QQ, KK) \
+  case KK: stress_pass_kernel<QQ, float, false, KK, double><<<g, kThreads, 0, st>>>(a); break;
+#define GMDS_PRECISE_Q(QQ)                                                                      \
+  case QQ:                                                                                      \
+    switch (a.kind) {                                                                           \
+      GMDS_PRECISE_KIND(QQ, kKruskal) GMDS_PRECISE_KIND(QQ, kHuber) GMDS_PRECISE_KIND(QQ, kSammon) \
+      GMDS_PRECISE_KIND(QQ, kSmacof) GMDS_PRECISE_KIND(QQ, kGuttman)                            \
+      default: fail(GMDS_ERROR, "stress pass: bad kind");                                       \
+    }                                                                                           \
+    break;
 
 }  // namespace gmds

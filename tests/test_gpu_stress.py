@@ -391,3 +391,48 @@ def test_tune_batched_eigensolver_matches(monkeypatch):
     r = O.tune_nu(X, 2, grid, 3) if hasattr(O, "tune_nu") else None
     if r is not None:
         assert np.allclose(a["mean_stress"], r.mean_stress, rtol=1e-8)
+
+
+def test_image_shape_fp32_storage_trajectory_scaled_init():
+    # the metric data's shape at moderate n: fp32 storage of D and a seeded init at
+    # D's scale (RMS(D)/sqrt(2q)) follow the fp64 reference trajectory within the
+    # north-star tolerance over the first iterations
+    g = np.random.default_rng(77)
+    n, p = 1800, 784
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < 0.8] = 0.0
+    X = X.astype(np.float32)
+    D = G.pairwise_matrix(X, 2.0)
+    iu = np.triu_indices(n, 1)
+    s = float(np.sqrt(np.mean(D[iu] ** 2) / 4.0))
+    Y0 = g.normal(0.0, s, (n, 2))
+    a = G.minimize_stress(D, 2, "kruskal", max_iters=30, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    o = O.minimize_stress(D, 2, "kruskal", max_iters=30, rel_tol=1e-300, Y0=Y0)
+    h, ho = np.array(a["stress_history"]), np.array(o.stress_history)
+    m = min(len(h), len(ho))
+    assert m >= 20
+    assert np.max(np.abs(h[:m] - ho[:m]) / ho[:m]) <= TRAJ
+
+
+def test_fp32_storage_follows_fp64_through_tiny_steps():
+    # Kruskal from N(0, 0.1^2) against Gini distances ~3e4: the reference's first
+    # iterations change the loss by ~1e-13 relative, below fp32 storage's resolution;
+    # those decisions are re-evaluated (fp64 arithmetic), so the fp32-storage fit
+    # follows the fp64-storage trajectory instead of stalling or wandering
+    g = np.random.default_rng(78)
+    n, p = 2600, 784
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < 0.8] = 0.0
+    X = X.astype(np.float32)
+    D = G.pairwise_matrix(X, 2.0)
+    Y0 = g.normal(0.0, 0.1, (n, 2))
+    a = G.minimize_stress(D, 2, "kruskal", max_iters=60, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    b = G.minimize_stress(D, 2, "kruskal", max_iters=60, rel_tol=1e-300, Y0=Y0, storage=G.F64)
+    assert a["iterations"] == b["iterations"] == 60
+    h, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
+    assert np.max(np.abs(h - hb) / hb) <= 1e-6
+    assert hb[-1] < 0.9 * hb[0]  # the fit left the tiny-step phase

@@ -99,6 +99,10 @@ def c3():
     Dm, td = timed(lambda: G.dmat_gini_device(dX.data_ptr(), G.F32, 5000, 784, 2.0, G.F32))
     Y0 = np.random.default_rng(3).normal(0.0, 0.1, (5000, 2))
     e, tf = timed(lambda: G.minimize_stress(Dm, 2, "kruskal", max_iters=2000, rel_tol=1e-300, Y0=Y0))
+    # the same fit with fp64 storage of D (parity mode): the reference's first iterations
+    # change the loss by ~1e-13 relative, below fp32 storage's resolution
+    Dm64 = G.dmat_gini_device(dX.data_ptr(), G.F32, 5000, 784, 2.0, G.F64)
+    e64, tf64 = timed(lambda: G.minimize_stress(Dm64, 2, "kruskal", max_iters=2000, rel_tol=1e-300, Y0=Y0))
     I = np.random.default_rng(4).integers(0, 5000, 2000)
     J = np.random.default_rng(5).integers(0, 5000, 2000)
     keep = I < J
@@ -114,6 +118,9 @@ def c3():
         tr = (time.perf_counter() - t0) / sum(4999 - i for i in range(rows)) * (5000 * 4999 / 2)
     return {"config": "C3", "n": 5000, "p": 784, "distance_s": td, "pairs_per_s": 5000 * 4999 / 2 / td,
             "fit_2000_iters_s": tf, "iters_per_s": e["iterations"] / tf, "final_stress": e["stress"],
+            "fit_iterations": e["iterations"],
+            "fp64_storage": {"fit_s": tf64, "iterations": e64["iterations"], "final_stress": e64["stress"],
+                             "iters_per_s": e64["iterations"] / tf64},
             "D_maxnorm_err_600rows": err, "ref_cpu_distance_s_extrapolated": tr, "checked_pairs": int(keep.sum()),
             "ref_pairs_mean": float(np.mean(ref))}
 
