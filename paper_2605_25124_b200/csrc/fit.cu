@@ -177,6 +177,22 @@ std::vector<double> Engine::loss_raw_precise(int kind, double delta, const doubl
   return out;
 }
 
+std::vector<double> Engine::loss_diff(int kind, double s0, double s1) {
+  PassArgs a = args(kind, 0.0);
+  a.Y[0] = Y.get();
+  a.Y[1] = graw.get();
+  a.ncand = 2;
+  a.dstep[0] = s0;
+  a.dstep[1] = s1;
+  launch_pass_diff_f32(a, Q, st);
+  launch_sum_parts(losspart.get(), nchunks, kMaxCand, 3, scal.get(), st);
+  double h[3];
+  GMDS_CUDA(cudaMemcpyAsync(h, scal.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  ++passes;
+  return {h[2], h[0], h[1]};  // Y, Y - s0 g, Y - s1 g (losspart column 0: the first trial, as a trial pass)
+}
+
 double Engine::grad_raw(int kind, double delta, const double* Yd) {
   if (q > 64) fail(GMDS_INVALID_INPUT, "stress gradient: embedding dimension above 64 is not supported");
   PassArgs a = args(kind, delta);
@@ -515,6 +531,7 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
   // keeps every decision on the host (same arithmetic, same trajectory).
   const bool devloop = spec && !std::getenv("GMDS_HOST_GD");
   const bool precise_ok = !std::getenv("GMDS_NO_PRECISE");
+  const bool diff_ok = !std::getenv("GMDS_NO_DIFF");  // GMDS_NO_DIFF=1: fp64-arithmetic re-evaluation instead
   for (; it < max_iters; ++it) {
     Engine::GradTrials gt;
     int slot_of[2] = {0, 1};  // slot of (step, step/2) in gt.trial / E.cand
@@ -575,8 +592,19 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     if (E.D->storage == GMDS_F32 && precise_ok) {
       const double tol = kPreciseRel * std::abs(f);
       if (std::abs(E.loss_of(kind, gt.trial[0]) - f) <= tol && std::abs(E.loss_of(kind, gt.trial[1]) - f) <= tol) {
-        const double* Ys[3] = {E.Y.get(), E.cand[0].get(), E.cand[1].get()};
-        const std::vector<double> raws = E.loss_raw_precise(kind, rp.delta, Ys, 3);
+        // Kruskal: the fp32 difference pass (the trial steps in slot order); other kinds:
+        // fp64 arithmetic over the fp32 image
+        std::vector<double> raws;
+        if (kind == kKruskal && !E.W && diff_ok) {
+          const double sf = (slot_of[0] == 0) ? step : step * 0.5, ss = (slot_of[0] == 0) ? step * 0.5 : step;
+          raws = E.loss_diff(kind, sf, ss);
+        } else {
+          // trial points first: losspart column 0 keeps the first trial's loss, which the
+          // next iteration's finish reads as the loss at the accepted point
+          const double* Ys[3] = {E.cand[0].get(), E.cand[1].get(), E.Y.get()};
+          const std::vector<double> r3 = E.loss_raw_precise(kind, rp.delta, Ys, 3);
+          raws = {r3[2], r3[0], r3[1]};
+        }
         f = E.loss_of(kind, raws[0]);
         if (!r.history.empty()) r.history.back() = f;  // the loss at Y, now in fp64 arithmetic
         gt.trial[0] = raws[1];

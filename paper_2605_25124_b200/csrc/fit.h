@@ -34,6 +34,9 @@ struct Engine {
   std::vector<double> loss_raw(int kind, double delta, const double* const* Ys, int nc);
   // the same in fp64 arithmetic over fp32 storage (stress_pass_kernel<.., float, .., double>)
   std::vector<double> loss_raw_precise(int kind, double delta, const double* const* Ys, int nc);
+  // e^2 kinds over fp32 storage: raw losses at Y and at Y - s0 g, Y - s1 g (g = graw, scaled),
+  // the trial values as Y's plus accurately summed differences (difference pass)
+  std::vector<double> loss_diff(int kind, double s0, double s1);
   // raw gradient sums into graw, returns the raw loss at Yd (one pass)
   double grad_raw(int kind, double delta, const double* Yd);
   // raw sums over one shard's chunks (sharded fits; summed across ranks)

@@ -30,6 +30,7 @@ struct PassArgs {
   int64_t cand_stride_row;  // elements between candidates' rowpart images (fused trial passes)
   int64_t cand_stride_col;  // elements between candidates' colpart images
   const int* halt;          // device flag: nonzero -> the pass is a no-op (device-resident loops)
+  double dstep[2];          // difference passes: trial steps (Y[0] = Y, Y[1] = scaled gradient)
 };
 
 // Device-resident gradient descent state (double-buffered by iteration parity)
@@ -61,6 +62,8 @@ void launch_sum_parts(const double* part, int64_t count, int stride, int m, doub
 void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st);
 // fp32 storage, fp64 arithmetic: loss of up to kMaxCand points
 void launch_pass_precise(const PassArgs& a, int Q, cudaStream_t st);
+// fp32 storage, e^2 kinds: losspart slots (sum of e_t^2 - e_0^2 at Y - s_t g for t = 0, 1; sum e_0^2 at Y)
+void launch_pass_diff_f32(const PassArgs& a, int Q, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 // raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;

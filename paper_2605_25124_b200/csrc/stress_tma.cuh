@@ -114,7 +114,8 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 template <int Q, int MODE, int KIND>
 __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
-  constexpr bool GRAD = (MODE != 0);  // gradient accumulation (of configuration 0)
+  constexpr bool DIFF = (MODE == 3);  // loss differences: configurations are Y and the gradient
+  constexpr bool GRAD = (MODE == 1 || MODE == 2);  // gradient accumulation (of configuration 0)
   constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
   constexpr int NS = GRAD ? kStagesGrad : kStages;
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   const int64_t J1 = min(J0 + a.chunk_len, a.nb);
   const int nblocks = static_cast<int>(J1 - J0);
   const int nhalves = kParts * nblocks;
-  const int nc = (MODE == 1) ? 1 : (MODE == 2 ? kTmaCand : a.ncand);  // fused passes always carry both trials
+  const int nc = (MODE == 1) ? 1 : (MODE >= 2 ? kTmaCand : a.ncand);  // fused / difference passes: two configurations
   const float* __restrict__ D = static_cast<const float*>(a.D);
   const float* __restrict__ W = static_cast<const float*>(a.W);
   const float delta = static_cast<float>(a.huber_delta);
@@ -171,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   double lossacc[NCM];
 #pragma unroll
   for (int c = 0; c < NCM; ++c) lossacc[c] = 0.0;
+  double diffacc[DIFF ? 3 : 1] = {};  // DIFF: sum dE_0, sum dE_1, sum e_0^2
+  const float ds0 = static_cast<float>(a.dstep[0]), ds1 = static_cast<float>(a.dstep[1]);
   // GRAD: this thread's 8 rows (4 per half) accumulate over every block of the
   // chunk in registers and are reduced across the 16 tj-threads once per chunk
   float rowsum[GRAD ? kParts : 1][GRAD ? kMR : 1][Q];
@@ -249,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       float2 lhalf[NCM];  // loss of this half, two fp32 lanes per candidate (widened once per half)
 #pragma unroll
       for (int c = 0; c < NCM; ++c) lhalf[c] = make_float2(0.f, 0.f);
+      float dhalf[3] = {0.f, 0.f, 0.f};  // DIFF: this half's sums
       // the row loop, instantiated per block kind (edge / packed / generic) so the
       // interior-block version is a branch-free, fully unrolled loop over the rows
       auto row_loop = [&](auto mode_tag) {
@@ -316,6 +320,48 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             }
           }
         };
+        // DIFF (e^2 kinds, unweighted): per pair, with dy = y_i - y_j and dg = g_i - g_j,
+        // a_t = |dy - s_t dg|^2 - |dy|^2 = s_t (s_t |dg|^2 - 2 <dy, dg>) is formed from the
+        // small quantities, dist_t - dist_0 = a_t / (dist_t + dist_0) and
+        // e_t^2 - e_0^2 = (dist_t - dist_0) (dist_t - dist_0 - 2 e_0): the loss changes
+        // keep fp32's relative precision however small the step (the direct e_t^2 would
+        // lose them below one ulp of e).
+        auto pairs_diff = [&]() {
+#pragma unroll
+          for (int y = 0; y < kMT; ++y) {
+            const int rj = tcol(tj, y);
+            bool keep = true;
+            if (edge) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
+            float dy[Q], dg[Q];
+            float d0 = FLT_MIN, pp = 0.f, qq = 0.f;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              dy[k] = yi[0][k] - ((y & 1) ? yj2[0][y / 2][k].y : yj2[0][y / 2][k].x);
+              dg[k] = yi[1][k] - ((y & 1) ? yj2[1][y / 2][k].y : yj2[1][y / 2][k].x);
+              d0 = fmaf(dy[k], dy[k], d0);
+              pp = fmaf(dy[k], dg[k], pp);
+              qq = fmaf(dg[k], dg[k], qq);
+            }
+            const float dist0 = d0 * rsqrt_mufu(d0);
+            const float e0 = dv[y] - dist0;
+            float t0 = 0.f, t1 = 0.f;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const float st = t ? ds1 : ds0;
+              const float at = st * fmaf(st, qq, -2.f * pp);
+              const float dt2 = fmaxf(d0 + at, FLT_MIN);
+              const float distt = dt2 * rsqrt_mufu(dt2);
+              const float dd = at / (distt + dist0);  // dist_t - dist_0
+              const float de = dd * (dd - 2.f * e0);  // e_t^2 - e_0^2
+              if (t) t1 = de; else t0 = de;
+            }
+            if (keep) {
+              dhalf[0] += t0;
+              dhalf[1] += t1;
+              dhalf[2] = fmaf(e0, e0, dhalf[2]);
+            }
+          }
+        };
         // Kruskal / Guttman, interior, unweighted: two pairs (y, y+1) per
         // FADD2 / FMUL2 / FFMA2, bare MUFU.RSQ on d2 seeded with FLT_MIN (so no
         // clamp: coincident points give dy = 0 and add exactly 0)
@@ -371,7 +417,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             }
           }
         };
-        if constexpr (MODE_ROWS == 1)
+        if constexpr (DIFF)
+          pairs_diff();
+        else if constexpr (MODE_ROWS == 1)
           pairs(std::true_type{});
         else if constexpr (MODE_ROWS == 0)
           pairs_packed();
@@ -387,6 +435,10 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
         row_loop(std::integral_constant<int, 2>{});
 #pragma unroll
       for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lhalf[c].x) + static_cast<double>(lhalf[c].y);
+      if constexpr (DIFF) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) diffacc[c] += static_cast<double>(dhalf[c]);
+      }
       if constexpr (GRAD) {
         if (half == kParts - 1) {
 #pragma unroll
@@ -432,6 +484,26 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
     if ((tid & 31) == 0) sLoss[tid >> 5][c] = v;
   }
+  if constexpr (DIFF) {
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double v = diffacc[c];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+      if ((tid & 31) == 0) sLoss[tid >> 5][c] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {  // slots: raw at Y - s0 g, raw at Y - s1 g, raw at Y (slot 0 as a trial pass leaves it)
+      double sd[3] = {0.0, 0.0, 0.0};
+      for (int w = 0; w < kThreads / 32; ++w)
+        for (int c = 0; c < 3; ++c) sd[c] += sLoss[w][c];
+      a.losspart[chunk * kMaxCand + 0] = sd[2] + sd[0];
+      a.losspart[chunk * kMaxCand + 1] = sd[2] + sd[1];
+      a.losspart[chunk * kMaxCand + 2] = sd[2];
+    }
+    return;
+  }
   __syncthreads();
   if (tid < nc) {
     double s = 0.0;
@@ -464,6 +536,13 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
       GMDS_TMA_Q(1) GMDS_TMA_Q(2) GMDS_TMA_Q(3) GMDS_TMA_Q(4)                                             \
       default: fail(GMDS_ERROR, "stress pass: unsupported padded dimension");                             \
     }
+#define GMDS_INSTANTIATE_TMA_DIFF                                                                         \
+  void launch_pass_diff_f32(const PassArgs& a, int Q, cudaStream_t st) {                                  \
+    constexpr int MODE = 3;                                                                               \
+    GMDS_TMA_SWITCH                                                                                       \
+    count_launch();                                                                                       \
+    check_launch("stress_tma_kernel (difference)");                                                       \
+  }
 #define GMDS_INSTANTIATE_TMA_FUSED                                                                        \
   void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st) {                                 \
     constexpr int MODE = 2;                                                                               \
