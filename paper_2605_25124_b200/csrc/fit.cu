@@ -339,16 +339,29 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   S.it = it;
   S.pred = pred;
   GMDS_CUDA(cudaMemcpyAsync(gdst.get(), &S, sizeof S, cudaMemcpyHostToDevice, st));
-  int par = 0;
+  int par = 0;  // state buffer (flips per gd_step launch)
+  int sqp = 0;  // |g|^2 partials buffer (flips per iteration)
   int issued = it;
+  PassArgs dpa = args(kind, delta);  // the device loop's difference pass (runs only when a decision is pending)
+  dpa.Y[0] = Y.get();
+  dpa.Y[1] = graw.get();
+  dpa.ncand = 2;
+  const bool dev_diff = precise_rel > 0.0 && kind == kKruskal && !W;
   for (;;) {
     const int batch = std::max(1, std::min(16, max_iters - issued));
     for (int k = 0; k < batch; ++k) {
-      launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + par * kSqBlocks, nsq,
-                     sq2.get() + (par ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
-                     cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
-                     rel_tol, have_pre ? pre : nullptr, precise_rel, st);
-      par ^= 1;
+      for (int phase = 0; phase < (dev_diff ? 2 : 1); ++phase) {
+        launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + sqp * kSqBlocks, nsq,
+                       sq2.get() + (sqp ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
+                       cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
+                       rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st);
+        par ^= 1;
+        if (phase == 0 && dev_diff) {
+          dpa.gds = gdst.get() + par;
+          launch_pass_diff_f32(dpa, Q, st);
+        }
+      }
+      sqp ^= 1;
       b.halt = &gdst.get()[par].stop;
       launch_pass_fused_f32(b, Q, st);
       launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(),
@@ -360,7 +373,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
     if (S.stop != 0) break;
   }
   // passes: the prime plus one per decision that continued (all accepted ones but a final stop)
-  passes += (S.it - it) - (S.stop == 1 ? 1 : 0);
+  passes += (S.it - it) - (S.stop == 1 ? 1 : 0) + S.ndiff;  // + the difference passes run on the device
   if (S.it > it) {
     std::vector<double> h(static_cast<size_t>(S.it - it));
     GMDS_CUDA(cudaMemcpyAsync(h.data(), hist.get() + it + 1, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));

@@ -31,6 +31,7 @@ struct PassArgs {
   int64_t cand_stride_col;  // elements between candidates' colpart images
   const int* halt;          // device flag: nonzero -> the pass is a no-op (device-resident loops)
   double dstep[2];          // difference passes: trial steps (Y[0] = Y, Y[1] = scaled gradient)
+  const struct GdState* gds;  // difference passes in the device loop: run only if gds->pending, steps from it
 };
 
 // Device-resident gradient descent state (double-buffered by iteration parity)
@@ -38,6 +39,9 @@ struct GdState {
   double f, step;
   double t0, t1, gsq;  // the last decided pass: raw trial losses (slot order), |g|^2
   int it, pred, stop, stalled;  // stop: 0 running, 1 finished, 2 iteration handed to the host
+  int ndiff;                    // difference passes run so far (pass accounting)
+  int pending;                  // 1: the fused pass's trial losses were below fp32 resolution; a
+                                // difference pass follows and gd_step phase 1 decides on it
 };
 
 struct Steps {
@@ -55,7 +59,7 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    cudaStream_t st);
+                    int phase, cudaStream_t st);
 size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass

@@ -289,17 +289,23 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                double* __restrict__ cand1, double* __restrict__ gnext,
                                const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
-                               double rel_tol, const double* __restrict__ pre, double precise_rel) {
+                               double rel_tol, const double* __restrict__ pre, double precise_rel, int phase) {
   __shared__ double red[1024];
   __shared__ double sgsq;
   const GdState S = st[par];
   GdState* N = st + (par ^ 1);
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  if (S.stop) {
+  if (S.stop || (phase == 1 && !S.pending)) {
     if (lead) *N = S;
     return;
   }
-  // the same sums the host path reads: trial losses as sum_parts_kernel, |g|^2 in order
+  // phase 1: the difference pass left raw losses at the two trials (columns 0, 1) and at
+  // Y (column 2); the loss at Y is re-based on it (history too), as the host path does
+  double fY = S.f;
+  if (phase == 1) {
+    pre = nullptr;
+    fY = -1.0;  // set below once loss_of is defined
+  }
   // the pass's loss sums: from the reduction launch's extra CTA when it ran, else here (same order)
   const double t0 = pre ? pre[0] : tree_sum<1024>(losspart, nparts, stride, 0, red);
   const double t1 = pre ? pre[1] : tree_sum<1024>(losspart, nparts, stride, 1, red);
@@ -323,17 +329,31 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     if (kind == kSammon) return __dmul_rn(__ddiv_rn(1.0, sum), raw);
     return raw;
   };
+  if (phase == 1) {
+    fY = loss_of(tree_sum<1024>(losspart, nparts, stride, 2, red));
+    R.f = fY;
+    R.pending = 0;
+    if (lead) history[S.it] = fY;
+  }
   int acc_c = -1;
-  double f_new = S.f, sc_acc = 0.0;
-  // both trials within fp32 storage's resolution of f: the host re-evaluates them in fp64
-  const double tol = precise_rel * fabs(S.f);
-  const bool unresolved = precise_rel > 0.0 && fabs(loss_of(t0) - S.f) <= tol && fabs(loss_of(t1) - S.f) <= tol;
+  double f_new = fY, sc_acc = 0.0;
+  // phase 0, both trials within fp32 storage's resolution of f: Kruskal defers to a
+  // difference pass (phase 1 decides); other kinds hand the iteration to the host
+  const double tol = precise_rel * fabs(fY);
+  const bool unresolved = phase == 0 && precise_rel > 0.0 && fabs(loss_of(t0) - fY) <= tol &&
+                          fabs(loss_of(t1) - fY) <= tol;
+  if (unresolved && kind == kKruskal) {
+    R.pending = 1;
+    R.ndiff = S.ndiff + 1;
+    if (lead) *N = R;
+    return;
+  }
   if (gsq > 0.0 && !unresolved) {
     for (int c = 0; c < 2; ++c) {  // step, then step/2 (the reference's order)
       const double sc = (c == 0) ? S.step : __dmul_rn(S.step, 0.5);
       const int slot = (S.pred == 0) ? c : 1 - c;
       const double fc = loss_of(slot == 0 ? t0 : t1);
-      if (fc <= __dsub_rn(S.f, __dmul_rn(__dmul_rn(1e-4, sc), gsq))) {
+      if (fc <= __dsub_rn(fY, __dmul_rn(__dmul_rn(1e-4, sc), gsq))) {
         acc_c = c;
         f_new = fc;
         sc_acc = sc;
@@ -360,7 +380,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     combine();
     return;
   }
-  const double decrease = __ddiv_rn(__dsub_rn(S.f, f_new), fmax(S.f, 1e-300));
+  const double decrease = __ddiv_rn(__dsub_rn(fY, f_new), fmax(fY, 1e-300));
   R.f = f_new;
   R.it = S.it + 1;
   R.step = __dmul_rn(sc_acc, 2.0);
@@ -486,10 +506,10 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    cudaStream_t st) {
+                    int phase, cudaStream_t st) {
   gd_step_kernel<<<nsq, 256, 0, st>>>(st2, par, losspart, nparts, stride, sqprev, nsq, sqnext, kind, sum_sq, sum, Y,
                                       cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-                                      precise_rel);
+                                      precise_rel, phase);
   count_launch();
   check_launch("gd_step_kernel");
 }

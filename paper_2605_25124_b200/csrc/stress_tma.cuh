@@ -127,6 +127,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   if (a.halt && *a.halt) return;
+  if constexpr (MODE == 3) {
+    if (a.gds && (a.gds->pending == 0 || a.gds->stop != 0)) return;
+  }
   const int tid = threadIdx.x;
   const int ti = tid / kTG, tj = tid % kTG;
   const int64_t chunk = blockIdx.x;
@@ -173,7 +176,12 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
 #pragma unroll
   for (int c = 0; c < NCM; ++c) lossacc[c] = 0.0;
   double diffacc[DIFF ? 3 : 1] = {};  // DIFF: sum dE_0, sum dE_1, sum e_0^2
-  const float ds0 = static_cast<float>(a.dstep[0]), ds1 = static_cast<float>(a.dstep[1]);
+  float ds0 = static_cast<float>(a.dstep[0]), ds1 = static_cast<float>(a.dstep[1]);
+  if (DIFF && a.gds) {  // device loop: the trial steps of the pending decision (slot order)
+    const double st = a.gds->step;
+    ds0 = static_cast<float>(a.gds->pred == 0 ? st : 0.5 * st);
+    ds1 = static_cast<float>(a.gds->pred == 0 ? 0.5 * st : st);
+  }
   // GRAD: this thread's 8 rows (4 per half) accumulate over every block of the
   // chunk in registers and are reduced across the 16 tj-threads once per chunk
   float rowsum[GRAD ? kParts : 1][GRAD ? kMR : 1][Q];
