@@ -370,6 +370,52 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             }
           }
         };
+        // DIFF on interior blocks: the same on column pairs (y, y+1) with packed fp32 math
+        auto pairs_diff_packed = [&]() {
+          const float2 dvp[kMT / 2] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
+                                       make_float2(v1.z, v1.w)};
+          float2 yY[Q], yG[Q];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            yY[k] = make_float2(yi[0][k], yi[0][k]);
+            yG[k] = make_float2(yi[1][k], yi[1][k]);
+          }
+          const float2 s0v = make_float2(ds0, ds0), s1v = make_float2(ds1, ds1);
+          const float2 m2 = make_float2(-2.f, -2.f);
+          float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0;
+#pragma unroll
+          for (int yy = 0; yy < kMT / 2; ++yy) {
+            float2 d0 = make_float2(FLT_MIN, FLT_MIN), pp = make_float2(0.f, 0.f), qq = pp;
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              const float2 dy = f2sub(yY[k], yj2[0][yy][k]);
+              const float2 dg = f2sub(yG[k], yj2[1][yy][k]);
+              d0 = f2fma(dy, dy, d0);
+              pp = f2fma(dy, dg, pp);
+              qq = f2fma(dg, dg, qq);
+            }
+            const float2 dist0 = f2mul(d0, make_float2(rsqrt_mufu(d0.x), rsqrt_mufu(d0.y)));
+            const float2 e0 = f2sub(dvp[yy], dist0);
+            a2 = f2fma(e0, e0, a2);
+            const float2 m2p = f2mul(pp, m2);
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+              const float2 sv = t ? s1v : s0v;
+              const float2 at = f2mul(sv, f2fma(sv, qq, m2p));
+              float2 dt2 = f2add(d0, at);
+              dt2.x = fmaxf(dt2.x, FLT_MIN);
+              dt2.y = fmaxf(dt2.y, FLT_MIN);
+              const float2 distt = f2mul(dt2, make_float2(rsqrt_mufu(dt2.x), rsqrt_mufu(dt2.y)));
+              const float2 den = f2add(distt, dist0);
+              const float2 dd = f2mul(at, make_float2(rcp_mufu(den.x), rcp_mufu(den.y)));
+              const float2 de = f2mul(dd, f2fma(e0, m2, dd));
+              if (t) a1 = f2add(a1, de); else a0 = f2add(a0, de);
+            }
+          }
+          dhalf[0] += a0.x + a0.y;
+          dhalf[1] += a1.x + a1.y;
+          dhalf[2] += a2.x + a2.y;
+        };
         // Kruskal / Guttman, interior, unweighted: two pairs (y, y+1) per
         // FADD2 / FMUL2 / FFMA2, bare MUFU.RSQ on d2 seeded with FLT_MIN (so no
         // clamp: coincident points give dy = 0 and add exactly 0)
@@ -425,8 +471,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             }
           }
         };
-        if constexpr (DIFF)
-          pairs_diff();
+        if constexpr (DIFF) {
+          if constexpr (MODE_ROWS == 0) pairs_diff_packed(); else pairs_diff();
+        }
         else if constexpr (MODE_ROWS == 1)
           pairs(std::true_type{});
         else if constexpr (MODE_ROWS == 0)
