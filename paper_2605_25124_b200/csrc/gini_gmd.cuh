@@ -71,6 +71,18 @@ __device__ __forceinline__ int lower_count(const float* sv, int n, uint32_t t) {
   return pos;
 }
 
+// the same on a row of precomputed codes (the linear kernel stages codes, not values)
+__device__ __forceinline__ int lower_count_codes(const uint32_t* sc, int n, uint32_t t) {
+  int pos = 0;
+#pragma unroll
+  for (int step = 128; step > 0; step >>= 1) {
+    const int idx = pos + step - 1;
+    pos += ((idx < n) && (sc[idx] < t)) ? step : 0;  // idx <= 254: inside shared memory even past n
+  }
+  if (pos == 255 && n == 256 && sc[255] < t) pos = 256;
+  return pos;
+}
+
 // #{F positions < pos} from a position mask QM[8] and its word prefix QP[8]
 __device__ __forceinline__ int qcount(const uint32_t* QM, const uint32_t* QP, int pos, int s) {
   if (pos >= kMaxC) return s;
@@ -119,8 +131,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
   uint32_t* smask = reinterpret_cast<uint32_t*>(rcnt + kRows);  // [64][W]
   uint16_t* spre = reinterpret_cast<uint16_t*>(smask + kRows * W);
   float* svals = reinterpret_cast<float*>(spre + ((kRows * W + 1) & ~1));  // [64][stride]
-  float* ssv = svals + kRows * stride;                                       // [64][stride]
-  uint16_t* spm = reinterpret_cast<uint16_t*>(ssv + kRows * stride);         // [64][stride]
+  uint32_t* ssc = reinterpret_cast<uint32_t*>(svals + kRows * stride);     // [64][stride] sorted value codes
+  uint16_t* spm = reinterpret_cast<uint16_t*>(ssc + kRows * stride);         // [64][stride]
   const float* gv = static_cast<const float*>(sa.vals);
   const double h = 0.5 * static_cast<double>(d + 1);
   const int tstride = kTile + 1;
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
         cnt = static_cast<int>(sa.rowptr[row + 1] - b);
         for (int k = lane; k < cnt && k < stride; k += 32) {
           svals[r * stride + k] = gv[b + k];
-          ssv[r * stride + k] = ga.svs[b + k];
+          ssc[r * stride + k] = fkey(ga.svs[b + k]);
           spm[r * stride + k] = ga.pmap[b + k];
         }
       }
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
         const float f = __double2float_rz(mg);
         const uint32_t code = fkey(f) + ((static_cast<double>(f) != mg) ? 1u : 0u);
         const int n = pos ? ci : cj;
-        const int lb = lower_count(ssv + (pos ? ri : rj) * stride, n, code);  // #{row values < |zz|}
+        const int lb = lower_count_codes(ssc + (pos ? ri : rj) * stride, n, code);  // #{row values < |zz|}
         const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
         const double sl = (lb < n) ? __ldg((pos ? sufi : sufj) + lb) : 0.0;
         if (pos)
