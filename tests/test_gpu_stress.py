@@ -436,3 +436,24 @@ def test_fp32_storage_follows_fp64_through_tiny_steps():
     h, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
     assert np.max(np.abs(h - hb) / hb) <= 1e-6
     assert hb[-1] < 0.9 * hb[0]  # the fit left the tiny-step phase
+
+
+@pytest.mark.parametrize("kind", ["sammon", "huber"])
+def test_fp32_storage_other_kinds_follow_fp64(kind):
+    # the same regime for the other gradient-descent kinds: sub-resolution decisions are
+    # handed to the host and re-taken in fp64 arithmetic over the fp32 image
+    g = np.random.default_rng(79)
+    n, p = 2600, 300  # above the persistent small-fit size: the tiled fp32 passes
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < 0.8] = 0.0
+    X = X.astype(np.float32)
+    D = G.pairwise_matrix(X, 2.0)
+    Y0 = g.normal(0.0, 0.1, (n, 2))
+    hd = 0.5 * float(np.median(D)) if kind == "huber" else None
+    a = G.minimize_stress(D, 2, kind, huber_delta=hd, max_iters=40, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    b = G.minimize_stress(D, 2, kind, huber_delta=hd, max_iters=40, rel_tol=1e-300, Y0=Y0, storage=G.F64)
+    assert a["iterations"] == b["iterations"]
+    h, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
+    assert np.max(np.abs(h - hb) / np.abs(hb)) <= 1e-5
