@@ -362,8 +362,16 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
         }
       }
       sqp ^= 1;
-      b.halt = &gdst.get()[par].stop;
+      b.halt = &gdst.get()[par].halt_fused;
       launch_pass_fused_f32(b, Q, st);
+      if (dev_diff) {  // tiny mode: the gradient at the first trial only (its losses are re-taken anyway)
+        PassArgs gp = args(kind, delta);
+        gp.Y[0] = cand[0].get();
+        gp.ncand = 1;
+        gp.halt = &gdst.get()[par].halt_grad;
+        launch_stress_pass(gp, Q, true, GMDS_F32, st);
+      }
+      b.halt = &gdst.get()[par].stop;
       launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(),
                          b.halt, f32parts(), losspart.get(), nchunks, kMaxCand, have_pre ? pre : nullptr);
     }

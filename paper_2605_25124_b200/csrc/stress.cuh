@@ -42,6 +42,9 @@ struct GdState {
   int ndiff;                    // difference passes run so far (pass accounting)
   int pending;                  // 1: the fused pass's trial losses were below fp32 resolution; a
                                 // difference pass follows and gd_step phase 1 decides on it
+  int tiny;                     // 1: the last change was far below resolution -- the next iteration
+                                // runs the gradient pass only, and its decision defers directly
+  int halt_fused, halt_grad;    // halt flags of the next fused pass / gradient-only pass
 };
 
 struct Steps {

@@ -295,8 +295,13 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   const GdState S = st[par];
   GdState* N = st + (par ^ 1);
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+  auto publish = [&](GdState R) {  // the next passes' halt flags follow stop / tiny
+    R.halt_fused = (R.stop != 0 || R.tiny != 0) ? 1 : 0;
+    R.halt_grad = (R.stop != 0 || R.tiny == 0) ? 1 : 0;
+    *N = R;
+  };
   if (S.stop || (phase == 1 && !S.pending)) {
-    if (lead) *N = S;
+    if (lead) publish(S);
     return;
   }
   // phase 1: the difference pass left raw losses at the two trials (columns 0, 1) and at
@@ -340,12 +345,13 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   // phase 0, both trials within fp32 storage's resolution of f: Kruskal defers to a
   // difference pass (phase 1 decides); other kinds hand the iteration to the host
   const double tol = precise_rel * fabs(fY);
-  const bool unresolved = phase == 0 && precise_rel > 0.0 && fabs(loss_of(t0) - fY) <= tol &&
-                          fabs(loss_of(t1) - fY) <= tol;
+  // (tiny mode: the pass was the gradient-only one, its losses are not trial losses: defer)
+  const bool unresolved = phase == 0 && precise_rel > 0.0 &&
+                          (S.tiny != 0 || (fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol));
   if (unresolved && kind == kKruskal) {
     R.pending = 1;
     R.ndiff = S.ndiff + 1;
-    if (lead) *N = R;
+    if (lead) publish(R);
     return;
   }
   if (gsq > 0.0 && !unresolved) {
@@ -376,7 +382,8 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   };
   if (acc_c < 0 || ((S.pred == 0) ? acc_c : 1 - acc_c) != 0) {  // host takes this iteration
     R.stop = 2;
-    if (lead) *N = R;
+    R.tiny = 0;
+    if (lead) publish(R);
     combine();
     return;
   }
@@ -390,9 +397,12 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   } else if (R.it >= max_iters) {
     R.stop = 1;
   }
+  // tiny mode for the next iteration: this (difference-pass) decision changed f by less than a
+  // quarter of the resolution threshold, so the doubled step will not be resolved either
+  R.tiny = (phase == 1 && fabs(__dsub_rn(fY, f_new)) <= 0.25 * tol) ? 1 : 0;
   if (lead) {
     history[R.it] = f_new;
-    *N = R;
+    publish(R);
   }
   // Y <- cand0 (the accepted point); graw <- scaled gradient there; next trial pair
   const double scale = grad_scale(kind, pre ? pre[2] : tree_sum<256>(losspart, nparts, stride, 0, red), sum_sq, sum);
