@@ -358,7 +358,8 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
         par ^= 1;
         if (phase == 0 && dev_diff) {
           dpa.gds = gdst.get() + par;
-          launch_pass_diff_f32(dpa, Q, st);
+          launch_pass_diff_f32(dpa, Q, st);   // both trials (runs unless the decision is single)
+          launch_pass_diff1_f32(dpa, Q, st);  // the first trial only (runs if single)
         }
       }
       sqp ^= 1;

@@ -45,6 +45,7 @@ struct GdState {
   int tiny;                     // 1: the last change was far below resolution -- the next iteration
                                 // runs the gradient pass only, and its decision defers directly
   int halt_fused, halt_grad;    // halt flags of the next fused pass / gradient-only pass
+  int single;                   // the pending decision's difference pass evaluates the first trial only
 };
 
 struct Steps {
@@ -71,6 +72,8 @@ void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st);
 void launch_pass_precise(const PassArgs& a, int Q, cudaStream_t st);
 // fp32 storage, e^2 kinds: losspart slots (sum of e_t^2 - e_0^2 at Y - s_t g for t = 0, 1; sum e_0^2 at Y)
 void launch_pass_diff_f32(const PassArgs& a, int Q, cudaStream_t st);
+// the same for the first trial only (slot 1 then holds the loss at Y; device loop, tiny mode)
+void launch_pass_diff1_f32(const PassArgs& a, int Q, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 // raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;

@@ -350,6 +350,9 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                           (S.tiny != 0 || (fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol));
   if (unresolved && kind == kKruskal) {
     R.pending = 1;
+    // tiny mode with the step first in slot order: the first trial is all the decision
+    // needs (if it is rejected the iteration goes to the host, which evaluates both)
+    R.single = (S.tiny != 0 && S.pred == 0) ? 1 : 0;
     R.ndiff = S.ndiff + 1;
     if (lead) publish(R);
     return;

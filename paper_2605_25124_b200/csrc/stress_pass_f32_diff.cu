@@ -4,4 +4,5 @@
 
 namespace gmds {
 GMDS_INSTANTIATE_TMA_DIFF
+GMDS_INSTANTIATE_TMA_DIFF1
 }  // namespace gmds

@@ -114,7 +114,8 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 template <int Q, int MODE, int KIND>
 __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
   using namespace tma_detail;
-  constexpr bool DIFF = (MODE == 3);  // loss differences: configurations are Y and the gradient
+  constexpr bool DIFF = (MODE == 3 || MODE == 5);  // loss differences: configurations are Y and the gradient
+  constexpr int NT = (MODE == 5) ? 1 : 2;            // trial steps of a difference pass (5: the first only)
   constexpr bool GRAD = (MODE == 1 || MODE == 2);  // gradient accumulation (of configuration 0)
   constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
@@ -127,8 +128,8 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   if (a.halt && *a.halt) return;
-  if constexpr (MODE == 3) {
-    if (a.gds && (a.gds->pending == 0 || a.gds->stop != 0)) return;
+  if constexpr (DIFF) {  // device loop: run only for a pending decision, in the matching width
+    if (a.gds && (a.gds->pending == 0 || a.gds->stop != 0 || (a.gds->single != 0) != (NT == 1))) return;
   }
   const int tid = threadIdx.x;
   const int ti = tid / kTG, tj = tid % kTG;
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             const float e0 = dv[y] - dist0;
             float t0 = 0.f, t1 = 0.f;
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < NT; ++t) {
               const float st = t ? ds1 : ds0;
               const float at = st * fmaf(st, qq, -2.f * pp);
               const float dt2 = fmaxf(d0 + at, FLT_MIN);
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             a2 = f2fma(e0, e0, a2);
             const float2 m2p = f2mul(pp, m2);
 #pragma unroll
-            for (int t = 0; t < 2; ++t) {
+            for (int t = 0; t < NT; ++t) {
               const float2 sv = t ? s1v : s0v;
               const float2 at = f2mul(sv, f2fma(sv, qq, m2p));
               float2 dt2 = f2add(d0, at);
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       for (int w = 0; w < kThreads / 32; ++w)
         for (int c = 0; c < 3; ++c) sd[c] += sLoss[w][c];
       a.losspart[chunk * kMaxCand + 0] = sd[2] + sd[0];
-      a.losspart[chunk * kMaxCand + 1] = sd[2] + sd[1];
+      a.losspart[chunk * kMaxCand + 1] = sd[2] + (NT == 2 ? sd[1] : 0.0);  // single: Y (never accepted)
       a.losspart[chunk * kMaxCand + 2] = sd[2];
     }
     return;
@@ -597,6 +598,13 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
     GMDS_TMA_SWITCH                                                                                       \
     count_launch();                                                                                       \
     check_launch("stress_tma_kernel (difference)");                                                       \
+  }
+#define GMDS_INSTANTIATE_TMA_DIFF1                                                                        \
+  void launch_pass_diff1_f32(const PassArgs& a, int Q, cudaStream_t st) {                                 \
+    constexpr int MODE = 5;                                                                               \
+    GMDS_TMA_SWITCH                                                                                       \
+    count_launch();                                                                                       \
+    check_launch("stress_tma_kernel (difference, first trial)");                                          \
   }
 #define GMDS_INSTANTIATE_TMA_FUSED                                                                        \
   void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st) {                                 \
