@@ -93,7 +93,8 @@ gmds_status gmds_pairwise_euclidean(const void* X, gmds_dtype xt, gmds_layout lx
 
 /* Device-resident variant for callers that keep X and D in HBM (bench,
  * the fit path).  dX row-major on the device; dD receives nnu full n x n
- * matrices (out_t) or, with packed != 0, nnu packed upper-triangle tile
+ * matrices (out_t; shard 0 zeroes the diagonal) or, with packed != 0, nnu
+ * packed upper-triangle tile
  * images (see gmds_packed_elems).  stream: a cudaStream_t or NULL.
  * shard/nshards split the tile list (multi-GPU, one process per GPU): a
  * shard writes only its own tiles. */

@@ -263,6 +263,14 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   a.nb_packed = ceil_div(n, kPT);
   a.out_stride = packed ? packed_elems(n) : n * n;
   a.flag = dflag;
+  if (!packed && !score && shard == 0) {
+    // full layout: the tiles write i != j only; the diagonal is D(i, i) = 0
+    // (pairwise_matrix starts from Matrix::Zero, metrics.cpp:210)
+    const size_t es = dtype_size(ot);
+    for (int v = 0; v < nnu; ++v)
+      GMDS_CUDA(cudaMemset2DAsync(static_cast<unsigned char*>(dD) + static_cast<size_t>(v) * a.out_stride * es,
+                                  static_cast<size_t>(n + 1) * es, 0, es, static_cast<size_t>(n), st));
+  }
   if (score) {
     spart.alloc(static_cast<size_t>(score_grid) * 2 * nnu);
     GMDS_CUDA(cudaMemsetAsync(spart.get(), 0, spart.n * sizeof(double), st));

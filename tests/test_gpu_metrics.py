@@ -432,3 +432,49 @@ def test_general_counting_kernel_vs_oracle(kind, monkeypatch):
     monkeypatch.setenv("GMDS_NO_GEN", "1")
     Dm = G.pairwise_gini(X, nus)
     assert np.max(np.abs(D - Dm)) <= 1e-12 * np.max(np.abs(Dm))
+
+
+@pytest.mark.parametrize("nu", [2.0, 2.5])
+def test_metric_shape_full_size_properties(nu):
+    # BASELINE's metric shape (n = 20000, p = 784, image-like): the whole matrix
+    # on the device (fp32, full layout), then size-independent checks --
+    # finite, non-negative, zero diagonal, symmetric, bit-identical on a repeat
+    # and across a 2-way tile sharding -- and 400 random pairs plus the
+    # duplicated-row pair against the oracle (fp32 output: 1e-6 max-normalised)
+    torch = pytest.importorskip("torch")
+    n, p = 20000, 784
+    X = image_like(n, p, 2024)
+    X[17] = X[19011]
+    dX = torch.from_numpy(X).cuda()
+    D = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    G.pairwise_gini_device(dX.data_ptr(), G.F32, n, p, [nu], G.F32, False, D.data_ptr())
+    torch.cuda.synchronize()
+    M = D.view(n, n)
+    assert bool(torch.isfinite(M).all()) and float(M.min()) >= 0.0
+    assert float(M.diagonal().abs().max()) == 0.0
+    scale = float(M.max())
+    rng = np.random.default_rng(int(nu * 10))
+    I = rng.integers(0, n, 400)
+    J = rng.integers(0, n, 400)
+    I, J = np.minimum(I, J), np.maximum(I, J)
+    keep = I < J
+    I, J = np.append(I[keep], 17), np.append(J[keep], 19011)
+    ti, tj = torch.from_numpy(I).cuda(), torch.from_numpy(J).cuda()
+    got = M[ti, tj].double().cpu().numpy()
+    assert np.array_equal(got, M[tj, ti].double().cpu().numpy())
+    ref = O.gini_pairs(X.astype(np.float64), I, J, nu)
+    assert np.max(np.abs(got - ref)) <= 1e-6 * scale
+    assert got[-1] == 0.0
+    R = torch.empty_like(D)
+    G.pairwise_gini_device(dX.data_ptr(), G.F32, n, p, [nu], G.F32, False, R.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(D, R)
+    del R
+    pe = G.packed_elems(n)
+    full = torch.zeros(pe, dtype=torch.float32, device="cuda")
+    G.pairwise_gini_device(dX.data_ptr(), G.F32, n, p, [nu], G.F32, True, full.data_ptr())
+    sh = torch.zeros_like(full)
+    for s in range(2):
+        G.pairwise_gini_device(dX.data_ptr(), G.F32, n, p, [nu], G.F32, True, sh.data_ptr(), s, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(full, sh)
