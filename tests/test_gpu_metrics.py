@@ -478,3 +478,22 @@ def test_metric_shape_full_size_properties(nu):
         G.pairwise_gini_device(dX.data_ptr(), G.F32, n, p, [nu], G.F32, True, sh.data_ptr(), s, 2)
     torch.cuda.synchronize()
     assert torch.equal(full, sh)
+
+
+def test_metric_shape_pinned_drop_in_matches_device():
+    # the bench's e2e call at the metric shape: host fp32 X -> pinned fp64 n x n,
+    # filled stripe by stripe while later tiles compute (launches capped at
+    # nbt/24 block rows); every entry written (NaN-prefilled destination) and
+    # equal bit for bit to the device-resident entry's full fp64 matrix
+    torch = pytest.importorskip("torch")
+    n, p = 20000, 784
+    X = image_like(n, p, 2026)
+    pinned = torch.full((1, n, n), float("nan"), dtype=torch.float64).pin_memory()
+    got = G.pairwise_gini(X, [2.0], out=pinned.numpy())
+    assert not bool(torch.isnan(pinned).any())
+    dX = torch.from_numpy(X).cuda()
+    D = torch.empty(n * n, dtype=torch.float64, device="cuda")
+    G.pairwise_gini_device(dX.data_ptr(), G.F32, n, p, [2.0], G.F64, False, D.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(pinned.view(-1).cuda(), D)
+    assert got[0][123, 123] == 0.0 and got[0][5, 19000] == got[0][19000, 5]
