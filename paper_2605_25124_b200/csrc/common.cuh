@@ -4,7 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <stdexcept>
+#include <utility>
 #include <string>
 
 #include "gmds.h"
@@ -47,6 +49,31 @@ gmds_status guard(F&& f) {
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch (stress loop): a kernel launched with
+// launch_pdl may be scheduled while its predecessor in the stream drains; it
+// must call pdl_wait() before touching memory (griddepcontrol.wait returns once
+// the predecessor grid has completed and its writes are visible).
+// GMDS_NO_PDL=1 launches them with ordinary stream order.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("GMDS_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
 
 inline size_t dtype_size(gmds_dtype t) { return t == GMDS_F32 ? 4 : 8; }
 

@@ -140,6 +140,7 @@ __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* _
                                      double* __restrict__ gpart, const int* __restrict__ halt,
                                      const double* __restrict__ losspart, int64_t nparts, int lstride,
                                      double* __restrict__ sums) {
+  pdl_wait();
   if (halt && *halt) return;
   if (blockIdx.x >= nb * kRedGroups) {  // the extra CTAs (device loop): the pass's loss sums
     gd_pass_sums(losspart, nparts, lstride, sums, static_cast<int>(blockIdx.x - nb * kRedGroups));
@@ -172,6 +173,7 @@ __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* _
 }
 __global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int Q, double* __restrict__ out,
                                const int* __restrict__ halt) {
+  pdl_wait();
   if (halt && *halt) return;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n * Q) return;
@@ -290,6 +292,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
                                double rel_tol, const double* __restrict__ pre, double precise_rel, int phase) {
+  pdl_wait();
   __shared__ double red[1024];
   __shared__ double sgsq;
   const GdState S = st[par];
@@ -475,12 +478,14 @@ static void reduce_rows_t(const TP* rowpart, const TP* colpart, const int64_t* s
                           const double* losspart, int64_t nparts, int lstride, double* sums) {
   if (gpart) {
     const bool extra = sums != nullptr && kPT * q >= 256;
-    reduce_groups_kernel<TP><<<static_cast<unsigned>(nb * kRedGroups + (extra ? 3 : 0)), kPT * q, 0, st>>>(
-        rowpart, colpart, strip_first, nb, q, gpart, halt, losspart, nparts, lstride, extra ? sums : nullptr);
+    launch_pdl(reduce_groups_kernel<TP>, dim3(static_cast<unsigned>(nb * kRedGroups + (extra ? 3 : 0))),
+               dim3(kPT * q), 0, st, rowpart, colpart, strip_first, nb, q, gpart, halt, losspart, nparts, lstride,
+               extra ? sums : nullptr);
     count_launch();
     check_launch("reduce_groups_kernel");
     if (!out) return;  // the caller adds the groups itself (gd_step_kernel)
-    combine_kernel<<<static_cast<unsigned>(ceil_div(n * q, 256)), 256, 0, st>>>(gpart, n, q, out, halt);
+    launch_pdl(combine_kernel, dim3(static_cast<unsigned>(ceil_div(n * q, 256))), dim3(256), 0, st, gpart, n, q, out,
+               halt);
     count_launch();
     check_launch("combine_kernel");
     return;
@@ -520,9 +525,9 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
                     int phase, cudaStream_t st) {
-  gd_step_kernel<<<nsq, 256, 0, st>>>(st2, par, losspart, nparts, stride, sqprev, nsq, sqnext, kind, sum_sq, sum, Y,
-                                      cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-                                      precise_rel, phase);
+  launch_pdl(gd_step_kernel, dim3(nsq), dim3(256), 0, st, st2, par, losspart, nparts, stride, sqprev, nsq, sqnext,
+             kind, sum_sq, sum, Y, cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
+             precise_rel, phase);
   count_launch();
   check_launch("gd_step_kernel");
 }

@@ -113,6 +113,7 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 // Armijo acceptance, so the next iteration usually needs no gradient pass).
 template <int Q, int MODE, int KIND>
 __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
+  pdl_wait();
   using namespace tma_detail;
   constexpr bool DIFF = (MODE == 3 || MODE == 5);  // loss differences: configurations are Y and the gradient
   constexpr int NT = (MODE == 5) ? 1 : 2;            // trial steps of a difference pass (5: the first only)
@@ -576,7 +577,7 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
     GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, MODE, KK>,                                        \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,                            \
                                    static_cast<int>(MODE ? kTmaSmemGrad : kTmaSmemLoss)));                 \
-    stress_tma_kernel<QQ, MODE, KK><<<g, kThreads, MODE ? kTmaSmemGrad : kTmaSmemLoss, st>>>(a);             \
+    launch_pdl(stress_tma_kernel<QQ, MODE, KK>, dim3(g), dim3(kThreads), MODE ? kTmaSmemGrad : kTmaSmemLoss, st, a); \
     break;
 #define GMDS_TMA_Q(QQ)                                                                                    \
   case QQ:                                                                                                \
