@@ -56,6 +56,9 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // the predecessor grid has completed and its writes are visible).
 // GMDS_NO_PDL=1 launches them with ordinary stream order.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// lets the next PDL launch in the stream be scheduled now (its pdl_wait still
+// waits for this grid to complete)
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 inline bool pdl_enabled() {
   static const bool on = std::getenv("GMDS_NO_PDL") == nullptr;
   return on;

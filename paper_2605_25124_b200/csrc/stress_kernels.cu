@@ -141,6 +141,7 @@ __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* _
                                      const double* __restrict__ losspart, int64_t nparts, int lstride,
                                      double* __restrict__ sums) {
   pdl_wait();
+  pdl_trigger();
   if (halt && *halt) return;
   if (blockIdx.x >= nb * kRedGroups) {  // the extra CTAs (device loop): the pass's loss sums
     gd_pass_sums(losspart, nparts, lstride, sums, static_cast<int>(blockIdx.x - nb * kRedGroups));
@@ -174,6 +175,7 @@ __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* _
 __global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int Q, double* __restrict__ out,
                                const int* __restrict__ halt) {
   pdl_wait();
+  pdl_trigger();
   if (halt && *halt) return;
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= n * Q) return;
@@ -293,6 +295,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
                                double rel_tol, const double* __restrict__ pre, double precise_rel, int phase) {
   pdl_wait();
+  pdl_trigger();
   __shared__ double red[1024];
   __shared__ double sgsq;
   const GdState S = st[par];

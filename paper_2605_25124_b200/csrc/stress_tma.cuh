@@ -114,6 +114,7 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 template <int Q, int MODE, int KIND>
 __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
   pdl_wait();
+  pdl_trigger();
   using namespace tma_detail;
   constexpr bool DIFF = (MODE == 3 || MODE == 5);  // loss differences: configurations are Y and the gradient
   constexpr int NT = (MODE == 5) ? 1 : 2;            // trial steps of a difference pass (5: the first only)
