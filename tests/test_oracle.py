@@ -190,3 +190,22 @@ def test_thread_count_bit_identity():
     d4 = R.pairwise_matrix(X, 1.8)
     R.set_max_threads(0)
     assert np.array_equal(d1, d4)
+
+
+def test_pairwise_properties():
+    # Size-independent properties the GPU tests also check at full size
+    # (symmetric, zero diagonal, non-negative, zero on duplicated rows), plus
+    # invariance under one permutation of the features applied to every row.
+    g = np.random.default_rng(7)
+    X = g.standard_normal((12, 9))
+    X[g.random(X.shape) < 0.3] = 0.0
+    X[5] = X[2]
+    perm = g.permutation(X.shape[1])
+    for nu in (1.5, 2.0, 3.0):
+        D = O.pairwise_matrix(X, nu)
+        assert np.array_equal(D, D.T)
+        assert np.all(np.diag(D) == 0.0)
+        assert np.all(D >= 0.0)
+        assert D[2, 5] == 0.0
+        Dp = O.pairwise_matrix(X[:, perm], nu)
+        np.testing.assert_allclose(Dp, D, rtol=1e-12, atol=1e-12 * D.max())
