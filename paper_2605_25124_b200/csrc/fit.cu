@@ -37,8 +37,9 @@ namespace gmds {
 
 namespace {
 
-// Blocks per CTA of a tiled pass (one block row): 4 at large n (measured best
-// at n = 20000), fewer when that would leave the pass short of ~8 CTAs per SM
+// Blocks per CTA of a tiled pass (one block row): 8 at large n (measured best
+// at n = 20000 with programmatic dependent launch: 2,730 it/s vs 2,706 at 4,
+// 2,595 at 16; profiles/r1_stress_chunk_sweep.txt), fewer when that would leave the pass short of ~8 CTAs per SM
 // (n = 5000: 820 blocks -> 1 per CTA); GMDS_STRESS_CHUNK overrides (tuning).
 int64_t chunk_blocks(int64_t nb) {
   if (const char* e = std::getenv("GMDS_STRESS_CHUNK")) {
@@ -46,7 +47,7 @@ int64_t chunk_blocks(int64_t nb) {
     if (c > 0) return c;
   }
   const int64_t nblk = nb * (nb + 1) / 2;
-  return std::max<int64_t>(1, std::min<int64_t>(4, nblk / (148 * 8)));
+  return std::max<int64_t>(1, std::min<int64_t>(8, nblk / (148 * 8)));
 }
 constexpr double kTiny = 1e-300;  // embed.cpp:13
 constexpr double kPreciseRel = 1e-6;  // fp32-storage loss changes below this are re-evaluated in fp64
