@@ -205,24 +205,59 @@ def reference_stress_rate(seconds_cap=8.0):
             f"({per_iter * 1e3:.1f} ms/iter), x{scale:.0f} pair-count extrapolation to n={N}", "cores": 1}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, rank, world):
+    """The reference's own CPU path, W untimed + K timed steps; each step is the same bounded
+    sample of the workload (a block of rows of the n x n matrix through the reference's
+    gen_gini_distance under its parallel_for), sized so the whole run ends in a few minutes."""
     if rank != 0:
         return
+    from oracle import ref_lib
+
     X = make_image_like(N, P)
-    rate, cores, kind, sample, dt = reference_rate(X)
+    steps, warm = max(1, args.steps), max(0, args.warmup)
+    per_step = min(8.0, max(1.0, 150.0 / (steps + warm)))
+    rate0, cores, kind, sample, _ = reference_rate(X, seconds_target=per_step)  # calibration (untimed)
+    rows = int(sample.split("rows 0..")[1].split(" ")[0]) + 1 if kind == "reference" else None
+    Xd = np.ascontiguousarray(X, dtype=np.float64)
+    pairs = sum(N - 1 - i for i in range(rows)) if rows else None
+    times = []
+    for k in range(warm + steps):
+        if rows:
+            t0 = time.perf_counter()
+            ref_lib.gini_rows(Xd, NU, 0, rows)
+            dt = time.perf_counter() - t0
+        else:
+            r, _, _, _, dt = reference_rate(X, seconds_target=per_step)
+        if k >= warm:
+            times.append(dt)
+    rate = (pairs / float(np.mean(times))) if rows else rate0
     srate = reference_stress_rate()
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "pairs/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "steps": steps, "warmup": warm, "ms_per_step": float(np.mean(times)) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "metric: n=20000 p=784 image-like fp32 (widened exactly to f64), nu=2, q=2",
                    "n": N, "p": P, "q": Q, "nu": NU},
-        "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": "pairs/s", "cores": cores, "cpu_model": cpu_model(), "kind": kind,
+                         "sample": sample + f"; {warm} untimed + {steps} timed repetitions of this sample"},
         "e2e": {"value": rate, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_times_s": [round(t, 3) for t in times],
     }
     if srate:
         line["stress_iters_per_sec"] = srate["iters_per_sec"]
         line["stress_sample"] = srate["sample"]
+        line["stress_cores"] = srate["cores"]
     print(json.dumps(line), flush=True)
 
 
@@ -383,17 +418,26 @@ def run_engine(args, rank, world, dist):
                "d2h_bytes_per_step": int(Dh.nbytes), "ms_per_step": float(np.mean(etimes)) * 1e3,
                "call": "gmds_pairwise_gini (pairwise_matrix drop-in, fp64 n x n out)"}
 
-    # ---- roofline of the dominant kernel (gini_tile_kernel: the whole distance step is this kernel
-    # plus a 12 KB LUT upload and two 4-byte flag copies)
+    # ---- roofline of the dominant kernel (gini_gmd_kernel: the whole distance step is this kernel
+    # plus a 12 KB LUT upload and two 4-byte flag copies).  Peak: the NOMINAL FP32/INT32 lane-op
+    # rate (SMs x 128 lanes x max SM clock; MEASURED_PEAKS.json has no ALU figure); the probe's
+    # measured rate is reported beside it
     alu = ctypes_double()
     G.lib().gmds_probe_alu(ctypes_ref(alu))
+    props = torch.cuda.get_device_properties(dev)
+    sm_max = clk.summary().get("sm_max_mhz") or 1965.0
+    alu_nominal = props.multi_processor_count * 128 * sm_max * 1e6
     ops_pair = ops_per_pair(P, 1)
     my_pairs = npairs  # all ranks together
     achieved = my_pairs * ops_pair / t_dist
     peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
     traffic_dist, traffic_stress = load_traffic()
-    stress_bytes = npairs * 4  # one read of the packed fp32 triangle per pass
-    pass_time = t_stress / max(1, spasses / max(1, world))
+    # stress: unit = one iteration; algorithmic bytes = one read of the packed fp32
+    # triangle (n(n-1)/2 x 4 B) per iteration, whatever the passes per iteration
+    bytes_iter = npairs * 4
+    ms_iter = 1e3 / iters_per_sec
+    ach_iter = bytes_iter / (ms_iter * 1e-3) / 1e9
     value = npairs / t_dist
     line = {
         "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
@@ -408,28 +452,39 @@ def run_engine(args, rank, world, dist):
                    "parallelism": f"pair tiles sharded over {world} GPU(s)"},
         "distance_ms": t_dist * 1e3,
         "distance_general_nu": {"nu": NU_GENERAL, "ms": t_general * 1e3, "pairs_per_s": npairs / t_general,
-                                "kernel": "gini_gen_kernel (midranks counted, one LUT pass)"},
+                                "kernel": "gini_gen_kernel (midranks counted, one LUT pass)",
+                                "alu_frac_of_nominal": npairs * ops_pair / t_general / alu_nominal},
         "stress_iters_per_sec": iters_per_sec,
         "stress_resolved_steps": resolved,
-        "stress_ms_per_iter": 1e3 / iters_per_sec,
+        "stress_ms_per_iter": ms_iter,
         "stress_passes_per_iter": spasses / max(1, siters),
         "gpu_launches": int(dist_launches + stress_launches),
-        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu.value / 1e12, "unit": "Tops/s",
-                     "frac": achieved / alu.value, "traffic": traffic_dist, "traffic_unit": "bytes/launch (ncu)",
+        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu_nominal / 1e12, "unit": "Tops/s",
+                     "frac": achieved / alu_nominal, "traffic": traffic_dist, "traffic_unit": "bytes/launch (ncu)",
                      "kernel": "gini_gmd_kernel (nu = 2: linear-weight path)", "ops_per_pair": ops_pair,
-                     "peak_source": "measured on this GPU by gmds_probe_alu (FFMA + IADD3/LOP3 lane-op rate)"},
-        "stress_roofline": {"bound": "hbm", "achieved": stress_bytes / pass_time / 1e9, "peak": peaks.get("hbm_gbs"),
-                            "unit": "GB/s", "frac": stress_bytes / pass_time / 1e9 / peaks.get("hbm_gbs", 6446.6),
-                            "traffic": traffic_stress, "kernel": "stress_tma_kernel fused (+ reductions, per pass)",
-                            "bytes_per_pass": stress_bytes},
+                     "peak_source": f"nominal: {props.multi_processor_count} SMs x 128 lanes x {sm_max:.0f} MHz "
+                                    "(MEASURED_PEAKS.json has no ALU figure)",
+                     "probe_peak": alu.value / 1e12, "frac_of_probe": achieved / alu.value,
+                     "probe_source": "gmds_probe_alu on this GPU (FFMA + IADD3/LOP3 lane-op rate)"},
+        "stress_roofline": {"bound": "hbm", "unit": "GB/s", "peak": hbm,
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if peaks.get("fallback") else ""),
+                            "bytes_per_iter": bytes_iter,
+                            "achieved": ach_iter, "frac": ach_iter / hbm,
+                            "iterations": f"1-{STRESS_ITERS} of the fit (the bench's stress step)",
+                            "traffic": traffic_stress, "kernel": "stress_tma_kernel fused (+ reductions, gd_step)"},
         "clocks": clk.summary(),
         "clocks_stress": clk2.summary(),
     }
+    if resolved:
+        a2 = bytes_iter / (resolved["ms_per_iter"] * 1e-3) / 1e9
+        line["stress_roofline"]["resolved"] = {"achieved": a2, "frac": a2 / hbm,
+                                               "iterations": resolved["iterations"]}
     if e2e:
         line["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, kind, sample, _ = reference_rate(X, seconds_target=10.0)
-        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": cores, "kind": kind, "sample": sample}
+        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": cores, "cpu_model": cpu_model(),
+                                "kind": kind, "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
 

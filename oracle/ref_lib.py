@@ -258,3 +258,61 @@ class RefRng:
 
     def normal(self):
         return load().ref_rng_normal(self._h)
+
+
+# ---- seeded-init iterate loops and sampled pairs (oracle/ref_seeded.cpp) ----
+SEEDED_PATH = os.path.join(HERE, "_ref", "libginimds_ref_seeded.so")
+_seeded = None
+
+
+def load_seeded():
+    """The reference's gradient_descent / smacof_iterate (embed.cpp:222-347) with a
+    caller-supplied start, and gen_gini_distance over a pair list.
+    None when oracle/_ref was not built."""
+    global _seeded
+    if _seeded is not None:
+        return _seeded
+    if not os.path.exists(SEEDED_PATH):
+        return None
+    L = ctypes.CDLL(SEEDED_PATH)
+    L.ref_seeded_last_error.restype = ctypes.c_char_p
+    _seeded = L
+    return L
+
+
+def _check_seeded(rc: int):
+    if rc != 0:
+        raise RefError(rc, _seeded.ref_seeded_last_error().decode())
+
+
+def seeded_fit(D, Y0, kind="kruskal", huber_delta=None, max_iters=300, rel_tol=1e-6):
+    """minimize_stress with Y0 in place of the classical init (embed.cpp:518-522)."""
+    L = load_seeded()
+    D = _f(D)
+    n = D.shape[0]
+    Y0 = _f(Y0)
+    q = Y0.shape[1]
+    coords = np.zeros((n, q), order="F")
+    cap = max_iters + 2
+    hist = np.zeros(cap)
+    hl, it, conv, loss = ctypes.c_int64(), ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    _check_seeded(L.ref_seeded_fit(_p(D), _i64(n), ctypes.c_int(q), ctypes.c_int(KIND[kind]),
+                                   ctypes.c_double(math.nan if huber_delta is None else huber_delta),
+                                   ctypes.c_int(max_iters), ctypes.c_double(rel_tol), _p(Y0), _p(coords), _p(hist),
+                                   _i64(cap), ctypes.byref(hl), ctypes.byref(it), ctypes.byref(conv),
+                                   ctypes.byref(loss)))
+    return dict(coords=np.ascontiguousarray(coords), stress_history=list(hist[: hl.value]), iterations=it.value,
+                converged=bool(conv.value), stress=loss.value)
+
+
+def gini_pairs(X, I, J, nu):
+    """gen_gini_distance(X[I[k]], X[J[k]], nu) for every k (the reference's own per-pair call)."""
+    L = load_seeded()
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    I = np.ascontiguousarray(I, dtype=np.int64)
+    J = np.ascontiguousarray(J, dtype=np.int64)
+    out = np.zeros(I.size)
+    ip = ctypes.POINTER(ctypes.c_int64)
+    _check_seeded(L.ref_gini_pairs(_p(X), _i64(X.shape[0]), _i64(X.shape[1]), ctypes.c_double(nu),
+                                   I.ctypes.data_as(ip), J.ctypes.data_as(ip), _i64(I.size), _p(out)))
+    return out

@@ -614,7 +614,10 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
     // change by ~1e-13, are then followed instead of stalling on equal fp32 sums.
     if (E.D->storage == GMDS_F32 && precise_ok) {
       const double tol = kPreciseRel * std::abs(f);
-      if (std::abs(E.loss_of(kind, gt.trial[0]) - f) <= tol && std::abs(E.loss_of(kind, gt.trial[1]) - f) <= tol) {
+      // ... and whenever a tested trial's Armijo margin is inside that resolution
+      const double f_step = E.loss_of(kind, gt.trial[slot_of[0]]), f_half = E.loss_of(kind, gt.trial[slot_of[1]]);
+      if ((std::abs(E.loss_of(kind, gt.trial[0]) - f) <= tol && std::abs(E.loss_of(kind, gt.trial[1]) - f) <= tol) ||
+          armijo_unresolved(f, step, grad_sq, f_step, f_half, tol)) {
         // Kruskal: the fp32 difference pass (the trial steps in slot order); other kinds:
         // fp64 arithmetic over the fp32 image
         std::vector<double> raws;

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
+
 #include "gmds.h"
 
 namespace gmds {
@@ -52,6 +54,32 @@ struct Steps {
   double v[kMaxCand];
   int n;
 };
+
+// fp32 storage: could the Armijo decision on fp32 sums differ from the reference's fp64
+// one (embed.cpp:242-250)?  The trials are tested in the reference's order (step, then
+// step / 2) and the first accepted wins, so the decision is unresolved when a TESTED
+// trial's loss lies within `tol` of its threshold f - 1e-4 s |g|^2 (f_step, f_half: the
+// losses at step and step / 2).  Host and device use the same rounding (no FMA).
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline bool armijo_unresolved(double f, double step, double gsq, double f_step, double f_half, double tol) {
+  for (int c = 0; c < 2; ++c) {
+#if defined(__CUDA_ARCH__)
+    const double sc = c == 0 ? step : __dmul_rn(step, 0.5);
+    const double thr = __dsub_rn(f, __dmul_rn(__dmul_rn(1e-4, sc), gsq));
+    const double fc = c == 0 ? f_step : f_half;
+    if (fabs(__dsub_rn(fc, thr)) <= tol) return true;
+#else
+    const double sc = c == 0 ? step : step * 0.5;
+    const double thr = f - 1e-4 * sc * gsq;
+    const double fc = c == 0 ? f_step : f_half;
+    if (std::fabs(fc - thr) <= tol) return true;
+#endif
+    if (fc <= thr) return false;  // accepted: later trials are not tested
+  }
+  return false;
+}
 
 void launch_stress_pass(const PassArgs& a, int q, bool grad, gmds_dtype storage, cudaStream_t st);
 // gpart (reduce_rows_scratch(nb, q) doubles): the two-level reduction; nullptr: one-level

@@ -351,9 +351,13 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   // phase 0, both trials within fp32 storage's resolution of f: Kruskal defers to a
   // difference pass (phase 1 decides); other kinds hand the iteration to the host
   const double tol = precise_rel * fabs(fY);
+  // ... or a tested trial whose Armijo margin is inside that resolution (the decision
+  // could flip against the reference's fp64 sums): the same deferral (armijo_unresolved)
   // (tiny mode: the pass was the gradient-only one, its losses are not trial losses: defer)
-  const bool unresolved = phase == 0 && precise_rel > 0.0 &&
-                          (S.tiny != 0 || (fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol));
+  const bool unresolved =
+      phase == 0 && precise_rel > 0.0 &&
+      (S.tiny != 0 || (fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
+       armijo_unresolved(fY, S.step, gsq, loss_of(S.pred == 0 ? t0 : t1), loss_of(S.pred == 0 ? t1 : t0), tol));
   if (unresolved && kind == kKruskal) {
     R.pending = 1;
     // tiny mode with the step first in slot order: the first trial is all the decision
