@@ -192,6 +192,34 @@ gmds_status gmds_minimize_stress(const gmds_dmat* D, int32_t q, const gmds_stres
 gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
                          const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
                          double* mean_stress, double* nu_star, double* coords, double* stress);
+/* The whole Embedding (embed.hpp:28-40) a tune entry returns: embed_distances'
+ * result (tune.cpp:20-33) -- classical_mds (eigenvalues, clamped stats) or
+ * minimize_stress with a default StressConfig (iterations, converged, history,
+ * huber_delta).  Caller buffers: coords n x q column-major, eigenvalues q (may
+ * be NULL), history history_cap entries (may be NULL). */
+typedef struct gmds_embedding {
+  double* coords;
+  double* eigenvalues;
+  double* history;
+  int64_t history_cap;
+  int64_t history_len;     /* out: full length of stress_history */
+  int32_t method;          /* out: gmds_method */
+  int32_t n_eigenvalues;   /* out: q for classical, 0 for stress fits (the reference leaves them empty) */
+  int32_t clamped_count;   /* out */
+  int32_t iterations;      /* out */
+  int32_t converged;       /* out */
+  double clamped_mass;     /* out */
+  double stress;           /* out */
+  double huber_delta;      /* out */
+} gmds_embedding;
+/* tune_nu with TuneReport::best_embedding in full (tune.cpp:132-133). */
+gmds_status gmds_tune_nu_ex(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                            const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
+                            double* mean_stress, double* nu_star, gmds_embedding* best);
+/* alternating_tune with AlternatingResult::embedding in full (tune.cpp:149). */
+gmds_status gmds_alternating_tune_ex(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                                     int32_t outer_iters, const double* grid, int32_t m, uint64_t seed,
+                                     double* nu_path, double* nu_star, gmds_embedding* emb);
 /* Fused nu-sweep scorer (the grid sweep of alternating_tune,
  * tune.cpp:153-157): ks[g] = kruskal_stress(Y, pairwise_matrix(X, gini(grid[g])))
  * for every grid value from ONE distance pass (one sort per pair serves every

@@ -320,6 +320,37 @@ NuGrid NuGrid::from_values(std::vector<double> values) {
   return NuGrid(std::move(values));
 }
 
+namespace {
+// Embedding by value from a gmds_embedding filled by the library (every field of embed.hpp:28-40)
+struct EmbeddingOut {
+  gmds_embedding raw{};
+  Embedding e;
+  std::vector<double> hist;
+  EmbeddingOut(Eigen::Index n, int p) {
+    e.coords.resize(n, p);
+    e.eigenvalues.resize(p);
+    hist.resize(302);  // embed_distances' default StressConfig: max_iters 300 -> <= 301 entries
+    raw.coords = e.coords.data();
+    raw.eigenvalues = e.eigenvalues.data();
+    raw.history = hist.data();
+    raw.history_cap = static_cast<int64_t>(hist.size());
+  }
+  Embedding finish() {
+    if (raw.n_eigenvalues != e.eigenvalues.size()) e.eigenvalues.resize(raw.n_eigenvalues);  // 0: stress fits
+    hist.resize(static_cast<std::size_t>(std::min<int64_t>(raw.history_len, raw.history_cap)));
+    e.stress_history = std::move(hist);
+    e.method = static_cast<EmbeddingMethod>(raw.method);
+    e.stress = raw.stress;
+    e.clamped_count = raw.clamped_count;
+    e.clamped_mass = raw.clamped_mass;
+    e.converged = raw.converged != 0;
+    e.iterations = raw.iterations;
+    e.huber_delta = raw.huber_delta;
+    return std::move(e);
+  }
+};
+}  // namespace
+
 TuneReport tune_nu(const Matrix& X, int p, const NuGrid& grid, int k_folds, EmbeddingMethod method,
                    std::uint64_t seed) {
   TuneReport r;
@@ -327,22 +358,22 @@ TuneReport tune_nu(const Matrix& X, int p, const NuGrid& grid, int k_folds, Embe
   r.mean_stress.resize(grid.size());
   r.folds = k_folds;
   r.seed = seed;
-  r.best_embedding.coords.resize(X.rows(), p);
-  check(gmds_tune_nu(X.data(), GMDS_F64, GMDS_COL_MAJOR, X.rows(), X.cols(), p, grid.values().data(),
-                     static_cast<int32_t>(grid.size()), k_folds, static_cast<int32_t>(method), seed,
-                     r.mean_stress.data(), &r.nu_star, r.best_embedding.coords.data(), &r.best_embedding.stress));
-  r.best_embedding.method = method;
+  EmbeddingOut out(X.rows(), p);
+  check(gmds_tune_nu_ex(X.data(), GMDS_F64, GMDS_COL_MAJOR, X.rows(), X.cols(), p, grid.values().data(),
+                        static_cast<int32_t>(grid.size()), k_folds, static_cast<int32_t>(method), seed,
+                        r.mean_stress.data(), &r.nu_star, &out.raw));
+  r.best_embedding = out.finish();
   return r;
 }
 
 AlternatingResult alternating_tune(const Matrix& X, int p, int outer_iters, const NuGrid& grid, std::uint64_t seed) {
   AlternatingResult r;
   r.nu_path.resize(static_cast<std::size_t>(std::max(outer_iters, 0)));
-  r.embedding.coords.resize(X.rows(), p);
-  check(gmds_alternating_tune(X.data(), GMDS_F64, GMDS_COL_MAJOR, X.rows(), X.cols(), p, outer_iters,
-                              grid.values().data(), static_cast<int32_t>(grid.size()), seed, r.nu_path.data(),
-                              &r.nu_star, r.embedding.coords.data(), &r.embedding.stress));
-  r.embedding.method = EmbeddingMethod::sammon;
+  EmbeddingOut out(X.rows(), p);
+  check(gmds_alternating_tune_ex(X.data(), GMDS_F64, GMDS_COL_MAJOR, X.rows(), X.cols(), p, outer_iters,
+                                 grid.values().data(), static_cast<int32_t>(grid.size()), seed, r.nu_path.data(),
+                                 &r.nu_star, &out.raw));
+  r.embedding = out.finish();
   return r;
 }
 

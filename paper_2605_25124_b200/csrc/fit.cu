@@ -1322,12 +1322,15 @@ gmds_status gmds_stress_partial(int32_t kind, const gmds_dmat* D, const double* 
     check_coords(D, coords, q, "stress_partial");
     if (nshards < 1 || shard < 0 || shard >= nshards) fail(GMDS_INVALID_CONFIG, "stress_partial: bad shard");
     if (q > 4) fail(GMDS_INVALID_INPUT, "stress_partial: sharded passes support q <= 4");
+    // resolve_params (embed.cpp:54-109): NaN / non-positive Huber delta, unknown kinds,
+    // all-zero D (Kruskal), non-positive off-diagonals (Sammon) are rejected as the reference does
+    const Resolved rp = (kind == kGuttman) ? Resolved{kGuttman} : resolve(D, kind, huber_delta, nullptr, "stress_partial");
     Stream st;
     EngineLease L = acquire_engine(D, q, st.s);
     Engine& E = *L;
     E.upload(coords, E.Y.get());
     // this shard's chunks: a contiguous, pair-balanced slice of the chunk list
-    *raw_loss = E.grad_raw_shard(kind, huber_delta, E.Y.get(), shard, nshards);
+    *raw_loss = E.grad_raw_shard(rp.kind, rp.delta, E.Y.get(), shard, nshards);
     E.download(E.graw.get(), raw_grad);
   });
 }

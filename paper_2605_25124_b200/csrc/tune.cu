@@ -89,19 +89,38 @@ std::vector<std::unique_ptr<gmds_dmat>> gini_multi(const void* dX, gmds_dtype xt
 }
 
 struct Emb {
-  std::vector<double> coords;
-  double stress = 0.0;
+  std::vector<double> coords, eigenvalues, history;
+  double stress = 0.0, clamped_mass = 0.0, huber_delta = 0.0;
+  int method = GMDS_M_CLASSICAL, clamped_count = 0, iterations = 0, converged = 1;
+
+  void put(gmds_embedding* out) const {  // Embedding by value, into the caller's buffers
+    std::memcpy(out->coords, coords.data(), coords.size() * sizeof(double));
+    out->n_eigenvalues = static_cast<int32_t>(eigenvalues.size());
+    if (out->eigenvalues)
+      std::memcpy(out->eigenvalues, eigenvalues.data(), eigenvalues.size() * sizeof(double));
+    out->history_len = static_cast<int64_t>(history.size());
+    if (out->history)
+      for (int64_t t = 0; t < std::min<int64_t>(out->history_len, out->history_cap); ++t)
+        out->history[t] = history[static_cast<size_t>(t)];
+    out->method = method;
+    out->clamped_count = clamped_count;
+    out->iterations = iterations;
+    out->converged = converged;
+    out->clamped_mass = clamped_mass;
+    out->stress = stress;
+    out->huber_delta = huber_delta;
+  }
 };
 
-// embed_distances (tune.cpp:20-33): classical, or minimize_stress with a default StressConfig.
+// embed_distances (tune.cpp:20-33): classical, or minimize_stress with a default StressConfig;
+// every Embedding field as the reference fills it (embed.cpp:415-460, 491-532)
 Emb embed(const gmds_dmat* D, int q, int method, uint64_t seed, cudaStream_t st) {
   Emb e;
+  e.method = method;
   e.coords.assign(static_cast<size_t>(D->n) * q, 0.0);
   if (method == GMDS_M_CLASSICAL) {
-    std::vector<double> ev(static_cast<size_t>(q));
-    int cc = 0;
-    double cm = 0.0;
-    classical_mds_dev(D, q, e.coords.data(), ev.data(), &cc, &cm, &e.stress, st);
+    e.eigenvalues.assign(static_cast<size_t>(q), 0.0);
+    classical_mds_dev(D, q, e.coords.data(), e.eigenvalues.data(), &e.clamped_count, &e.clamped_mass, &e.stress, st);
     return e;
   }
   gmds_stress_cfg cfg{};
@@ -111,10 +130,17 @@ Emb embed(const gmds_dmat* D, int q, int method, uint64_t seed, cudaStream_t st)
   cfg.max_iters = 300;
   cfg.rel_tol = 1e-6;
   cfg.seed = seed;
+  e.history.assign(static_cast<size_t>(cfg.max_iters) + 2, 0.0);
   gmds_fit_result r{};
   r.coords = e.coords.data();
+  r.history = e.history.data();
+  r.history_cap = static_cast<int64_t>(e.history.size());
   minimize_stress_dev(D, q, cfg, nullptr, &r, st, nullptr);
+  e.history.resize(static_cast<size_t>(std::min<int64_t>(r.history_len, r.history_cap)));
   e.stress = r.stress;
+  e.iterations = r.iterations;
+  e.converged = r.converged;
+  e.huber_delta = r.huber_delta;
   return e;
 }
 
@@ -190,10 +216,11 @@ using namespace gmds;
 
 extern "C" {
 
-gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
-                         const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
-                         double* mean_stress, double* nu_star, double* coords, double* stress) {
+gmds_status gmds_tune_nu_ex(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                            const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
+                            double* mean_stress, double* nu_star, gmds_embedding* best_emb) {
   return guard([&] {
+    if (!best_emb || !best_emb->coords) fail(GMDS_INVALID_INPUT, "tune_nu: null embedding buffers");
     check_grid(grid, m);
     if (k_folds < 1) fail(GMDS_INVALID_CONFIG, "tune_nu: k_folds must be >= 1");
     if (n < k_folds) fail(GMDS_INVALID_CONFIG, "tune_nu: more folds than rows");
@@ -255,10 +282,18 @@ gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n
     std::iota(all.begin(), all.end(), 0);
     DevBuf<double> dX = upload_f64(rows_of(X, xt, lx, n, p, all), st.s);
     const auto Dfull = gini_multi(dX.get(), GMDS_F64, n, p, nu_star, 1, st.s);
-    const Emb e = embed(Dfull[0].get(), q, method, seed, st.s);
-    std::memcpy(coords, e.coords.data(), e.coords.size() * sizeof(double));
-    *stress = e.stress;
+    embed(Dfull[0].get(), q, method, seed, st.s).put(best_emb);
   });
+}
+
+gmds_status gmds_tune_nu(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                         const double* grid, int32_t m, int32_t k_folds, int32_t method, uint64_t seed,
+                         double* mean_stress, double* nu_star, double* coords, double* stress) {
+  gmds_embedding e{};
+  e.coords = coords;
+  const gmds_status s = gmds_tune_nu_ex(X, xt, lx, n, p, q, grid, m, k_folds, method, seed, mean_stress, nu_star, &e);
+  if (s == GMDS_OK) *stress = e.stress;
+  return s;
 }
 
 gmds_status gmds_nu_sweep_kruskal(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
@@ -278,10 +313,11 @@ gmds_status gmds_nu_sweep_kruskal(const void* X, gmds_dtype xt, gmds_layout lx, 
   });
 }
 
-gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
-                                  int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
-                                  double* nu_star, double* coords, double* stress) {
+gmds_status gmds_alternating_tune_ex(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                                     int32_t outer_iters, const double* grid, int32_t m, uint64_t seed,
+                                     double* nu_path, double* nu_star, gmds_embedding* out) {
   return guard([&] {
+    if (!out || !out->coords) fail(GMDS_INVALID_INPUT, "alternating_tune: null embedding buffers");
     if (outer_iters < 1) fail(GMDS_INVALID_CONFIG, "alternating_tune: need at least one outer iteration");
     check_grid(grid, m);
     if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
@@ -307,9 +343,19 @@ gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, 
       nu_path[t] = nu;
     }
     *nu_star = nu;
-    std::memcpy(coords, emb.coords.data(), emb.coords.size() * sizeof(double));
-    *stress = emb.stress;
+    emb.put(out);
   });
+}
+
+gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, int32_t q,
+                                  int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
+                                  double* nu_star, double* coords, double* stress) {
+  gmds_embedding e{};
+  e.coords = coords;
+  const gmds_status s =
+      gmds_alternating_tune_ex(X, xt, lx, n, p, q, outer_iters, grid, m, seed, nu_path, nu_star, &e);
+  if (s == GMDS_OK) *stress = e.stress;
+  return s;
 }
 
 }  // extern "C"

@@ -90,15 +90,22 @@ def minimize_stress_sharded(partial: Callable[[str, np.ndarray], tuple[float, np
                             rel_tol: float = 1e-6) -> dict:
     """Reference control flow over all-reduced partial passes.
 
-    partial(kind, Y) -> (raw_loss, raw_grad) over this rank's tiles (kind
+    partial(kind, Y[, huber_delta]) -> (raw_loss, raw_grad) over this rank's tiles (kind
     "guttman" for the SMACOF transform); allreduce_sum sums a flat float64
     vector across ranks.  stats = (sum D^2, sum D, min D, max D).
     """
     sum_sq, sum_d = float(stats[0]), float(stats[1])
+    if kind == "huber" and huber_delta is None:
+        # the reference's auto mode (embed.cpp:499-515) fits three deltas from the median and keeps the
+        # lowest Kruskal stress; the sharded driver takes an explicit delta (resolved by the caller)
+        raise ValueError("minimize_stress_sharded: huber needs an explicit huber_delta (auto mode is "
+                         "minimize_stress's)")
+    if kind == "huber" and not (huber_delta > 0.0):
+        raise ValueError("minimize_stress_sharded: huber_delta must be > 0")
     Y = np.array(Y0, dtype=np.float64, copy=True)
 
     def full(kd, Yc):
-        raw, g = partial(kd, Yc)
+        raw, g = partial(kd, Yc, huber_delta) if kd == "huber" else partial(kd, Yc)
         v = allreduce_sum(np.concatenate([[raw], np.asarray(g, dtype=np.float64).ravel()]))
         return float(v[0]), v[1:].reshape(Yc.shape)
 
@@ -178,11 +185,12 @@ def gpu_partial(dmat, rank: int, world: int, huber_delta=None):
 
     codes = {"kruskal": 0, "huber": 1, "sammon": 2, "smacof": 3, "guttman": 4}
 
-    def partial(kind, Y):
+    def partial(kind, Y, delta=None):
         Yf = np.asfortranarray(Y, dtype=np.float64)
         g = np.zeros_like(Yf, order="F")
         raw = ctypes.c_double()
-        hd = ctypes.c_double(math.nan if huber_delta is None else float(huber_delta))
+        delta = huber_delta if delta is None else delta
+        hd = ctypes.c_double(math.nan if delta is None else float(delta))
         G._check(G.lib().gmds_stress_partial(G._i32(codes[kind]), dmat.handle, G._p(Yf), G._i32(Yf.shape[1]), hd,
                                              G._i32(rank), G._i32(world), ctypes.byref(raw), G._p(g)))
         return raw.value, np.ascontiguousarray(g)

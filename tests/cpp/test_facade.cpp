@@ -196,6 +196,27 @@ static void tune_tests() {
   sam.loss = StressKind::sammon;
   const Embedding fit = minimize_stress(pairwise_matrix(X2, MetricSpec::gini(2.0)), 2, sam);
   CHECK(alt.nu_star == 2.0 && approx(alt.embedding.stress, fit.stress, 1e-12));
+  // the returned embeddings carry every Embedding field of the direct pipeline
+  // (tools/main.cpp's embedding_diagnostics reads them for tune_report.json)
+  CHECK(r2.best_embedding.method == EmbeddingMethod::classical);
+  CHECK(r2.best_embedding.eigenvalues.size() == 2 && direct.eigenvalues.size() == 2);
+  for (int k = 0; k < 2; ++k) CHECK(approx(r2.best_embedding.eigenvalues(k), direct.eigenvalues(k), 1e-12));
+  CHECK(r2.best_embedding.clamped_count == direct.clamped_count);
+  CHECK(approx(r2.best_embedding.clamped_mass, direct.clamped_mass, 1e-12));
+  CHECK(r2.best_embedding.converged == direct.converged && r2.best_embedding.iterations == direct.iterations);
+  CHECK(alt.embedding.method == EmbeddingMethod::sammon && alt.embedding.eigenvalues.size() == 0);
+  CHECK(alt.embedding.iterations == fit.iterations && alt.embedding.converged == fit.converged);
+  CHECK(alt.embedding.stress_history.size() == fit.stress_history.size() && fit.stress_history.size() > 1);
+  for (std::size_t t = 0; t < fit.stress_history.size(); ++t)
+    CHECK(approx(alt.embedding.stress_history[t], fit.stress_history[t], 1e-12));
+  const TuneReport r3 = tune_nu(X2, 2, NuGrid::linspace(2.0, 2.0, 1), 1, EmbeddingMethod::kruskal, 9);
+  StressConfig kr;
+  kr.loss = StressKind::kruskal;
+  const Embedding kfit = minimize_stress(pairwise_matrix(X2, MetricSpec::gini(2.0)), 2, kr);
+  CHECK(r3.best_embedding.method == EmbeddingMethod::kruskal && r3.best_embedding.eigenvalues.size() == 0);
+  CHECK(r3.best_embedding.iterations == kfit.iterations && r3.best_embedding.converged == kfit.converged);
+  CHECK(r3.best_embedding.stress_history.size() == kfit.stress_history.size());
+  CHECK(approx(r3.best_embedding.stress, kfit.stress, 1e-12));
   CHECK_THROWS_AS(alternating_tune(X2, 2, 0, NuGrid::linspace(2.0, 2.0, 1), 1), InvalidConfig);
 }
 
