@@ -230,6 +230,53 @@ gmds_status gmds_alternating_tune(const void* X, gmds_dtype xt, gmds_layout lx, 
                                   int32_t outer_iters, const double* grid, int32_t m, uint64_t seed, double* nu_path,
                                   double* nu_star, double* coords, double* stress);
 
+/* ---- multi-GPU: one rank per GPU ----
+ * The reference's only parallelism is std::thread parallel_for
+ * (parallel.hpp:24-59) over rows (metrics.cpp:213-219), (nu, fold) cells
+ * (tune.cpp:101-113) and the grid sweep (tune.cpp:154-157); its stress loop
+ * is serial (embed.cpp:222-272).  Here the rows of D (its packed blocks) and
+ * the nu grid are split across ranks, and the stress iteration is one
+ * all-reduce of [gradient | loss sums] per pass, enqueued on the rank's stream
+ * (NCCL over NVLink / NVSwitch). */
+typedef struct gmds_comm gmds_comm;
+#define GMDS_COMM_ID_BYTES 128
+/* A new NCCL unique id (rank 0 creates it; the caller's plumbing shares it). */
+gmds_status gmds_comm_unique_id(unsigned char* id);
+/* Rank `rank` of `nranks` on the current device (gmds_set_device first). */
+gmds_status gmds_comm_init_nccl(const unsigned char* id, int32_t nranks, int32_t rank, gmds_comm** out);
+/* nranks ranks in ONE process on the current device (tests with fewer GPUs
+ * than ranks): comms[r] must be driven by its own host thread; collectives are
+ * one reduction kernel over every rank's buffer in rank order. */
+gmds_status gmds_comm_init_local(int32_t nranks, gmds_comm** comms);
+int32_t gmds_comm_rank(const gmds_comm* c);
+int32_t gmds_comm_size(const gmds_comm* c);
+/* In-place all-reduce of a device buffer (op 0 sum, 1 min, 2 max); blocking. */
+gmds_status gmds_comm_allreduce_device(gmds_comm* c, double* dbuf, int64_t count, int32_t op, void* stream);
+void gmds_comm_free(gmds_comm* c);
+
+/* This rank's share of pairwise_matrix(X, gini(nu)) kept on the device: the
+ * contiguous range [nblk*r/N, nblk*(r+1)/N) of the packed 128 x 128 blocks
+ * (row-major upper triangle), computed here and nowhere else; the per-fit
+ * constants (sum D^2, sum D, min, max) are all-reduced over the group.  dX:
+ * the full row-major X on this device.  Usable by gmds_minimize_stress_sharded
+ * and gmds_dmat_stats only. */
+gmds_status gmds_dmat_gini_sharded(gmds_comm* comm, const void* dX, gmds_dtype xt, int64_t n, int64_t p, double nu,
+                                   gmds_dtype storage, gmds_dmat** out);
+/* minimize_stress (embed.cpp:491-532) over a row-sharded D: every rank runs
+ * the device-resident loop on its blocks and all-reduces [gradient | loss sums]
+ * once per pass; every rank returns the same embedding.  fp32 storage, q <= 4,
+ * seeded start Y0 (n x q column-major, required: the classical init needs all of
+ * D), Huber with an explicit delta. */
+gmds_status gmds_minimize_stress_sharded(gmds_comm* comm, const gmds_dmat* D, int32_t q, const gmds_stress_cfg* cfg,
+                                         const double* Y0, gmds_fit_result* res);
+/* The fused nu-sweep scorer over a nu grid split across ranks (tune.cpp:153-157
+ * with the grid shared out as replicas): each rank scores its contiguous block of
+ * grid values from one distance pass, the scores are all-reduced, and every rank
+ * returns all m values.  X, Y host as gmds_nu_sweep_kruskal. */
+gmds_status gmds_nu_sweep_kruskal_sharded(gmds_comm* comm, const void* X, gmds_dtype xt, gmds_layout lx, int64_t n,
+                                          int64_t p, const double* Y, int32_t q, const double* grid, int32_t m,
+                                          double* ks);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,5 +34,14 @@ struct gmds_dmat {
   mutable std::vector<bool> busy;
   // dense row-major fp64 copy for the single-CTA small-n fit (n <= 1024), built once
   mutable std::shared_ptr<gmds::DevBuf<double>> dense;
-  const void* ptr() const { return shared ? static_cast<const void*>(shared->get() + offset) : buf.get(); }
+  // row-sharded (gmds_dmat_gini_sharded): only packed blocks [blk_lo, blk_hi) are held, in a
+  // compact buffer; ptr() is the (virtual) base of the full packed image, so block b lives at
+  // ptr() + b * kPT^2 elements for b in range
+  int64_t blk_lo = 0, blk_hi = -1;
+  bool sharded() const { return blk_hi >= 0; }
+  const void* ptr() const {
+    if (sharded())
+      return buf.get() - static_cast<size_t>(blk_lo) * gmds::kPT * gmds::kPT * gmds::dtype_size(storage);
+    return shared ? static_cast<const void*>(shared->get() + offset) : buf.get();
+  }
 };

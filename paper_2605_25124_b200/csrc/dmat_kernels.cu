@@ -57,11 +57,11 @@ __global__ void unpack_kernel(const TD* __restrict__ packed, int64_t n, int64_t 
 
 // Per-CTA partials over valid entries: [sum D^2, sum D, min D, max D].
 template <typename TD>
-__global__ void stats_kernel(const TD* __restrict__ packed, int64_t n, int64_t nb, int64_t total,
+__global__ void stats_kernel(const TD* __restrict__ packed, int64_t n, int64_t nb, int64_t ebeg, int64_t total,
                              double* __restrict__ part) {
   double s2 = 0.0, s1 = 0.0, mn = INFINITY, mx = -INFINITY;
-  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-  const int64_t e0 = blockIdx.x * per, e1 = min(total, e0 + per);
+  const int64_t per = (total - ebeg + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = ebeg + blockIdx.x * per, e1 = min(total, e0 + per);
   for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     int64_t i, j;
     unpack_index(e, nb, i, j);
@@ -161,14 +161,17 @@ void unpack_full(const void* dpacked, gmds_dtype storage, int64_t n, double* dfu
   check_launch("unpack_kernel");
 }
 
-DStats packed_stats(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st) {
-  const int64_t nb = ceil_div(n, kPT), total = packed_elems(n);
-  const int blocks = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(1, ceil_div(total, 4096))));
+DStats packed_stats(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st, int64_t blk_lo,
+                    int64_t blk_hi) {
+  const int64_t nb = ceil_div(n, kPT);
+  const int64_t ebeg = blk_lo * kPT * kPT;
+  const int64_t total = blk_hi < 0 ? packed_elems(n) : blk_hi * kPT * kPT;  // elements [ebeg, total)
+  const int blocks = static_cast<int>(std::min<int64_t>(1024, std::max<int64_t>(1, ceil_div(total - ebeg, 4096))));
   DevBuf<double> part(static_cast<size_t>(blocks) * 4);
   if (storage == GMDS_F32)
-    stats_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dpacked), n, nb, total, part.get());
+    stats_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(dpacked), n, nb, ebeg, total, part.get());
   else
-    stats_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dpacked), n, nb, total, part.get());
+    stats_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(dpacked), n, nb, ebeg, total, part.get());
   count_launch();
   check_launch("stats_kernel");
   std::vector<double> h(static_cast<size_t>(blocks) * 4);

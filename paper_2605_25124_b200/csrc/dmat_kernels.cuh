@@ -17,7 +17,9 @@ struct DStats {
 
 void pack_full(const double* dfull, int64_t n, gmds_dtype storage, void* dpacked, cudaStream_t st);
 void unpack_full(const void* dpacked, gmds_dtype storage, int64_t n, double* dfull, bool square, cudaStream_t st);
-DStats packed_stats(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st);
+// statistics over packed blocks [blk_lo, blk_hi) (blk_hi < 0: all)
+DStats packed_stats(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st, int64_t blk_lo = 0,
+                    int64_t blk_hi = -1);
 double packed_median(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st);
 void double_center_dev(double* dS, int64_t n, cudaStream_t st);
 

@@ -35,8 +35,6 @@
 
 namespace gmds {
 
-namespace {
-
 // Blocks per CTA of a tiled pass (one block row): 8 at large n (measured best
 // at n = 20000 with programmatic dependent launch: 2,730 it/s vs 2,706 at 4,
 // 2,595 at 16; profiles/r1_stress_chunk_sweep.txt), fewer when that would leave the pass short of ~8 CTAs per SM
@@ -49,6 +47,38 @@ int64_t chunk_blocks(int64_t nb) {
   const int64_t nblk = nb * (nb + 1) / 2;
   return std::max<int64_t>(1, std::min<int64_t>(8, nblk / (148 * 8)));
 }
+
+namespace {
+// (I, J0) of every chunk, in packed order
+void chunk_list(int64_t nb, int64_t len, std::vector<int64_t>& cI, std::vector<int64_t>& cJ) {
+  for (int64_t I = 0; I < nb; ++I)
+    for (int64_t J0 = I; J0 < nb; J0 += len) {
+      cI.push_back(I);
+      cJ.push_back(J0);
+    }
+}
+int64_t blk_of(int64_t I, int64_t J, int64_t nb) { return I * nb - (I * (I - 1)) / 2 + (J - I); }
+}  // namespace
+
+// Rank `rank`'s packed blocks [blk_lo, blk_hi): the chunks whose preceding block count
+// reaches nblk * rank / size start the share (the split grad_raw_shard uses).
+void shard_blocks(int64_t n, int rank, int size, int64_t& blk_lo, int64_t& blk_hi) {
+  const int64_t nb = ceil_div(n, kPT), nblk = nb * (nb + 1) / 2;
+  std::vector<int64_t> cI, cJ;
+  chunk_list(nb, chunk_blocks(nb), cI, cJ);
+  auto edge = [&](int r) {
+    if (r >= size) return nblk;
+    for (size_t c = 0; c < cI.size(); ++c) {
+      const int64_t before = blk_of(cI[c], cJ[c], nb);
+      if (before * size >= nblk * r) return before;
+    }
+    return nblk;
+  };
+  blk_lo = edge(rank);
+  blk_hi = edge(rank + 1);
+}
+
+namespace {
 constexpr double kTiny = 1e-300;  // embed.cpp:13
 constexpr double kPreciseRel = 1e-6;  // fp32-storage loss changes below this are re-evaluated in fp64
 
@@ -72,36 +102,50 @@ cusolverDnHandle_t solver_handle(cudaStream_t st) {
 }  // namespace
 
 // ---------------------------------------------------------------------------
-Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st(st_) {
+Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_, Comm* comm_) : D(Dm), q(q_), st(st_), comm(comm_) {
   n = D->n;
   nb = ceil_div(n, kPT);
   Q = padded_q(q);
   rows_mode = (q > 4);
+  if (D->sharded() && (rows_mode || !comm)) fail(GMDS_INVALID_INPUT, "row-sharded distance matrix: q <= 4 and its comm");
   if (!rows_mode) {
     chunk_len = chunk_blocks(nb);
-    std::vector<int64_t> cI, cJ, sf;
-    for (int64_t I = 0; I < nb; ++I) {
-      sf.push_back(static_cast<int64_t>(cI.size()));
-      for (int64_t J0 = I; J0 < nb; J0 += chunk_len) {
-        cI.push_back(I);
-        cJ.push_back(J0);
-      }
+    std::vector<int64_t> aI, aJ, cI, cJ, sf;
+    chunk_list(nb, chunk_len, aI, aJ);
+    for (size_t c = 0; c < aI.size(); ++c) {  // row-sharded: this rank's chunks only
+      const int64_t b = blk_of(aI[c], aJ[c], nb);
+      if (D->sharded() && (b < D->blk_lo || b >= D->blk_hi)) continue;
+      cI.push_back(aI[c]);
+      cJ.push_back(aJ[c]);
     }
-    sf.push_back(static_cast<int64_t>(cI.size()));
+    for (int64_t I = 0, c = 0; I <= nb; ++I) {  // strip I's chunks: [sf[I], sf[I + 1])
+      while (c < static_cast<int64_t>(cI.size()) && cI[c] < I) ++c;
+      sf.push_back(c);
+    }
     nchunks = static_cast<int64_t>(cI.size());
-    chunk_I.alloc(cI.size());
-    chunk_J0.alloc(cJ.size());
+    chunk_I.alloc(std::max<size_t>(1, cI.size()));
+    chunk_J0.alloc(std::max<size_t>(1, cJ.size()));
     strip_first.alloc(sf.size());
-    GMDS_CUDA(cudaMemcpyAsync(chunk_I.get(), cI.data(), cI.size() * 8, cudaMemcpyHostToDevice, st));
-    GMDS_CUDA(cudaMemcpyAsync(chunk_J0.get(), cJ.data(), cJ.size() * 8, cudaMemcpyHostToDevice, st));
+    if (nchunks) {
+      GMDS_CUDA(cudaMemcpyAsync(chunk_I.get(), cI.data(), cI.size() * 8, cudaMemcpyHostToDevice, st));
+      GMDS_CUDA(cudaMemcpyAsync(chunk_J0.get(), cJ.data(), cJ.size() * 8, cudaMemcpyHostToDevice, st));
+    }
     GMDS_CUDA(cudaMemcpyAsync(strip_first.get(), sf.data(), sf.size() * 8, cudaMemcpyHostToDevice, st));
     const int64_t nblk = nb * (nb + 1) / 2;
-    stride_row = nchunks * kPT * Q;
+    stride_row = std::max<int64_t>(1, nchunks) * kPT * Q;
     stride_col = nblk * kPT * Q;
     rowpart.alloc(static_cast<size_t>(stride_row));
     colpart.alloc(static_cast<size_t>(stride_col));
     gpart.alloc(reduce_rows_scratch(nb, Q));
-    losspart.alloc(static_cast<size_t>(nchunks * kMaxCand));
+    losspart.alloc(static_cast<size_t>(std::max<int64_t>(1, nchunks) * kMaxCand));
+    if (D->sharded()) {  // foreign blocks' column partials are never written: zero once
+      GMDS_CUDA(cudaMemsetAsync(colpart.get(), 0, colpart.n * sizeof(double), st));
+      GMDS_CUDA(cudaMemsetAsync(rowpart.get(), 0, rowpart.n * sizeof(double), st));
+      GMDS_CUDA(cudaMemsetAsync(losspart.get(), 0, losspart.n * sizeof(double), st));
+      xred.alloc(static_cast<size_t>(n * Q + 8));
+      dsum.alloc(4);
+      rawy.alloc(1);
+    }
   } else {
     nchunks = n;
     rowpart.alloc(static_cast<size_t>(n * Q));
@@ -113,6 +157,10 @@ Engine::Engine(const gmds_dmat* Dm, int q_, cudaStream_t st_) : D(Dm), q(q_), st
   scal.alloc(8);
   sqpart.alloc(kSqBlocks);
   GMDS_CUDA(cudaStreamSynchronize(st));
+}
+
+void Engine::allreduce(double* d, size_t count) {
+  if (comm) comm->allreduce(d, count, RedOp::kSum, st);
 }
 
 void Engine::upload(const double* coords_colmajor, double* dst) {
@@ -158,6 +206,7 @@ std::vector<double> Engine::loss_raw(int kind, double delta, const double* const
   a.ncand = nc;
   launch_stress_pass(a, Q, false, D->storage, st);
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
+  allreduce(scal.get(), static_cast<size_t>(nc));
   std::vector<double> out(static_cast<size_t>(nc));
   GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
@@ -171,6 +220,7 @@ std::vector<double> Engine::loss_raw_precise(int kind, double delta, const doubl
   a.ncand = nc;
   launch_pass_precise(a, Q, st);
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, nc, scal.get(), st);
+  allreduce(scal.get(), static_cast<size_t>(nc));
   std::vector<double> out(static_cast<size_t>(nc));
   GMDS_CUDA(cudaMemcpyAsync(out.data(), scal.get(), nc * sizeof(double), cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
@@ -187,6 +237,7 @@ std::vector<double> Engine::loss_diff(int kind, double s0, double s1) {
   a.dstep[1] = s1;
   launch_pass_diff_f32(a, Q, st);
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 3, scal.get(), st);
+  allreduce(scal.get(), 3);
   double h[3];
   GMDS_CUDA(cudaMemcpyAsync(h, scal.get(), sizeof h, cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
@@ -205,6 +256,12 @@ double Engine::grad_raw(int kind, double delta, const double* Yd) {
   else
     GMDS_CUDA(cudaMemcpyAsync(graw.get(), rowpart.get(), sizeof(double) * n * Q, cudaMemcpyDeviceToDevice, st));
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 1, scal.get(), st);
+  if (comm) {  // row-sharded: [gradient | raw loss] summed over the ranks
+    double* bufs[2] = {graw.get(), scal.get()};
+    const size_t counts[2] = {static_cast<size_t>(n * Q), 1};
+    comm->allreduce_group(bufs, counts, 2, st);
+    GMDS_CUDA(cudaMemcpyAsync(rawy.get(), scal.get(), sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
   double out = 0.0;
   GMDS_CUDA(cudaMemcpyAsync(&out, scal.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
   GMDS_CUDA(cudaStreamSynchronize(st));
@@ -254,6 +311,7 @@ double Engine::grad_raw_shard(int kind, double delta, const double* Yd, int shar
 }
 
 Engine::GradTrials Engine::grad_and_trials(int kind, double delta, double s0, double s1) {
+  if (comm) fail(GMDS_INVALID_CONFIG, "row-sharded fits run on fp32 storage");
   if (q > 64) fail(GMDS_INVALID_INPUT, "stress gradient: embedding dimension above 64 is not supported");
   PassArgs a = args(kind, delta);
   a.Y[0] = Y.get();
@@ -289,7 +347,8 @@ Engine::GradTrials Engine::grad_and_trials(int kind, double delta, double s0, do
 Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, double s1) {
   if (!gnext.get()) gnext.alloc(static_cast<size_t>(n * Q));
   const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
-                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sqpart.get(), scal.get(), st);
+                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sqpart.get(), scal.get(), st,
+                                     comm ? rawy.get() : nullptr);
   PassArgs b = args(kind, delta);
   b.Y[0] = cand[0].get();
   b.Y[1] = cand[1].get();
@@ -297,6 +356,13 @@ Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, doubl
   launch_pass_fused_f32(b, Q, st);
   launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, gnext.get(), st, gpart.get(), nullptr, f32parts());
   launch_sum_parts(losspart.get(), nchunks, kMaxCand, 2, scal.get() + 1, st);
+  if (comm) {  // row-sharded: [gradient at cand0 | both trial losses] over the ranks
+    double* bufs[2] = {gnext.get(), scal.get() + 1};
+    const size_t counts[2] = {static_cast<size_t>(n * Q), 2};
+    comm->allreduce_group(bufs, counts, 2, st);
+    // the raw loss at cand0: the next finish's loss at Y when that trial is accepted
+    GMDS_CUDA(cudaMemcpyAsync(rawy.get(), scal.get() + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
   double h[3];
   std::vector<double> sq(static_cast<size_t>(nsq));
   GMDS_CUDA(cudaMemcpyAsync(h, scal.get(), sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -323,16 +389,25 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   const double s0 = pred == 0 ? step : step * 0.5, s1 = pred == 0 ? step * 0.5 : step;
   // prime: the trial pair of iteration `it` and its fused pass (as fused_trials, without the round trip)
   const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
-                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sq2.get(), scal.get(), st);
+                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sq2.get(), scal.get(), st,
+                                     comm ? rawy.get() : nullptr);
   PassArgs b = args(kind, delta);
   b.Y[0] = cand[0].get();
   b.Y[1] = cand[1].get();
   b.ncand = 2;
   launch_pass_fused_f32(b, Q, st);
   double* pre = scal.get() + 5;  // the pass's loss sums (reduction launch's extra CTA; q >= 2)
-  const bool have_pre = kPT * Q >= 256;
+  const bool have_pre = kPT * Q >= 256 && !comm;
+  // row-sharded: this rank's [gradient | trial loss sums] -> xred, all-reduced (one collective per pass)
+  double* xr = comm ? xred.get() : nullptr;
+  auto collect = [&](const int* halt) {
+    if (!comm) return;
+    launch_shard_collect(gpart.get(), n, Q, losspart.get(), nchunks, kMaxCand, xr, halt, st);
+    comm->allreduce(xr, static_cast<size_t>(n * Q + 2), RedOp::kSum, st);
+  };
   launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(), nullptr,
                      f32parts(), losspart.get(), nchunks, kMaxCand, have_pre ? pre : nullptr);
+  collect(nullptr);
   ++passes;
   GdState S{};
   S.f = f;
@@ -355,12 +430,16 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
         launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + sqp * kSqBlocks, nsq,
                        sq2.get() + (sqp ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
                        cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
-                       rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st);
+                       rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st, xr, comm ? dsum.get() : nullptr);
         par ^= 1;
         if (phase == 0 && dev_diff) {
           dpa.gds = gdst.get() + par;
           launch_pass_diff_f32(dpa, Q, st);   // both trials (runs unless the decision is single)
           launch_pass_diff1_f32(dpa, Q, st);  // the first trial only (runs if single)
+          if (comm) {  // the difference sums over the ranks (read by phase 1 only when pending)
+            launch_sum_parts(losspart.get(), nchunks, kMaxCand, 3, dsum.get(), st);
+            comm->allreduce(dsum.get(), 3, RedOp::kSum, st);
+          }
         }
       }
       sqp ^= 1;
@@ -376,6 +455,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       b.halt = &gdst.get()[par].stop;
       launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(),
                          b.halt, f32parts(), losspart.get(), nchunks, kMaxCand, have_pre ? pre : nullptr);
+      collect(b.halt);
     }
     issued += batch;
     GMDS_CUDA(cudaMemcpyAsync(&S, gdst.get() + par, sizeof S, cudaMemcpyDeviceToHost, st));
@@ -446,6 +526,11 @@ EngineLease::~EngineLease() {
 
 // ---------------------------------------------------------------------------
 namespace {
+
+void not_sharded(const gmds_dmat* D, const char* who) {
+  if (D && D->sharded())
+    fail(GMDS_INVALID_INPUT, std::string(who) + ": row-sharded distance matrix (use the *_sharded entry points)");
+}
 
 void check_coords(const gmds_dmat* D, const double* coords, int q, const char* who) {
   // embed.cpp:15-21
@@ -1236,6 +1321,7 @@ gmds_status gmds_dmat_gini_device(const void* dX, gmds_dtype xt, int64_t n, int6
 gmds_status gmds_dmat_download(const gmds_dmat* d, double* D_full) {
   return guard([&] {
     if (!d) fail(GMDS_INVALID_INPUT, "dmat_download: null handle");
+    if (d->sharded()) fail(GMDS_INVALID_INPUT, "dmat_download: row-sharded distance matrix");
     Stream st;
     DevBuf<double> full(static_cast<size_t>(d->n * d->n));
     unpack_full(d->ptr(), d->storage, d->n, full.get(), false, st.s);
@@ -1260,6 +1346,7 @@ void gmds_dmat_free(gmds_dmat* d) { delete d; }
 gmds_status gmds_kruskal_stress(const gmds_dmat* D, const double* coords, int32_t q, double* out) {
   return guard([&] {
     check_coords(D, coords, q, "kruskal_stress");
+    not_sharded(D, "kruskal_stress");
     if (D->sum_sq <= 0.0) fail(GMDS_DEGENERATE_INPUT, "kruskal_stress: all-zero distance matrix");
     Stream st;
     EngineLease L = acquire_engine(D, q, st.s);
@@ -1274,6 +1361,7 @@ gmds_status gmds_stress_loss(int32_t kind, const gmds_dmat* D, const double* coo
                              const double* weights, double* out) {
   return guard([&] {
     check_coords(D, coords, q, "stress_loss");
+    not_sharded(D, "stress_loss");
     const Resolved rp = resolve(D, kind, huber_delta, weights, "stress_loss");
     Stream st;
     EngineLease L = acquire_engine(D, q, st.s);
@@ -1293,6 +1381,7 @@ gmds_status gmds_stress_gradient(int32_t kind, const gmds_dmat* D, const double*
                                  double huber_delta, const double* weights, double* grad) {
   return guard([&] {
     check_coords(D, coords, q, "stress_gradient");
+    not_sharded(D, "stress_gradient");
     const Resolved rp = resolve(D, kind, huber_delta, weights, "stress_gradient");
     Stream st;
     EngineLease L = acquire_engine(D, q, st.s);
@@ -1320,6 +1409,7 @@ gmds_status gmds_stress_partial(int32_t kind, const gmds_dmat* D, const double* 
                                 int32_t shard, int32_t nshards, double* raw_loss, double* raw_grad) {
   return guard([&] {
     check_coords(D, coords, q, "stress_partial");
+    not_sharded(D, "stress_partial");
     if (nshards < 1 || shard < 0 || shard >= nshards) fail(GMDS_INVALID_CONFIG, "stress_partial: bad shard");
     if (q > 4) fail(GMDS_INVALID_INPUT, "stress_partial: sharded passes support q <= 4");
     // resolve_params (embed.cpp:54-109): NaN / non-positive Huber delta, unknown kinds,
@@ -1339,6 +1429,7 @@ gmds_status gmds_classical_mds(const gmds_dmat* D, int32_t q, double* coords, do
                                double* clamped_mass, double* stress) {
   return guard([&] {
     if (!D) fail(GMDS_INVALID_INPUT, "classical_mds: null distance matrix");
+    not_sharded(D, "classical_mds");
     Stream st;
     int cc = 0;
     classical_mds_dev(D, q, coords, eigvals, &cc, clamped_mass, stress, st.s);
@@ -1350,6 +1441,7 @@ gmds_status gmds_classical_mds_topq(const gmds_dmat* D, int32_t q, double tol, i
                                     double* eigvals, int32_t* clamped_count, int32_t* iterations) {
   return guard([&] {
     if (!D) fail(GMDS_INVALID_INPUT, "classical_mds: null distance matrix");
+    not_sharded(D, "classical_mds");
     Stream st;
     int cc = 0, its = 0;
     classical_topq_dev(D, q, tol, max_iters, coords, eigvals, &cc, &its, st.s);
@@ -1358,10 +1450,121 @@ gmds_status gmds_classical_mds_topq(const gmds_dmat* D, int32_t q, double tol, i
   });
 }
 
+// ---- row-sharded multi-GPU path ----
+
+namespace {
+// every rank's flag bits OR-ed (max of the value) so a failure is taken by the whole group
+int group_flag(gmds::Comm& c, int local, cudaStream_t st) {
+  DevBuf<double> v(1);
+  const double h = static_cast<double>(local);
+  GMDS_CUDA(cudaMemcpyAsync(v.get(), &h, sizeof h, cudaMemcpyHostToDevice, st));
+  c.allreduce(v.get(), 1, RedOp::kMax, st);
+  double out = 0.0;
+  GMDS_CUDA(cudaMemcpyAsync(&out, v.get(), sizeof out, cudaMemcpyDeviceToHost, st));
+  GMDS_CUDA(cudaStreamSynchronize(st));
+  return static_cast<int>(out);
+}
+}  // namespace
+
+gmds_status gmds_dmat_gini_sharded(gmds_comm* comm, const void* dX, gmds_dtype xt, int64_t n, int64_t p, double nu,
+                                   gmds_dtype storage, gmds_dmat** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!comm) fail(GMDS_INVALID_INPUT, "pairwise_matrix (sharded): null comm");
+    check_nu(nu);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    require_device();
+    Stream st;
+    Comm& c = *comm->impl;
+    int64_t range[2];
+    shard_blocks(n, c.rank, c.size, range[0], range[1]);
+    if (group_flag(c, range[1] <= range[0] ? 1 : 0, st.s))
+      fail(GMDS_INVALID_CONFIG, "pairwise_matrix (sharded): more ranks than work chunks");
+    auto* d = new gmds_dmat();
+    d->n = n;
+    d->storage = storage;
+    d->blk_lo = range[0];
+    d->blk_hi = range[1];
+    try {
+      const size_t bytes = static_cast<size_t>(range[1] - range[0]) * kPT * kPT * dtype_size(storage);
+      d->buf.alloc(bytes);
+      GMDS_CUDA(cudaMemsetAsync(d->buf.get(), 0, bytes, st.s));
+      DevBuf<int> flag(1);
+      GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st.s));
+      launch_finite_check(dX, xt, n * p, flag.get(), st.s);
+      // only this rank's blocks: the tile rows covering them, filtered per tile in the kernels
+      run_gini(dX, xt, n, p, &nu, 1, storage, 1, const_cast<void*>(d->ptr()), 0, 1, st.s, flag.get(), nullptr,
+               nullptr, range);
+      int hflag = 0;
+      GMDS_CUDA(cudaMemcpyAsync(&hflag, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st.s));
+      GMDS_CUDA(cudaStreamSynchronize(st.s));
+      const int g = group_flag(c, hflag, st.s);
+      if (g & 4) fail(GMDS_INVALID_INPUT, "gen_gini_directed: non-finite input");
+      if (g & 1) fail(GMDS_INVALID_INPUT, "DistanceMatrix: non-finite entry");
+      // per-fit constants over the whole matrix: sums, min and max all-reduced
+      const DStats s = packed_stats(d->ptr(), storage, n, st.s, range[0], range[1]);
+      DevBuf<double> v(4);
+      const double hv[4] = {s.sum_sq, s.sum, s.min_off, s.max_off};
+      GMDS_CUDA(cudaMemcpyAsync(v.get(), hv, sizeof hv, cudaMemcpyHostToDevice, st.s));
+      c.allreduce(v.get(), 2, RedOp::kSum, st.s);
+      c.allreduce(v.get() + 2, 1, RedOp::kMin, st.s);
+      c.allreduce(v.get() + 3, 1, RedOp::kMax, st.s);
+      double r[4];
+      GMDS_CUDA(cudaMemcpyAsync(r, v.get(), sizeof r, cudaMemcpyDeviceToHost, st.s));
+      GMDS_CUDA(cudaStreamSynchronize(st.s));
+      d->sum_sq = r[0];
+      d->sum = r[1];
+      d->min_off = r[2];
+      d->max_val = std::max(0.0, r[3]);
+      d->stats = true;
+    } catch (...) {
+      delete d;
+      throw;
+    }
+    *out = d;
+  });
+}
+
+gmds_status gmds_minimize_stress_sharded(gmds_comm* comm, const gmds_dmat* D, int32_t q, const gmds_stress_cfg* cfg,
+                                         const double* Y0, gmds_fit_result* res) {
+  return guard([&] {
+    if (!comm) fail(GMDS_INVALID_INPUT, "minimize_stress (sharded): null comm");
+    if (!D) fail(GMDS_INVALID_INPUT, "minimize_stress: null distance matrix");
+    if (!D->sharded()) fail(GMDS_INVALID_INPUT, "minimize_stress (sharded): D is not row-sharded");
+    if (D->storage != GMDS_F32) fail(GMDS_INVALID_CONFIG, "minimize_stress (sharded): fp32 storage only");
+    if (q < 1 || q > 4) fail(GMDS_INVALID_INPUT, "minimize_stress (sharded): 1 <= q <= 4");
+    if (!Y0) fail(GMDS_INVALID_CONFIG, "minimize_stress (sharded): needs the seeded start Y0");
+    if (cfg->max_iters < 1) fail(GMDS_INVALID_CONFIG, "minimize_stress: max_iters must be >= 1");
+    if (!(cfg->rel_tol > 0.0)) fail(GMDS_INVALID_CONFIG, "minimize_stress: rel_tol must be > 0");
+    if (cfg->smacof_weights) fail(GMDS_INVALID_CONFIG, "minimize_stress (sharded): uniform SMACOF weights only");
+    if (cfg->kind == GMDS_HUBER && std::isnan(cfg->huber_delta))
+      fail(GMDS_INVALID_CONFIG, "minimize_stress (sharded): huber needs an explicit huber_delta");
+    check_coords(D, Y0, q, "minimize_stress");
+    const Resolved rp = resolve(D, cfg->kind, cfg->huber_delta, nullptr, "minimize_stress");
+    Stream st;
+    Engine E(D, q, st.s, comm->impl.get());
+    E.upload(Y0, E.Y.get());
+    const IterResult r = (cfg->kind == GMDS_SMACOF) ? smacof_iterate(E, rp, nullptr, cfg->max_iters, cfg->rel_tol, nullptr)
+                                                    : gradient_descent(E, rp, cfg->max_iters, cfg->rel_tol);
+    E.download(E.Y.get(), res->coords);
+    res->history_len = static_cast<int64_t>(r.history.size());
+    if (res->history)
+      for (int64_t t = 0; t < std::min<int64_t>(res->history_len, res->history_cap); ++t)
+        res->history[t] = r.history[static_cast<size_t>(t)];
+    res->iterations = r.iterations;
+    res->converged = r.converged ? 1 : 0;
+    res->stress = r.loss;
+    res->huber_delta = (cfg->kind == GMDS_HUBER) ? cfg->huber_delta : 0.0;
+    res->passes = E.passes;
+  });
+}
+
 gmds_status gmds_minimize_stress(const gmds_dmat* D, int32_t q, const gmds_stress_cfg* cfg, const double* Y0,
                                  gmds_fit_result* res) {
   return guard([&] {
     if (!D) fail(GMDS_INVALID_INPUT, "minimize_stress: null distance matrix");
+    not_sharded(D, "minimize_stress");
     if (Y0) check_coords(D, Y0, q, "minimize_stress");
     Stream st;
     minimize_stress_dev(D, q, *cfg, Y0, res, st.s, nullptr);

@@ -6,11 +6,18 @@
 #include <memory>
 #include <vector>
 
+#include "comm.h"
 #include "common.cuh"
 #include "dmat.cuh"
 #include "stress.cuh"
 
 namespace gmds {
+
+// The tiled passes' work list: chunks of up to chunk_len blocks of one block row,
+// in packed (row-major) order.  A row-sharded D holds the blocks of a contiguous
+// chunk range balanced by block count (shard_blocks), so shard edges are chunk edges.
+int64_t chunk_blocks(int64_t nb);
+void shard_blocks(int64_t n, int rank, int size, int64_t& blk_lo, int64_t& blk_hi);
 
 struct Engine {
   const gmds_dmat* D;
@@ -26,7 +33,10 @@ struct Engine {
   DevBuf<double> rowpart, colpart, losspart, graw, scal, Y, sqpart;
   DevBuf<double> cand[kMaxCand];
 
-  Engine(const gmds_dmat* D, int q, cudaStream_t st);
+  Comm* comm = nullptr;  // row-sharded engine: this rank's chunks, sums all-reduced after every pass
+  DevBuf<double> xred, dsum, rawy;  // sharded device loop payload, difference-pass sums, raw loss at Y
+  Engine(const gmds_dmat* D, int q, cudaStream_t st, Comm* comm = nullptr);
+  void allreduce(double* d, size_t count);  // no-op unless sharded
   void upload(const double* coords_colmajor, double* dst);
   void download(const double* src, double* coords_colmajor);
   PassArgs args(int kind, double delta) const;

@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
     decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
     const int64_t i0 = I * kTile, j0 = J * kTile;
     for (int e = threadIdx.x; e < kRows * W; e += blockDim.x) {
       const int r = e / W, w = e - (e / W) * W;
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
     decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
     const int64_t i0 = I * kTile, j0 = J * kTile;
     for (int e = threadIdx.x; e < kRows * W; e += blockDim.x) {
       const int r = e / W, w = e - (e / W) * W;

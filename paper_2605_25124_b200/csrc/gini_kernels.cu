@@ -134,6 +134,7 @@ __global__ void gini_block_kernel(GiniTileArgs a, const T* __restrict__ X, TO* _
     int64_t i, jj;
     decode_tile(pr, a.n - 1, i, jj);  // rows of the strict upper triangle: (i, j = jj + 1)
     const int64_t j = jj + 1;
+    if (!tile_in_blocks(a, i, j)) continue;
     for (int e = threadIdx.x; e < n2; e += blockDim.x)
       key[e] = (e < d) ? static_cast<double>(X[i * d + e]) - static_cast<double>(X[j * d + e]) : INFINITY;
     __syncthreads();

@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(merge_detail::kMergeThreads, 1) gini_merge_ker
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
     decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
     const int64_t i0 = I * tile, j0 = J * tile;
     for (int e = threadIdx.x; e < 2 * tile * W; e += blockDim.x) {
       const int r = e / W, w = e % W;

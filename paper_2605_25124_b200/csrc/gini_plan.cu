@@ -194,8 +194,33 @@ inline int split_detail_min_blocks(int64_t p) { return split_min_blocks(p <= 256
 
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
               int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score,
-              RowSink* sink) {
+              RowSink* sink, const int64_t* blk_range) {
   Trace tr;
+  if (blk_range && (!packed || score || nshards != 1)) fail(GMDS_ERROR, "run_gini: block ranges are for packed stores");
+  // this launch's tiles: shard `shard` of the tile list, or (row-sharded packed builds) the tile
+  // rows covering packed block strips [strip(lo), strip(hi - 1)], filtered per tile in the kernels
+  auto set_range = [&](GiniTileArgs& g, int64_t units, int64_t decode_nbt) {
+    if (!blk_range) {
+      g.tile_begin = units * shard / nshards;
+      g.tile_end = units * (shard + 1) / nshards;
+      return;
+    }
+    g.blk_lo = blk_range[0];
+    g.blk_hi = blk_range[1];
+    const int64_t nb = g.nb_packed;
+    auto bstart = [nb](int64_t r) { return r * nb - (r * (r - 1)) / 2; };
+    int64_t sI = 0, eI = 0;
+    while (bstart(sI + 1) <= g.blk_lo) ++sI;
+    eI = sI;
+    while (bstart(eI + 1) <= g.blk_hi - 1) ++eI;
+    const int64_t r = kPT / g.tile;  // tile rows per block strip
+    auto tstart = [decode_nbt](int64_t R) {
+      R = std::min(R, decode_nbt);
+      return R * decode_nbt - (R * (R - 1)) / 2;
+    };
+    g.tile_begin = tstart(sI * r);
+    g.tile_end = tstart((eI + 1) * r);
+  };
   if (packed || score || nshards != 1) sink = nullptr;
   // Launch tiles [a.tile_begin, a.tile_end) -- in block-row chunks when a sink
   // wants the finished rows as they complete.
@@ -282,8 +307,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     a.tile = 1;
     a.nbt = n;
     const int64_t units = n * (n - 1) / 2;
-    a.tile_begin = units * shard / nshards;
-    a.tile_end = units * (shard + 1) / nshards;
+    set_range(a, units, n - 1);
     launch_gini(a, dX, xt, dD, ot, st);
     GMDS_CUDA(cudaStreamSynchronize(st));
     return;
@@ -296,8 +320,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     a.tile = gini_tile_size(static_cast<int>(p), xt, nnu);
     a.nbt = ceil_div(n, a.tile);
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
-    a.tile_begin = units * shard / nshards;
-    a.tile_end = units * (shard + 1) / nshards;
+    set_range(a, units, a.nbt);
     chunked(a, [&](GiniTileArgs& ga) { launch_gini(ga, dX, xt, dD, ot, st, score ? score_grid : 0); });
     finish_score(score ? std::min<int64_t>(a.tile_end - a.tile_begin, score_grid) : 0);
   };
@@ -335,8 +358,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     a.tile = gmd_detail::kTile;
     a.nbt = ceil_div(n, a.tile);
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
-    a.tile_begin = units * shard / nshards;
-    a.tile_end = units * (shard + 1) / nshards;
+    set_range(a, units, a.nbt);
     if (a.tile_end <= a.tile_begin) return;
     GmdArgs ga{};
     ga.s.g = a;
@@ -397,8 +419,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
       a.tile = mt;
       a.nbt = ceil_div(n, mt);
       const int64_t munits = a.nbt * (a.nbt + 1) / 2;
-      a.tile_begin = munits * shard / nshards;
-      a.tile_end = munits * (shard + 1) / nshards;
+      set_range(a, munits, a.nbt);
       if (a.tile_end <= a.tile_begin) return;
       MergeArgs ma{};
       ma.s.g = a;
@@ -482,8 +503,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
   a.tile = tile;
   a.nbt = ceil_div(n, tile);
   const int64_t units = a.nbt * (a.nbt + 1) / 2;
-  a.tile_begin = units * shard / nshards;
-  a.tile_end = units * (shard + 1) / nshards;
+  set_range(a, units, a.nbt);
   if (a.tile_end <= a.tile_begin) return;
   SplitArgs sa{};
   sa.g = a;

@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(256, split_min_blocks(KMAX)) gini_split_kernel
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
     decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
     const int64_t i0 = I * tile, j0 = J * tile;
     // ---- stage panels: rows 0..tile-1 = block I, tile..2tile-1 = block J
     if constexpr (!SPARSE) {

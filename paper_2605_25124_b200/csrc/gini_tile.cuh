@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(256) gini_tile_kernel(GiniTileArgs a, const T*
   for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
     int64_t I, J;
     decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
     const int64_t i0 = I * tile, j0 = J * tile;
     const bool diag = (I == J);
     // stage the two row panels (coalesced; rows past n are zero)

@@ -35,7 +35,17 @@ struct GiniTileArgs {
   const double* Y;     // n x q row-major fp64 (nullptr: store mode)
   int q;
   double* score_part;  // [gridDim][nnu][2] per-CTA partials (fixed-order sums)
+  // row-sharded packed builds (gmds_dmat_gini_sharded): only tiles inside packed
+  // blocks [blk_lo, blk_hi) are computed (blk_hi <= blk_lo: every tile); needs kPT % tile == 0
+  int64_t blk_lo, blk_hi;
 };
+
+__host__ __device__ inline bool tile_in_blocks(const GiniTileArgs& a, int64_t I, int64_t J) {
+  if (a.blk_hi <= a.blk_lo) return true;
+  const int64_t bI = I * a.tile / kPT, bJ = J * a.tile / kPT;
+  const int64_t b = bI * a.nb_packed - (bI * (bI - 1)) / 2 + (bJ - bI);
+  return b >= a.blk_lo && b < a.blk_hi;
+}
 
 constexpr int kMaxScoreNu = 64;
 

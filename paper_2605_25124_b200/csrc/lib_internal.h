@@ -65,7 +65,7 @@ struct RowSink {
 
 void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double* nus, int nnu, gmds_dtype ot,
               int packed, void* dD, int shard, int nshards, cudaStream_t st, int* dflag, ScoreSpec* score = nullptr,
-              RowSink* sink = nullptr);
+              RowSink* sink = nullptr, const int64_t* blk_range = nullptr);
 void check_flag(int* dflag, cudaStream_t st);
 // flag |= 4 when any of the m input entries is not finite
 void launch_finite_check(const void* dX, gmds_dtype xt, int64_t m, int* dflag, cudaStream_t st);

@@ -91,7 +91,10 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    int phase, cudaStream_t st);
+                    int phase, cudaStream_t st, const double* xred = nullptr, const double* dsum = nullptr);
+// row-sharded device loop: gradient groups -> xred[0, nQ), the pass's trial-loss sums -> xred[nQ, nQ + 2)
+void launch_shard_collect(const double* gpart, int64_t n, int Q, const double* losspart, int64_t nparts, int stride,
+                          double* xred, const int* halt, cudaStream_t st);
 size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass
@@ -108,7 +111,7 @@ void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double
 // returns the number of partials written to sqpart (<= kSqBlocks)
 int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int kind, double sum_sq, double sum,
                        double* g, const double* Y, int64_t m, double s0, double s1, double* T0, double* T1,
-                       double* sqpart, double* raw_out, cudaStream_t st);
+                       double* sqpart, double* raw_out, cudaStream_t st, const double* raw_in = nullptr);
 void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& s, double* const* outs,
                       cudaStream_t st);
 void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st);

@@ -187,6 +187,40 @@ __global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int 
   out[idx] = acc;
 }
 
+// Row-sharded device loop (gmds_minimize_stress_sharded): this rank's gradient groups
+// summed into xred[0, nQ) (combine_kernel's order) and its pass's two trial-loss sums
+// into xred[nQ], xred[nQ + 1] (tree_sum<1024>, gd_pass_sums' order) -- the payload of the
+// all-reduce that follows.  Once the loop has stopped the payload is zeros, so that
+// all-reduce (enqueued ahead with the batch) cannot re-add a stale buffer.
+__global__ void shard_collect_kernel(const double* __restrict__ gpart, int64_t n, int Q,
+                                     const double* __restrict__ losspart, int64_t nparts, int stride,
+                                     double* __restrict__ xred, const int* __restrict__ halt) {
+  pdl_wait();
+  pdl_trigger();
+  const bool stopped = halt && *halt;
+  const int64_t m = n * Q;
+  if (blockIdx.x == gridDim.x - 1) {
+    __shared__ double red[1024];
+    for (int c = 0; c < 2; ++c) {
+      const double v = stopped ? 0.0 : tree_sum<1024>(losspart, nparts, stride, c, red);
+      if (threadIdx.x == 0) xred[m + c] = v;
+    }
+    return;
+  }
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= m) return;
+  if (stopped) {
+    xred[idx] = 0.0;
+    return;
+  }
+  const int64_t r = idx / Q, R = r / kPT;
+  const int64_t e = (r % kPT) * Q + idx % Q, run = static_cast<int64_t>(kPT) * Q;
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < kRedGroups; ++s) acc += gpart[(R * kRedGroups + s) * run + e];
+  xred[idx] = acc;
+}
+
 // Deterministic single-CTA sums: out[c] = sum_k part[k*stride + c] for c < m.
 __global__ void sum_parts_kernel(const double* __restrict__ part, int64_t count, int stride, int m,
                                  double* __restrict__ out) {
@@ -270,9 +304,11 @@ __device__ void finish_body(double scale, double* __restrict__ g, const double* 
 __global__ void finish_grad_kernel(const double* __restrict__ losspart, int64_t nparts, int stride, int kind,
                                    double sum_sq, double sum, double* __restrict__ g, const double* __restrict__ Y,
                                    int64_t m, double s0, double s1, double* __restrict__ T0, double* __restrict__ T1,
-                                   double* __restrict__ sqpart, double* __restrict__ raw_out) {
+                                   double* __restrict__ sqpart, double* __restrict__ raw_out,
+                                   const double* __restrict__ raw_in) {
   __shared__ double red[256];
-  const double raw = tree_sum<256>(losspart, nparts, stride, 0, red);
+  // the raw loss at Y: this device's pass partials, or (row-sharded) the all-reduced value
+  const double raw = raw_in ? *raw_in : tree_sum<256>(losspart, nparts, stride, 0, red);
   const double scale = grad_scale(kind, raw, sum_sq, sum);
   if (blockIdx.x == 0 && threadIdx.x == 0) *raw_out = raw;
   finish_body(scale, g, Y, m, s0, s1, T0, T1, sqpart, red);
@@ -293,7 +329,10 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                double* __restrict__ cand1, double* __restrict__ gnext,
                                const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
-                               double rel_tol, const double* __restrict__ pre, double precise_rel, int phase) {
+                               double rel_tol, const double* __restrict__ pre, double precise_rel, int phase,
+                               const double* __restrict__ xred, const double* __restrict__ dsum) {
+  // xred (row-sharded loop): the all-reduced [gradient at cand0 (n Q) | trial loss sums (2)]
+  // of the last pass; dsum: the all-reduced sums of a difference pass (slots 0, 1, 2)
   pdl_wait();
   pdl_trigger();
   __shared__ double red[1024];
@@ -318,8 +357,9 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     fY = -1.0;  // set below once loss_of is defined
   }
   // the pass's loss sums: from the reduction launch's extra CTA when it ran, else here (same order)
-  const double t0 = pre ? pre[0] : tree_sum<1024>(losspart, nparts, stride, 0, red);
-  const double t1 = pre ? pre[1] : tree_sum<1024>(losspart, nparts, stride, 1, red);
+  if (xred && phase == 0) pre = xred + m;
+  const double t0 = (xred && phase == 1) ? dsum[0] : (pre ? pre[0] : tree_sum<1024>(losspart, nparts, stride, 0, red));
+  const double t1 = (xred && phase == 1) ? dsum[1] : (pre ? pre[1] : tree_sum<1024>(losspart, nparts, stride, 1, red));
   // |g|^2 = the finish partials added in order (as the host does); staged through
   // shared memory so the serial adds do not wait on 148 serial L2 loads
   for (int b = threadIdx.x; b < nsq; b += blockDim.x) red[b] = sqprev[b];
@@ -341,7 +381,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     return raw;
   };
   if (phase == 1) {
-    fY = loss_of(tree_sum<1024>(losspart, nparts, stride, 2, red));
+    fY = loss_of(xred ? dsum[2] : tree_sum<1024>(losspart, nparts, stride, 2, red));
     R.f = fY;
     R.pending = 0;
     if (lead) history[S.it] = fY;
@@ -382,6 +422,12 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   }
   // the raw gradient at cand0 (combine_kernel's sums, in its order) -> gnext
   auto combine = [&]() {
+    if (xred) {  // row-sharded: already combined and all-reduced
+      for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+           k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        gnext[k] = xred[k];
+      return;
+    }
     const int64_t run = static_cast<int64_t>(kPT) * Q;
     for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -418,7 +464,9 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     publish(R);
   }
   // Y <- cand0 (the accepted point); graw <- scaled gradient there; next trial pair
-  const double scale = grad_scale(kind, pre ? pre[2] : tree_sum<256>(losspart, nparts, stride, 0, red), sum_sq, sum);
+  const double raw_acc = xred ? (phase == 1 ? dsum[0] : xred[m])
+                              : (pre ? pre[2] : tree_sum<256>(losspart, nparts, stride, 0, red));
+  const double scale = grad_scale(kind, raw_acc, sum_sq, sum);
   const double s0 = (S.pred == 0) ? R.step : __dmul_rn(R.step, 0.5);
   const double s1 = (S.pred == 0) ? __dmul_rn(R.step, 0.5) : R.step;
   if (R.stop) {  // final point only
@@ -518,10 +566,10 @@ size_t reduce_rows_scratch(int64_t nb, int q) { return static_cast<size_t>(nb) *
 
 int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int kind, double sum_sq, double sum,
                        double* g, const double* Y, int64_t m, double s0, double s1, double* T0, double* T1,
-                       double* sqpart, double* raw_out, cudaStream_t st) {
+                       double* sqpart, double* raw_out, cudaStream_t st, const double* raw_in) {
   const int blocks = static_cast<int>(std::min<int64_t>(kSqBlocks, std::max<int64_t>(1, ceil_div(m, 256))));
   finish_grad_kernel<<<blocks, 256, 0, st>>>(losspart, nparts, stride, kind, sum_sq, sum, g, Y, m, s0, s1, T0, T1,
-                                             sqpart, raw_out);
+                                             sqpart, raw_out, raw_in);
   count_launch();
   check_launch("finish_grad_kernel");
   return blocks;
@@ -531,12 +579,20 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    int phase, cudaStream_t st) {
+                    int phase, cudaStream_t st, const double* xred, const double* dsum) {
   launch_pdl(gd_step_kernel, dim3(nsq), dim3(256), 0, st, st2, par, losspart, nparts, stride, sqprev, nsq, sqnext,
              kind, sum_sq, sum, Y, cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-             precise_rel, phase);
+             precise_rel, phase, xred, dsum);
   count_launch();
   check_launch("gd_step_kernel");
+}
+
+void launch_shard_collect(const double* gpart, int64_t n, int Q, const double* losspart, int64_t nparts, int stride,
+                          double* xred, const int* halt, cudaStream_t st) {
+  launch_pdl(shard_collect_kernel, dim3(static_cast<unsigned>(ceil_div(n * Q, 256) + 1)), dim3(256), 0, st, gpart, n, Q,
+             losspart, nparts, stride, xred, halt);
+  count_launch();
+  check_launch("shard_collect_kernel");
 }
 
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st) {

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "common.cuh"
 #include "dmat.cuh"
 #include "dmat_kernels.cuh"
@@ -310,6 +311,50 @@ gmds_status gmds_nu_sweep_kruskal(const void* X, gmds_dtype xt, gmds_layout lx, 
     Stream st;
     DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
     sweep_kruskal(dX.get(), xt, n, p, grid, m, Y, q, st.s, ks);
+  });
+}
+
+gmds_status gmds_nu_sweep_kruskal_sharded(gmds_comm* comm, const void* X, gmds_dtype xt, gmds_layout lx, int64_t n,
+                                          int64_t p, const double* Y, int32_t q, const double* grid, int32_t m,
+                                          double* ks) {
+  return guard([&] {
+    if (!comm) fail(GMDS_INVALID_INPUT, "nu sweep (sharded): null comm");
+    check_grid(grid, m);
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    if (q < 1) fail(GMDS_INVALID_INPUT, "kruskal_stress: coords have no columns");
+    check_finite_host(X, xt, n * p, "gen_gini_directed");
+    for (int64_t k = 0; k < n * q; ++k)
+      if (!std::isfinite(Y[k])) fail(GMDS_INVALID_INPUT, "kruskal_stress: non-finite coordinates");
+    require_device();
+    Stream st;
+    Comm& c = *comm->impl;
+    // this rank's contiguous block of the grid (replicas: no exchange until the scores)
+    int64_t g0 = 0, g1 = 0;
+    share_of(m, c.rank, c.size, g0, g1);
+    std::vector<double> mine(static_cast<size_t>(m), 0.0);
+    int err = 0;
+    std::string msg;
+    gmds_status code = GMDS_OK;
+    if (g1 > g0) {
+      try {
+        DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
+        sweep_kruskal(dX.get(), xt, n, p, grid + g0, static_cast<int>(g1 - g0), Y, q, st.s, mine.data() + g0);
+      } catch (const Failure& e) {  // every rank learns of it below, so no rank is left waiting
+        err = 1;
+        code = e.status;
+        msg = e.what();
+      }
+    }
+    DevBuf<double> v(static_cast<size_t>(m) + 1);
+    mine.push_back(static_cast<double>(err));
+    GMDS_CUDA(cudaMemcpyAsync(v.get(), mine.data(), mine.size() * sizeof(double), cudaMemcpyHostToDevice, st.s));
+    c.allreduce(v.get(), mine.size(), RedOp::kSum, st.s);  // other ranks' slots are 0: a gather
+    GMDS_CUDA(cudaMemcpyAsync(mine.data(), v.get(), mine.size() * sizeof(double), cudaMemcpyDeviceToHost, st.s));
+    GMDS_CUDA(cudaStreamSynchronize(st.s));
+    if (err) fail(code, msg);
+    if (mine[static_cast<size_t>(m)] != 0.0) fail(GMDS_ERROR, "nu sweep (sharded): another rank failed");
+    std::memcpy(ks, mine.data(), static_cast<size_t>(m) * sizeof(double));
   });
 }
 

@@ -466,3 +466,90 @@ def nu_sweep_kruskal(X, Y, grid) -> np.ndarray:
     _check(lib().gmds_nu_sweep_kruskal(_vp(X), _i32(xt), _i32(lx), _i64(n), _i64(p), _p(Y), _i32(Y.shape[1]), _p(g),
                                        _i32(g.size), _p(out)))
     return out
+
+
+# ---- multi-GPU: collectives + row-sharded D / fit, sharded nu sweep -----------------
+
+
+class Comm:
+    """One rank's collective handle (gmds_comm)."""
+
+    def __init__(self, handle: int):
+        self._h = ctypes.c_void_p(handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def rank(self) -> int:
+        return lib().gmds_comm_rank(self._h)
+
+    @property
+    def size(self) -> int:
+        return lib().gmds_comm_size(self._h)
+
+    def allreduce_device(self, dptr: int, count: int, op: int = 0, stream: int = 0):
+        _check(lib().gmds_comm_allreduce_device(self._h, ctypes.c_void_p(dptr), _i64(count), _i32(op),
+                                                ctypes.c_void_p(stream)))
+
+    def free(self):
+        if self._h:
+            lib().gmds_comm_free(self._h)
+            self._h = ctypes.c_void_p(0)
+
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib().gmds_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def comm_init_nccl(uid: bytes, nranks: int, rank: int) -> Comm:
+    """NCCL rank on the current device (gmds_set_device first); uid from rank 0's comm_unique_id."""
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+    h = ctypes.c_void_p()
+    _check(lib().gmds_comm_init_nccl(buf, _i32(nranks), _i32(rank), ctypes.byref(h)))
+    return Comm(h.value)
+
+
+def comm_init_local(nranks: int) -> list:
+    """nranks ranks in this process on the current device (drive each from its own thread)."""
+    hs = (ctypes.c_void_p * nranks)()
+    _check(lib().gmds_comm_init_local(_i32(nranks), hs))
+    return [Comm(h) for h in hs]
+
+
+def dmat_gini_sharded(comm: Comm, dX_ptr: int, xt: int, n: int, p: int, nu: float, storage=F32) -> DMat:
+    """This rank's contiguous share of the packed blocks of pairwise_matrix(X, gini(nu))."""
+    h = ctypes.c_void_p()
+    _check(lib().gmds_dmat_gini_sharded(comm.handle, ctypes.c_void_p(dX_ptr), _i32(xt), _i64(n), _i64(p),
+                                        ctypes.c_double(nu), _i32(storage), ctypes.byref(h)))
+    return DMat(h.value, n)
+
+
+def minimize_stress_sharded(comm: Comm, D: DMat, Y0, kind: str = "kruskal", huber_delta=None, max_iters: int = 300,
+                            rel_tol: float = 1e-6) -> dict:
+    y0 = _coords(Y0)
+    q = y0.shape[1]
+    cfg = StressCfg(kind=KIND[kind], huber_delta=(math.nan if huber_delta is None else float(huber_delta)),
+                    smacof_weights=None, max_iters=int(max_iters), rel_tol=float(rel_tol), seed=0)
+    coords = np.zeros((D.n, q), order="F")
+    cap = int(max_iters) + 2
+    hist = np.zeros(cap)
+    res = FitResult(coords=_p(coords), history=_p(hist), history_cap=cap)
+    _check(lib().gmds_minimize_stress_sharded(comm.handle, D.handle, _i32(q), ctypes.byref(cfg), _p(y0),
+                                              ctypes.byref(res)))
+    return dict(coords=np.ascontiguousarray(coords), stress_history=list(hist[: min(res.history_len, cap)]),
+                iterations=res.iterations, converged=bool(res.converged), stress=res.stress, passes=res.passes)
+
+
+def nu_sweep_kruskal_sharded(comm: Comm, X, Y, grid) -> np.ndarray:
+    X, xt, lx = _xarg(X)
+    n, p = X.shape
+    Y = _coords(Y)
+    g = np.ascontiguousarray(grid, dtype=np.float64)
+    ks = np.zeros(g.size)
+    _check(lib().gmds_nu_sweep_kruskal_sharded(comm.handle, _vp(X), _i32(xt), _i32(lx), _i64(n), _i64(p), _p(Y),
+                                               _i32(Y.shape[1]), _p(g), _i32(g.size), _p(ks)))
+    return ks
