@@ -20,8 +20,12 @@ init, rel_tol 1e-300) on that matrix.
 ``--impl reference`` times the reference's own CPU implementation (the
 UNMODIFIED reference core compiled by oracle/Makefile, all host threads) on a
 bounded sample of the same workload.  Multi-GPU (torchrun): the pair tiles are
-split across ranks (strong scaling, no collective on the data path); the
-timed region is bracketed by a barrier and the time is the max over ranks.
+split across ranks (strong scaling, no collective on the data path); the fit
+runs on each rank's share of D's packed blocks (gmds_dmat_gini_sharded) with one
+in-stream NCCL all-reduce of [gradient | loss sums] per pass
+(gmds_minimize_stress_sharded).  The timed regions are bracketed by a barrier and
+the time is the max over ranks.  ``--gpus N`` without torchrun re-launches
+itself under torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -335,23 +339,23 @@ def run_engine(args, rank, world, dist):
     t_general = max_over_ranks(dist, float(np.mean(gtimes)))
 
     # ---- stress: S Kruskal iterations on the packed matrix of this step.  One GPU: the
-    # device-controlled fit.  Several ranks: the tile-sharded fit, one NCCL all-reduce of
-    # [loss | gradient] per pass (paper_2605_25124_b200/distributed.py).
-    Dm = G.dmat_gini_device(dX.data_ptr(), G.F32, N, P, NU, G.F32)
+    # device-controlled fit.  Several ranks: the row-sharded device-controlled fit of libgmds.
     Y0 = np.random.default_rng(SEED).normal(0.0, 0.1, (N, Q))
     if world > 1:
-        from paper_2605_25124_b200 import distributed as MD
-
-        allreduce_sum, _ = MD.torch_collectives()
-        part = MD.gpu_partial(Dm, rank, world)
-        stats = MD.dmat_stats(Dm)
+        # libgmds multi-GPU path: an NCCL communicator (unique id shared over torch.distributed),
+        # this rank's share of D's packed blocks, and the device-resident sharded fit with one
+        # in-stream all-reduce of [gradient | loss sums] per pass
+        uid = [G.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = G.comm_init_nccl(uid[0], world, rank)
+        Dm = G.dmat_gini_sharded(comm, dX.data_ptr(), G.F32, N, P, NU, G.F32)
 
         def fit(iters):
-            r = MD.minimize_stress_sharded(part, allreduce_sum, Y0, "kruskal", stats, N, max_iters=iters,
-                                           rel_tol=1e-300)
-            r["passes"] = len(r["stress_history"]) * 2
-            return r
+            return G.minimize_stress_sharded(comm, Dm, Y0, "kruskal", max_iters=iters, rel_tol=1e-300)
     else:
+        comm = None
+        Dm = G.dmat_gini_device(dX.data_ptr(), G.F32, N, P, NU, G.F32)
+
         def fit(iters):
             return G.minimize_stress(Dm, Q, "kruskal", max_iters=iters, rel_tol=1e-300, Y0=Y0)
     fit(2)  # warm-up
@@ -377,7 +381,7 @@ def run_engine(args, rank, world, dist):
     # of a 100- and the 50-iteration run -- by then every step is above fp32 storage's
     # resolution (no difference passes); reported beside the headline rate
     resolved = None
-    if world == 1:
+    if True:
         def timed_fit(iters):
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -389,11 +393,14 @@ def run_engine(args, rank, world, dist):
 
         t100, r100 = timed_fit(2 * STRESS_ITERS)
         t50, r50 = timed_fit(STRESS_ITERS)
+        t100, t50 = max_over_ranks(dist, t100), max_over_ranks(dist, t50)
         if r100["iterations"] == 2 * STRESS_ITERS and t100 > t50:
             resolved = {"iters_per_sec": STRESS_ITERS / (t100 - t50), "ms_per_iter": 1e3 * (t100 - t50) / STRESS_ITERS,
                         "passes_per_iter": (r100["passes"] - r50["passes"]) / STRESS_ITERS,
                         "iterations": "51-100 of the fit (t(100) - t(50))"}
     Dm.free()
+    if comm is not None:
+        comm.free()
 
     # ---- e2e: the drop-in pairwise_matrix call, pinned host X -> host fp64 n x n D
     e2e = None
@@ -426,12 +433,12 @@ def run_engine(args, rank, world, dist):
     G.lib().gmds_probe_alu(ctypes_ref(alu))
     props = torch.cuda.get_device_properties(dev)
     sm_max = clk.summary().get("sm_max_mhz") or 1965.0
-    alu_nominal = props.multi_processor_count * 128 * sm_max * 1e6
+    alu_nominal = props.multi_processor_count * 128 * sm_max * 1e6 * world  # whole job
     ops_pair = ops_per_pair(P, 1)
     my_pairs = npairs  # all ranks together
     achieved = my_pairs * ops_pair / t_dist
     peaks = load_peaks()
-    hbm = peaks.get("hbm_gbs", 6650.0)
+    hbm = peaks.get("hbm_gbs", 6650.0) * world  # whole job: every rank streams its share of D
     traffic_dist, traffic_stress = load_traffic()
     # stress: unit = one iteration; algorithmic bytes = one read of the packed fp32
     # triangle (n(n-1)/2 x 4 B) per iteration, whatever the passes per iteration
@@ -449,7 +456,7 @@ def run_engine(args, rank, world, dist):
                    "stress_iters_per_step": STRESS_ITERS, "stress_kind": "kruskal (Armijo GD)",
                    "init": "seeded N(0, 0.1^2) (SURVEY F4)", "l2": "flushed (256 MB write) before every "
                    "distance step; the packed D (800 MB) exceeds L2 for the stress passes",
-                   "parallelism": f"pair tiles sharded over {world} GPU(s)"},
+                   "parallelism": f"dp{world}: distance pair tiles and the fit's packed blocks sharded over {world} GPU(s), one NCCL all-reduce per stress pass"},
         "distance_ms": t_dist * 1e3,
         "distance_general_nu": {"nu": NU_GENERAL, "ms": t_general * 1e3, "pairs_per_s": npairs / t_general,
                                 "kernel": "gini_gen_kernel (midranks counted, one LUT pass)",
@@ -526,6 +533,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:  # self-launch N ranks, one per GPU
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None

@@ -98,6 +98,21 @@ def img2600(t0):
     save("large_img2600", D_rowsum=D.sum(axis=1), **{"fit_" + k: v for k, v in fit.items()})
 
 
+def cls1500(t0):
+    # the reference's classical_mds (dense SelfAdjointEigenSolver, embed.cpp:415-460) at n = 1500,
+    # image-like data: pins the engine's top-q Lanczos solver (no dense B) directly
+    X = S.image_like(1500, 784, 9)
+    D = R.pairwise_matrix(X.astype(np.float64), 2.0)
+    out = {}
+    for q in (1, 2, 3):
+        e = R.classical_mds(D, q)
+        out[f"coords{q}"] = e["coords"]
+        out[f"eig{q}"] = e["eigenvalues"]
+        out[f"stress{q}"] = e["stress"]
+    log("cls1500: reference classical_mds q = 1, 2, 3", t0)
+    save("large_cls1500", D_rowsum=D.sum(axis=1), **out)
+
+
 def c2(t0):
     # C2: 8 nu in [1.1, 8]; per nu the reference pairwise_matrix and minimize_stress(Kruskal,
     # classical init, 1000 iterations)
@@ -143,7 +158,7 @@ def c4(t0):
 def main():
     if R.load() is None or R.load_seeded() is None:
         sys.exit("oracle/_ref not built: make -C oracle")
-    which = sys.argv[1:] or ["img2600", "c2", "c4", "c3", "metric"]
+    which = sys.argv[1:] or ["img2600", "cls1500", "c2", "c4", "c3", "metric"]
     t0 = time.perf_counter()
     for w in which:
         globals()[w](t0)

@@ -12,7 +12,6 @@
 // halving loop would accept.  SMACOF needs one pass per iteration: the pass
 // at Z yields loss(Z) and the Guttman transform of Z together.
 #include <cusolverDn.h>
-#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cmath>
@@ -48,7 +47,6 @@ int64_t chunk_blocks(int64_t nb) {
   return std::max<int64_t>(1, std::min<int64_t>(8, nblk / (148 * 8)));
 }
 
-namespace {
 // (I, J0) of every chunk, in packed order
 void chunk_list(int64_t nb, int64_t len, std::vector<int64_t>& cI, std::vector<int64_t>& cJ) {
   for (int64_t I = 0; I < nb; ++I)
@@ -57,6 +55,8 @@ void chunk_list(int64_t nb, int64_t len, std::vector<int64_t>& cI, std::vector<i
       cJ.push_back(J0);
     }
 }
+
+namespace {
 int64_t blk_of(int64_t I, int64_t J, int64_t nb) { return I * nb - (I * (I - 1)) / 2 + (J - I); }
 }  // namespace
 
@@ -785,8 +785,7 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
 }
 
 // smacof_iterate (embed.cpp:296-347).  pass(Z) -> (loss(Z), B(Z) Z).
-IterResult smacof_iterate(Engine& E, const Resolved& rp, const double* dVpinv, int max_iters, double rel_tol,
-                          cublasHandle_t blas) {
+IterResult smacof_iterate(Engine& E, const Resolved& rp, const double* dVpinv, int max_iters, double rel_tol) {
   IterResult r;
   const int64_t n = E.n;
   double* next = E.cand[0].get();
@@ -795,13 +794,7 @@ IterResult smacof_iterate(Engine& E, const Resolved& rp, const double* dVpinv, i
     if (!dVpinv) {
       launch_scale(E.graw.get(), n * E.Q, static_cast<double>(n), next, E.st);  // (B Z) / n
     } else {
-      // X+ = V^+ (B Z): column-major n x n times row-major n x Q (== column-major Q x n)^T
-      const double one = 1.0, zero = 0.0;
-      // out^T (Q x n, col-major == row-major n x Q) = (BZ)^T (Q x n) * Vpinv^T (n x n); Vpinv symmetric.
-      if (cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, E.Q, static_cast<int>(n), static_cast<int>(n), &one,
-                      E.graw.get(), E.Q, dVpinv, static_cast<int>(n), &zero, next, E.Q) != CUBLAS_STATUS_SUCCESS)
-        fail(GMDS_CUDA_ERROR, "smacof: cublasDgemm failed");
-      count_launch();
+      launch_vpinv_apply(dVpinv, E.graw.get(), n, E.Q, next, E.st);  // X+ = V^+ (B Z)
     }
   };
   double f = E.grad_raw(kGuttman, 0.0, E.Y.get());  // loss(Z0) and B(Z0) Z0
@@ -1180,14 +1173,8 @@ void minimize_stress_dev(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, 
   IterResult r;
   if (cfg.kind == GMDS_SMACOF) {
     DevBuf<double> vp;
-    cublasHandle_t blas = nullptr;
-    if (rp.weighted) {
-      vp = weights_pinv(cfg.smacof_weights, n, st);
-      if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) fail(GMDS_CUDA_ERROR, "cublasCreate failed");
-      cublasSetStream(blas, st);
-    }
-    r = smacof_iterate(E, rp, rp.weighted ? vp.get() : nullptr, cfg.max_iters, cfg.rel_tol, blas);
-    if (blas) cublasDestroy(blas);
+    if (rp.weighted) vp = weights_pinv(cfg.smacof_weights, n, st);
+    r = smacof_iterate(E, rp, rp.weighted ? vp.get() : nullptr, cfg.max_iters, cfg.rel_tol);
   } else {
     r = gradient_descent(E, rp, cfg.max_iters, cfg.rel_tol);
   }
@@ -1545,7 +1532,7 @@ gmds_status gmds_minimize_stress_sharded(gmds_comm* comm, const gmds_dmat* D, in
     Stream st;
     Engine E(D, q, st.s, comm->impl.get());
     E.upload(Y0, E.Y.get());
-    const IterResult r = (cfg->kind == GMDS_SMACOF) ? smacof_iterate(E, rp, nullptr, cfg->max_iters, cfg->rel_tol, nullptr)
+    const IterResult r = (cfg->kind == GMDS_SMACOF) ? smacof_iterate(E, rp, nullptr, cfg->max_iters, cfg->rel_tol)
                                                     : gradient_descent(E, rp, cfg->max_iters, cfg->rel_tol);
     E.download(E.Y.get(), res->coords);
     res->history_len = static_cast<int64_t>(r.history.size());

@@ -17,6 +17,7 @@ namespace gmds {
 // in packed (row-major) order.  A row-sharded D holds the blocks of a contiguous
 // chunk range balanced by block count (shard_blocks), so shard edges are chunk edges.
 int64_t chunk_blocks(int64_t nb);
+void chunk_list(int64_t nb, int64_t len, std::vector<int64_t>& cI, std::vector<int64_t>& cJ);
 void shard_blocks(int64_t n, int rank, int size, int64_t& blk_lo, int64_t& blk_hi);
 
 struct Engine {

@@ -115,5 +115,7 @@ int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int k
 void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& s, double* const* outs,
                       cudaStream_t st);
 void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st);
+// out (n x Q) = V^+ (n x n, symmetric) times bz (n x Q); Q <= 4
+void launch_vpinv_apply(const double* Vp, const double* bz, int64_t n, int Q, double* out, cudaStream_t st);
 
 }  // namespace gmds

@@ -617,6 +617,30 @@ void launch_axpy_cand(const double* Y, const double* G, int64_t m, const Steps& 
   check_launch("axpy_cand_kernel");
 }
 
+// Weighted SMACOF's X+ = V^+ (B Z) (embed.cpp:315-322): out (n x Q row-major) from the
+// symmetric n x n V^+ (column-major) and BZ (n x Q row-major); thread per row, reads of V^+
+// coalesced across threads, j in order
+__global__ void vpinv_apply_kernel(const double* __restrict__ Vp, const double* __restrict__ bz, int64_t n, int Q,
+                                   double* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int64_t j = 0; j < n; ++j) {
+      const double v = Vp[j * n + i];  // V+(i, j) = V+(j, i)
+      for (int k = 0; k < Q; ++k) acc[k] = fma(v, bz[j * Q + k], acc[k]);
+    }
+    for (int k = 0; k < Q; ++k) out[i * Q + k] = acc[k];
+  }
+}
+
+void launch_vpinv_apply(const double* Vp, const double* bz, int64_t n, int Q, double* out, cudaStream_t st) {
+  if (Q > 4) fail(GMDS_INVALID_INPUT, "weighted smacof: embedding dimension above 4 is not supported");
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n, 128)));
+  vpinv_apply_kernel<<<blocks, 128, 0, st>>>(Vp, bz, n, Q, out);
+  count_launch();
+  check_launch("vpinv_apply_kernel");
+}
+
 void launch_scale(const double* in, int64_t m, double divisor, double* out, cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, 256), 1024)));
   scale_kernel<<<blocks, 256, 0, st>>>(in, m, divisor, out);

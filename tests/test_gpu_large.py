@@ -185,3 +185,21 @@ def test_metric_fit_trajectory_vs_reference(golden):
     e, Dm = _seeded_fit(g, G.F32)
     _traj_check(e["stress_history"], g["fit_history"], int(g["fit_iterations"]), e["iterations"])
     assert abs(G.kruskal_stress(e["coords"], Dm) - e["stress"]) <= 1e-6 * e["stress"]
+
+
+@pytest.mark.parametrize("q", [1, 2, 3])
+@pytest.mark.parametrize("storage", [G.F64, G.F32])
+def test_classical_topq_vs_reference(golden, q, storage):
+    # the top-q classical init without a dense B (Lanczos over the packed
+    # triangle, hand-written kernels) against the reference's own classical_mds (dense
+    # SelfAdjointEigenSolver, embed.cpp:415-460) at n = 1500
+    g = golden("large_cls1500")
+    X = S.image_like(1500, 784, 9)
+    dX = _device_X(X)
+    Dm = G.dmat_gini_device(dX.data_ptr(), G.F32, 1500, 784, 2.0, storage)
+    t = G.classical_mds_topq(Dm, q, tol=1e-12)
+    ev, ref_c = g[f"eig{q}"], g[f"coords{q}"]
+    rel = 1e-9 if storage == G.F64 else 1e-6  # fp32 storage rounds D (and so B) at 6e-8
+    assert np.allclose(t["eigenvalues"], ev, rtol=rel, atol=0)
+    assert np.max(np.abs(t["coords"] - ref_c)) <= (1e-7 if storage == G.F64 else 1e-4) * np.max(np.abs(ref_c))
+    assert t["iterations"] < 400
