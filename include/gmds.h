@@ -88,8 +88,17 @@ gmds_status gmds_empirical_survival(const double* z, int64_t d, double* out);
 gmds_status gmds_pairwise_gini(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
                                const double* nus, int32_t nnu, gmds_dtype out_t, void* D);
 
-/* pairwise_matrix, Euclidean branch (metrics.cpp:220-235).  D: host n x n fp64. */
+/* pairwise_matrix, Euclidean branch (metrics.cpp:220-235).  D: host n x n fp64.
+ * n >= 512: tcgen05 path (see gmds_pairwise_euclidean_device), within 1e-6
+ * max-normalised of the reference; smaller n: the reference's arithmetic exactly. */
 gmds_status gmds_pairwise_euclidean(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, double* D);
+
+/* The Euclidean branch on the device: dX row-major, dD n x n fp64.  mode 0: the
+ * tcgen05 path for n >= 512 (bf16x3 split Gram GEMM in TMEM + fp64 norm
+ * corrections, near-duplicates recomputed exactly), else the exact fp64 kernel;
+ * 1: exact kernel; 2: tcgen05 path. */
+gmds_status gmds_pairwise_euclidean_device(const void* dX, gmds_dtype xt, int64_t n, int64_t p, double* dD,
+                                           int32_t mode, void* stream);
 
 /* Device-resident variant for callers that keep X and D in HBM (bench,
  * the fit path).  dX row-major on the device; dD receives nnu full n x n

@@ -351,6 +351,26 @@ gmds_status gmds_pairwise_gini(const void* X, gmds_dtype xt, gmds_layout lx, int
   });
 }
 
+gmds_status gmds_pairwise_euclidean_device(const void* dX, gmds_dtype xt, int64_t n, int64_t p, double* dD,
+                                           int32_t mode, void* stream) {
+  return guard([&] {
+    if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
+    if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
+    if (mode < 0 || mode > 2) fail(GMDS_INVALID_CONFIG, "pairwise_euclidean: mode must be 0 (auto), 1 (exact), 2 (tc)");
+    require_device();
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CallScope scope(st);
+    const bool tc = mode == 2 || (mode == 0 && euclid_tc_enabled(n, p));
+    if (tc) {
+      launch_euclid_tc(dX, xt, n, static_cast<int>(p), dD, st);
+    } else {
+      GMDS_CUDA(cudaMemsetAsync(dD, 0, sizeof(double) * n * n, st));
+      launch_euclid(dX, xt, n, static_cast<int>(p), dD, st);
+    }
+    GMDS_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 gmds_status gmds_pairwise_euclidean(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p, double* D) {
   return guard([&] {
     if (n < 2) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 2 rows");
@@ -360,7 +380,10 @@ gmds_status gmds_pairwise_euclidean(const void* X, gmds_dtype xt, gmds_layout lx
     DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
     DevBuf<double> dD(static_cast<size_t>(n * n));
     GMDS_CUDA(cudaMemsetAsync(dD.get(), 0, sizeof(double) * n * n, st.s));
-    launch_euclid(dX.get(), xt, n, static_cast<int>(p), dD.get(), st.s);
+    if (euclid_tc_enabled(n, p))
+      launch_euclid_tc(dX.get(), xt, n, static_cast<int>(p), dD.get(), st.s);
+    else
+      launch_euclid(dX.get(), xt, n, static_cast<int>(p), dD.get(), st.s);
     GMDS_CUDA(cudaMemcpyAsync(D, dD.get(), sizeof(double) * n * n, cudaMemcpyDeviceToHost, st.s));
     GMDS_CUDA(cudaStreamSynchronize(st.s));
     // from_matrix (metrics.cpp:169-191): Euclidean entries are finite for finite

@@ -58,6 +58,9 @@ void launch_midrank(const double* dv, const void* dX, gmds_dtype xt, const int64
 void launch_gini(GiniTileArgs a, const void* dX, gmds_dtype xt, void* dout, gmds_dtype ot, cudaStream_t st,
                  int64_t max_blocks = 0);
 void launch_euclid(const void* dX, gmds_dtype xt, int64_t n, int d, double* dout, cudaStream_t st);
+// tcgen05 path (euclid_tc.cu): full n x n fp64 out; used when euclid_tc_enabled (GMDS_EUCLID=exact|tc overrides)
+bool euclid_tc_enabled(int64_t n, int64_t p);
+void launch_euclid_tc(const void* dX, gmds_dtype xt, int64_t n, int p, double* dout, cudaStream_t st);
 void launch_transpose(const void* din, gmds_dtype t, int64_t rows, int64_t cols, void* dout, cudaStream_t st);
 
 }  // namespace gmds
