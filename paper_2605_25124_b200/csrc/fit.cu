@@ -403,7 +403,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   auto collect = [&](const int* halt) {
     if (!comm) return;
     launch_shard_collect(gpart.get(), n, Q, losspart.get(), nchunks, kMaxCand, xr, halt, st);
-    comm->allreduce(xr, static_cast<size_t>(n * Q + 2), RedOp::kSum, st);
+    comm->allreduce(xr, static_cast<size_t>(n * Q + 3), RedOp::kSum, st);
   };
   launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(), nullptr,
                      f32parts(), losspart.get(), nchunks, kMaxCand, have_pre ? pre : nullptr);
@@ -423,6 +423,9 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   dpa.Y[1] = graw.get();
   dpa.ncand = 2;
   const bool dev_diff = precise_rel > 0.0 && kind == kKruskal && !W;
+  // the tiny phase's difference + gradient pass (q <= 3); GMDS_NO_TINY=1: every sub-resolution
+  // decision takes the fused pass and a difference pass (the host loop's two passes)
+  const bool tiny_ok = dev_diff && Q <= 3 && !std::getenv("GMDS_NO_TINY");
   for (;;) {
     const int batch = std::max(1, std::min(16, max_iters - issued));
     for (int k = 0; k < batch; ++k) {
@@ -430,7 +433,8 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
         launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + sqp * kSqBlocks, nsq,
                        sq2.get() + (sqp ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
                        cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
-                       rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st, xr, comm ? dsum.get() : nullptr);
+                       rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st, xr, comm ? dsum.get() : nullptr,
+                       tiny_ok);
         par ^= 1;
         if (phase == 0 && dev_diff) {
           dpa.gds = gdst.get() + par;
@@ -445,12 +449,14 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       sqp ^= 1;
       b.halt = &gdst.get()[par].halt_fused;
       launch_pass_fused_f32(b, Q, st);
-      if (dev_diff) {  // tiny mode: the gradient at the first trial only (its losses are re-taken anyway)
+      if (tiny_ok) {  // tiny phase: one difference + gradient pass (the kernels exit unless tiny)
         PassArgs gp = args(kind, delta);
-        gp.Y[0] = cand[0].get();
-        gp.ncand = 1;
-        gp.halt = &gdst.get()[par].halt_grad;
-        launch_stress_pass(gp, Q, true, GMDS_F32, st);
+        gp.Y[0] = Y.get();
+        gp.Y[1] = graw.get();
+        gp.ncand = 2;
+        gp.gds = gdst.get() + par;
+        launch_pass_diffgrad_f32(gp, Q, false, st);  // both trials
+        launch_pass_diffgrad_f32(gp, Q, true, st);   // the first trial (when it leads the slot order)
       }
       b.halt = &gdst.get()[par].stop;
       launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(),

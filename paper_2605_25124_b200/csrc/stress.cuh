@@ -91,7 +91,8 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    int phase, cudaStream_t st, const double* xred = nullptr, const double* dsum = nullptr);
+                    int phase, cudaStream_t st, const double* xred = nullptr, const double* dsum = nullptr,
+                    bool tiny_ok = false);
 // row-sharded device loop: gradient groups -> xred[0, nQ), the pass's trial-loss sums -> xred[nQ, nQ + 2)
 void launch_shard_collect(const double* gpart, int64_t n, int Q, const double* losspart, int64_t nparts, int stride,
                           double* xred, const int* halt, cudaStream_t st);
@@ -105,6 +106,9 @@ void launch_pass_precise(const PassArgs& a, int Q, cudaStream_t st);
 void launch_pass_diff_f32(const PassArgs& a, int Q, cudaStream_t st);
 // the same for the first trial only (slot 1 then holds the loss at Y; device loop, tiny mode)
 void launch_pass_diff1_f32(const PassArgs& a, int Q, cudaStream_t st);
+// kruskal, device loop's tiny phase: the difference pass (both trials, or the first when single)
+// plus the raw gradient at a.Y[2] (the first trial point) -- runs only when a.gds->tiny
+void launch_pass_diffgrad_f32(const PassArgs& a, int Q, bool single, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 // raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;

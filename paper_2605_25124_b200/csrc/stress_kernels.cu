@@ -188,8 +188,8 @@ __global__ void combine_kernel(const double* __restrict__ gpart, int64_t n, int 
 }
 
 // Row-sharded device loop (gmds_minimize_stress_sharded): this rank's gradient groups
-// summed into xred[0, nQ) (combine_kernel's order) and its pass's two trial-loss sums
-// into xred[nQ], xred[nQ + 1] (tree_sum<1024>, gd_pass_sums' order) -- the payload of the
+// summed into xred[0, nQ) (combine_kernel's order) and its pass's loss-slot sums 0-2
+// into xred[nQ, nQ + 3) (tree_sum<1024>, gd_pass_sums' order) -- the payload of the
 // all-reduce that follows.  Once the loop has stopped the payload is zeros, so that
 // all-reduce (enqueued ahead with the batch) cannot re-add a stale buffer.
 __global__ void shard_collect_kernel(const double* __restrict__ gpart, int64_t n, int Q,
@@ -201,7 +201,7 @@ __global__ void shard_collect_kernel(const double* __restrict__ gpart, int64_t n
   const int64_t m = n * Q;
   if (blockIdx.x == gridDim.x - 1) {
     __shared__ double red[1024];
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < 3; ++c) {  // trial slots (or, after a tiny-phase pass, difference slots 0-2)
       const double v = stopped ? 0.0 : tree_sum<1024>(losspart, nparts, stride, c, red);
       if (threadIdx.x == 0) xred[m + c] = v;
     }
@@ -330,7 +330,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
                                double rel_tol, const double* __restrict__ pre, double precise_rel, int phase,
-                               const double* __restrict__ xred, const double* __restrict__ dsum) {
+                               const double* __restrict__ xred, const double* __restrict__ dsum, int tiny_ok) {
   // xred (row-sharded loop): the all-reduced [gradient at cand0 (n Q) | trial loss sums (2)]
   // of the last pass; dsum: the all-reduced sums of a difference pass (slots 0, 1, 2)
   pdl_wait();
@@ -349,13 +349,13 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     if (lead) publish(S);
     return;
   }
-  // phase 1: the difference pass left raw losses at the two trials (columns 0, 1) and at
-  // Y (column 2); the loss at Y is re-based on it (history too), as the host path does
+  // A decision on difference sums: phase 1 (a difference pass ran for a pending decision)
+  // or, in the tiny phase, phase 0 itself (the last pass was the difference + gradient
+  // pass).  Its columns 0, 1 hold the raw losses at the two trials and column 2 the raw
+  // loss at Y; the loss at Y is re-based on it (history too), as the host path does.
+  const bool diffdec = (phase == 1) || S.tiny != 0;
   double fY = S.f;
-  if (phase == 1) {
-    pre = nullptr;
-    fY = -1.0;  // set below once loss_of is defined
-  }
+  if (phase == 1) pre = nullptr;
   // the pass's loss sums: from the reduction launch's extra CTA when it ran, else here (same order)
   if (xred && phase == 0) pre = xred + m;
   const double t0 = (xred && phase == 1) ? dsum[0] : (pre ? pre[0] : tree_sum<1024>(losspart, nparts, stride, 0, red));
@@ -380,8 +380,9 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     if (kind == kSammon) return __dmul_rn(__ddiv_rn(1.0, sum), raw);
     return raw;
   };
-  if (phase == 1) {
-    fY = loss_of(xred ? dsum[2] : tree_sum<1024>(losspart, nparts, stride, 2, red));
+  if (diffdec) {
+    const double raw_y = xred ? (phase == 1 ? dsum[2] : xred[m + 2]) : tree_sum<1024>(losspart, nparts, stride, 2, red);
+    fY = loss_of(raw_y);
     R.f = fY;
     R.pending = 0;
     if (lead) history[S.it] = fY;
@@ -393,16 +394,13 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   const double tol = precise_rel * fabs(fY);
   // ... or a tested trial whose Armijo margin is inside that resolution (the decision
   // could flip against the reference's fp64 sums): the same deferral (armijo_unresolved)
-  // (tiny mode: the pass was the gradient-only one, its losses are not trial losses: defer)
   const bool unresolved =
-      phase == 0 && precise_rel > 0.0 &&
-      (S.tiny != 0 || (fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
+      !diffdec && precise_rel > 0.0 &&
+      ((fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
        armijo_unresolved(fY, S.step, gsq, loss_of(S.pred == 0 ? t0 : t1), loss_of(S.pred == 0 ? t1 : t0), tol));
   if (unresolved && kind == kKruskal) {
     R.pending = 1;
-    // tiny mode with the step first in slot order: the first trial is all the decision
-    // needs (if it is rejected the iteration goes to the host, which evaluates both)
-    R.single = (S.tiny != 0 && S.pred == 0) ? 1 : 0;
+    R.single = 0;
     R.ndiff = S.ndiff + 1;
     if (lead) publish(R);
     return;
@@ -456,9 +454,12 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   } else if (R.it >= max_iters) {
     R.stop = 1;
   }
-  // tiny mode for the next iteration: this (difference-pass) decision changed f by less than a
-  // quarter of the resolution threshold, so the doubled step will not be resolved either
-  R.tiny = (phase == 1 && fabs(__dsub_rn(fY, f_new)) <= 0.25 * tol) ? 1 : 0;
+  // tiny mode for the next iteration: this (difference-sum) decision changed f by less than a
+  // quarter of the resolution threshold, so the doubled step will not be resolved either: the
+  // next pass is the difference + gradient pass, of the first trial only when it leads the
+  // slot order (if it is rejected the iteration goes to the host, which evaluates both)
+  R.tiny = (tiny_ok && diffdec && fabs(__dsub_rn(fY, f_new)) <= 0.25 * tol) ? 1 : 0;
+  R.single = (R.tiny != 0 && S.pred == 0) ? 1 : 0;
   if (lead) {
     history[R.it] = f_new;
     publish(R);
@@ -579,10 +580,10 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    int phase, cudaStream_t st, const double* xred, const double* dsum) {
+                    int phase, cudaStream_t st, const double* xred, const double* dsum, bool tiny_ok) {
   launch_pdl(gd_step_kernel, dim3(nsq), dim3(256), 0, st, st2, par, losspart, nparts, stride, sqprev, nsq, sqnext,
              kind, sum_sq, sum, Y, cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-             precise_rel, phase, xred, dsum);
+             precise_rel, phase, xred, dsum, tiny_ok ? 1 : 0);
   count_launch();
   check_launch("gd_step_kernel");
 }

@@ -49,11 +49,6 @@ constexpr int kTmaCand = 2;                   // trial points per loss pass (y_j
 // 16-byte shared-memory read of a D row by 8 consecutive threads covers 128
 // contiguous bytes (no bank conflicts; 8 contiguous columns per thread gave 2-way).
 __device__ __forceinline__ int tcol(int tj, int y) { return (y < 4) ? 4 * tj + y : 64 + 4 * tj + (y - 4); }
-// slot of column r in the staged column coordinates: thread tj reads slot y * kTG + tj
-__device__ __forceinline__ int tslot(int r) {
-  const int hi = r >> 6, rr = r & 63;
-  return (4 * hi + (rr & 3)) * kTG + (rr >> 2);
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -110,27 +105,38 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 
 // MODE 0: loss of up to two trial points; 1: loss + gradient at one point;
 // 2 (fused): loss of two trial points + gradient at the first (the predicted
-// Armijo acceptance, so the next iteration usually needs no gradient pass).
+// Armijo acceptance, so the next iteration usually needs no gradient pass);
+// 3 / 5: loss differences of two / the first trial (configurations Y and the scaled
+// gradient); 6 / 7 (the device loop's sub-resolution "tiny" phase): 3 / 5 plus the
+// gradient at the first trial point, from the same per-pair quantities (y_i - y_j -
+// s_0 (g_i - g_j) and the trial distance the difference needs anyway: no extra MUFU) --
+// one pass per tiny iteration instead of a difference pass and a gradient pass.
 template <int Q, int MODE, int KIND>
 __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
   pdl_wait();
   pdl_trigger();
   using namespace tma_detail;
-  constexpr bool DIFF = (MODE == 3 || MODE == 5);  // loss differences: configurations are Y and the gradient
-  constexpr int NT = (MODE == 5) ? 1 : 2;            // trial steps of a difference pass (5: the first only)
-  constexpr bool GRAD = (MODE == 1 || MODE == 2);  // gradient accumulation (of configuration 0)
+  constexpr bool DG = (MODE == 6 || MODE == 7);      // difference + gradient at the first trial point
+  constexpr bool DIFF = (MODE == 3 || MODE == 5 || DG);  // loss differences: configurations are Y and the gradient
+  constexpr int NT = (MODE == 5 || MODE == 7) ? 1 : 2;   // trial steps of a difference pass (5, 7: the first only)
+  constexpr bool GRAD = (MODE == 1 || MODE == 2 || DG);  // gradient accumulation (configuration 0 / DG: trial 0)
   constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;
   extern __shared__ __align__(128) unsigned char dyn[];
   constexpr int NS = GRAD ? kStagesGrad : kStages;
   float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
   __shared__ __align__(8) uint64_t bars[NS];
   __shared__ __align__(16) float sYi[NCM][kPT][Q];
-  __shared__ __align__(16) float sYj[2][NCM][kPT][Q];  // [block parity][cand][tslot(r)][k]: double-buffered
+  // [block parity][cand][k][column]: one coordinate of consecutive columns is contiguous, so a
+  // thread's column pairs (y, y+1) arrive as one 16-byte load per 4 columns (no register moves
+  // to form the FFMA2 operand pairs); double-buffered
+  __shared__ __align__(16) float sYj[2][NCM][Q][kPT];
   __shared__ __align__(16) float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   if (a.halt && *a.halt) return;
-  if constexpr (DIFF) {  // device loop: run only for a pending decision, in the matching width
+  if constexpr (DG) {  // device loop: run only in the tiny phase, in the matching width
+    if (a.gds && (a.gds->tiny == 0 || a.gds->stop != 0 || (a.gds->single != 0) != (NT == 1))) return;
+  } else if constexpr (DIFF) {  // device loop: run only for a pending decision, in the matching width
     if (a.gds && (a.gds->pending == 0 || a.gds->stop != 0 || (a.gds->single != 0) != (NT == 1))) return;
   }
   const int tid = threadIdx.x;
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   const int64_t J1 = min(J0 + a.chunk_len, a.nb);
   const int nblocks = static_cast<int>(J1 - J0);
   const int nhalves = kParts * nblocks;
-  const int nc = (MODE == 1) ? 1 : (MODE >= 2 ? kTmaCand : a.ncand);  // fused / difference passes: two configurations
+  const int nc = (MODE == 1) ? 1 : (MODE >= 2 ? NCM : a.ncand);  // fused / difference passes: all configurations
   const float* __restrict__ D = static_cast<const float*>(a.D);
   const float* __restrict__ W = static_cast<const float*>(a.W);
   const float delta = static_cast<float>(a.huber_delta);
@@ -162,9 +168,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     for (int h = 0; h < min(NS, nhalves); ++h) issue(h);
 
   if constexpr (Q == 2) {  // one 16-byte load per (candidate, row)
-    const int c = tid >> 7, r = tid & (kPT - 1);
+    const int r = tid & (kPT - 1);
     const int64_t i = I * kPT + r;
-    if (c < NCM) {
+    for (int c = tid >> 7; c < NCM; c += 2) {
       const double2 v = (c < nc && i < a.n) ? reinterpret_cast<const double2*>(a.Y[c])[i] : make_double2(0.0, 0.0);
       *reinterpret_cast<float2*>(&sYi[c][r][0]) = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
     }
@@ -196,16 +202,23 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
 #pragma unroll
         for (int k = 0; k < Q; ++k) rowsum[hh][x][k] = 0.f;
   }
-  float2 yj2[NCM][kMT / 2][Q];  // this thread's 8 columns as (y, y+1) pairs, loaded once per block
+  // this thread's 8 columns as (y, y+1) pairs, loaded once per block
+  constexpr int NCMR = NCM;
+  float2 yj2[NCMR][kMT / 2][Q];
   // Q = 2: thread (c = tid / 128, r = tid % 128) stages point r of candidate c
   // as one 16-byte load, prefetched a block ahead into registers
   const int sc = tid >> 7, sr = tid & (kPT - 1);
-  auto col_load = [&](int64_t J) {
+  constexpr int NSC = (NCM + 1) / 2;  // configurations staged per thread (thread c stages c, c + 2)
+  auto col_load = [&](int64_t J, int c) {
     const int64_t j = J * kPT + sr;
-    return (sc < nc && j < a.n) ? reinterpret_cast<const double2*>(a.Y[sc])[j] : make_double2(0.0, 0.0);
+    return (c < nc && j < a.n) ? reinterpret_cast<const double2*>(a.Y[c])[j] : make_double2(0.0, 0.0);
   };
-  double2 ycol = make_double2(0.0, 0.0);
-  if constexpr (Q == 2) ycol = col_load(J0);
+  double2 ycol[NSC];
+#pragma unroll
+  for (int u = 0; u < NSC; ++u) ycol[u] = make_double2(0.0, 0.0);
+  if constexpr (Q == 2)
+#pragma unroll
+    for (int u = 0; u < NSC; ++u) ycol[u] = col_load(J0, sc + 2 * u);
 
   // Barriers per block: one after the column coordinates are staged (their
   // buffer alternates, so no barrier is needed before writing it), one per
@@ -214,35 +227,36 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     const int64_t J = J0 + b;
     const int yb = b & 1;
     if constexpr (Q == 2) {
-      if (sc < NCM)
-        *reinterpret_cast<float2*>(&sYj[yb][sc][tslot(sr)][0]) =
-            make_float2(static_cast<float>(ycol.x), static_cast<float>(ycol.y));
-      if (b + 1 < nblocks) ycol = col_load(J + 1);
+#pragma unroll
+      for (int u = 0; u < NSC; ++u) {
+        const int c = sc + 2 * u;
+        if (c < NCM)
+        {
+          sYj[yb][c][0][sr] = static_cast<float>(ycol[u].x);
+          sYj[yb][c][1][sr] = static_cast<float>(ycol[u].y);
+        }
+        if (b + 1 < nblocks) ycol[u] = col_load(J + 1, c);
+      }
     } else {
       for (int e = tid; e < nc * kPT * Q; e += kThreads) {
         const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
         const int64_t j = J * kPT + r;
-        sYj[yb][c][tslot(r)][k] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+        sYj[yb][c][k][r] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int c = 0; c < NCM; ++c)
+    for (int c = 0; c < NCMR; ++c)
 #pragma unroll
-      for (int y = 0; y < kMT; y += 2) {
-        if constexpr (Q == 2) {
-          const float2 p0 = (c < nc) ? *reinterpret_cast<const float2*>(&sYj[yb][c][y * kTG + tj][0])
-                                     : make_float2(0.f, 0.f);
-          const float2 p1 = (c < nc) ? *reinterpret_cast<const float2*>(&sYj[yb][c][(y + 1) * kTG + tj][0])
-                                     : make_float2(0.f, 0.f);
-          yj2[c][y / 2][0] = make_float2(p0.x, p1.x);
-          yj2[c][y / 2][1] = make_float2(p0.y, p1.y);
-        } else {
-#pragma unroll
-          for (int k = 0; k < Q; ++k)
-            yj2[c][y / 2][k] = (c < nc) ? make_float2(sYj[yb][c][y * kTG + tj][k], sYj[yb][c][(y + 1) * kTG + tj][k])
-                                        : make_float2(0.f, 0.f);
-        }
+      for (int k = 0; k < Q; ++k) {  // columns 4tj..4tj+3 and 64+4tj..64+4tj+3: two 16-byte loads
+        const float4 lo = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][4 * tj])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 hi = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][64 + 4 * tj])
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+        yj2[c][0][k] = make_float2(lo.x, lo.y);
+        yj2[c][1][k] = make_float2(lo.z, lo.w);
+        yj2[c][2][k] = make_float2(hi.x, hi.y);
+        yj2[c][3][k] = make_float2(hi.z, hi.w);
       }
     float2 colacc2[GRAD ? kMT / 2 : 1][Q];  // column sums of columns (y, y+1)
     if constexpr (GRAD) {
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
             const float Dv = dv[y];
             const float invD = (KIND == kSammon) ? 1.f / fmaxf(Dv, FLT_MIN) : 0.f;
 #pragma unroll
-            for (int c = 0; c < NCM; ++c) {
+            for (int c = 0; c < NCMR; ++c) {
               if (c >= nc) break;
               float dy[Q];
               float d2 = 0.f;
@@ -361,10 +375,23 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
               const float st = t ? ds1 : ds0;
               const float at = st * fmaf(st, qq, -2.f * pp);
               const float dt2 = fmaxf(d0 + at, FLT_MIN);
-              const float distt = dt2 * rsqrt_mufu(dt2);
+              const float rt = rsqrt_mufu(dt2);
+              const float distt = dt2 * rt;
               const float dd = at / (distt + dist0);  // dist_t - dist_0
               const float de = dd * (dd - 2.f * e0);  // e_t^2 - e_0^2
               if (t) t1 = de; else t0 = de;
+              if constexpr (DG) {
+                if (t == 0) {  // kruskal gradient at y - s_0 g: c = -(D - dist_0') / dist_0'
+                  const float cc = keep ? -(dv[y] - distt) * rt : 0.f;
+#pragma unroll
+                  for (int k = 0; k < Q; ++k) {
+                    const float dyt = fmaf(-st, dg[k], dy[k]);
+                    rowsum[half][x][k] = fmaf(cc, dyt, rowsum[half][x][k]);
+                    float& ca = (y & 1) ? colacc2[y / 2][k].y : colacc2[y / 2][k].x;
+                    ca = fmaf(-cc, dyt, ca);
+                  }
+                }
+              }
             }
             if (keep) {
               dhalf[0] += t0;
@@ -386,13 +413,20 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
           const float2 s0v = make_float2(ds0, ds0), s1v = make_float2(ds1, ds1);
           const float2 m2 = make_float2(-2.f, -2.f);
           float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0;
+          float2 racc[DG ? Q : 1];  // DG: this row's gradient sums at the first trial point
+#pragma unroll
+          for (int k = 0; k < (DG ? Q : 1); ++k) racc[k] = make_float2(0.f, 0.f);
+          const float2 ms0v = make_float2(-ds0, -ds0);
 #pragma unroll
           for (int yy = 0; yy < kMT / 2; ++yy) {
             float2 d0 = make_float2(FLT_MIN, FLT_MIN), pp = make_float2(0.f, 0.f), qq = pp;
+            float2 dyv[Q], dgv[Q];
 #pragma unroll
             for (int k = 0; k < Q; ++k) {
               const float2 dy = f2sub(yY[k], yj2[0][yy][k]);
               const float2 dg = f2sub(yG[k], yj2[1][yy][k]);
+              dyv[k] = dy;
+              dgv[k] = dg;
               d0 = f2fma(dy, dy, d0);
               pp = f2fma(dy, dg, pp);
               qq = f2fma(dg, dg, qq);
@@ -408,12 +442,28 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
               float2 dt2 = f2add(d0, at);
               dt2.x = fmaxf(dt2.x, FLT_MIN);
               dt2.y = fmaxf(dt2.y, FLT_MIN);
-              const float2 distt = f2mul(dt2, make_float2(rsqrt_mufu(dt2.x), rsqrt_mufu(dt2.y)));
+              const float2 rt = make_float2(rsqrt_mufu(dt2.x), rsqrt_mufu(dt2.y));
+              const float2 distt = f2mul(dt2, rt);
               const float2 den = f2add(distt, dist0);
               const float2 dd = f2mul(at, make_float2(rcp_mufu(den.x), rcp_mufu(den.y)));
               const float2 de = f2mul(dd, f2fma(e0, m2, dd));
               if (t) a1 = f2add(a1, de); else a0 = f2add(a0, de);
+              if constexpr (DG) {
+                if (t == 0) {  // kruskal gradient at y - s_0 g (pairs_packed's conventions: u = e / dist)
+                  const float2 u = f2mul(f2sub(dvp[yy], distt), rt);
+#pragma unroll
+                  for (int k = 0; k < Q; ++k) {
+                    const float2 dyt = f2fma(ms0v, dgv[k], dyv[k]);
+                    racc[k] = f2fma(u, dyt, racc[k]);
+                    colacc2[yy][k] = f2fma(u, dyt, colacc2[yy][k]);
+                  }
+                }
+              }
             }
+          }
+          if constexpr (DG) {
+#pragma unroll
+            for (int k = 0; k < Q; ++k) rowsum[half][x][k] += -(racc[k].x + racc[k].y);
           }
           dhalf[0] += a0.x + a0.y;
           dhalf[1] += a1.x + a1.y;
@@ -427,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
           const float2 dvp[kMT / 2] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
                                        make_float2(v1.z, v1.w)};
 #pragma unroll
-          for (int c = 0; c < NCM; ++c) {
+          for (int c = 0; c < NCMR; ++c) {
             if (c >= nc) break;
             float2 yi2[Q];
 #pragma unroll
@@ -607,6 +657,32 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
     GMDS_TMA_SWITCH                                                                                       \
     count_launch();                                                                                       \
     check_launch("stress_tma_kernel (difference, first trial)");                                          \
+  }
+#define GMDS_TMA_DG_Q(QQ)                                                                                 \
+  case QQ:                                                                                                \
+    GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, MODE, kKruskal>,                                  \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmemGrad))); \
+    launch_pdl(stress_tma_kernel<QQ, MODE, kKruskal>, dim3(g), dim3(kThreads), kTmaSmemGrad, st, a);       \
+    break;
+#define GMDS_INSTANTIATE_TMA_DG                                                                           \
+  void launch_pass_diffgrad_f32(const PassArgs& a, int Q, bool single, cudaStream_t st) {                 \
+    if (a.kind != kKruskal) fail(GMDS_ERROR, "difference + gradient pass: kruskal only");                 \
+    const unsigned g = static_cast<unsigned>(a.nchunks);                                                  \
+    if (single) {                                                                                         \
+      constexpr int MODE = 7;                                                                             \
+      switch (Q) {                                                                                        \
+        GMDS_TMA_DG_Q(1) GMDS_TMA_DG_Q(2) GMDS_TMA_DG_Q(3)                                                \
+        default: fail(GMDS_ERROR, "difference + gradient pass: q <= 3");                                  \
+      }                                                                                                   \
+    } else {                                                                                              \
+      constexpr int MODE = 6;                                                                             \
+      switch (Q) {                                                                                        \
+        GMDS_TMA_DG_Q(1) GMDS_TMA_DG_Q(2) GMDS_TMA_DG_Q(3)                                                \
+        default: fail(GMDS_ERROR, "difference + gradient pass: q <= 3");                                  \
+      }                                                                                                   \
+    }                                                                                                     \
+    count_launch();                                                                                       \
+    check_launch("stress_tma_kernel (difference + gradient)");                                            \
   }
 #define GMDS_INSTANTIATE_TMA_FUSED                                                                        \
   void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st) {                                 \

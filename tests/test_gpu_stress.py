@@ -338,6 +338,7 @@ def test_speculative_trial_gradient_identical(monkeypatch, kind, q):
     # fp32 storage above the small-fit size: the trial pass also carries the
     # gradient of the predicted acceptance; the arithmetic per trial point is the
     # same as separate loss / gradient passes, so trajectories are bit-identical
+    monkeypatch.setenv("GMDS_NO_TINY", "1")  # the tiny phase's single pass: test_tiny_phase_one_pass
     rng = np.random.default_rng(11)
     n = 2600
     X = rng.standard_normal((n, 6)) * np.linspace(2.0, 0.5, 6)
@@ -362,6 +363,7 @@ def test_device_resident_descent_identical(monkeypatch, kind, rel_tol, iters):
     # trip) with the host loop's arithmetic: same history, coordinates,
     # iteration count and converged flag as GMDS_HOST_GD=1, through the
     # max_iters and rel_tol exits and the hand-backs to the host
+    monkeypatch.setenv("GMDS_NO_TINY", "1")  # the tiny phase's single pass: test_tiny_phase_one_pass
     rng = np.random.default_rng(21)
     n = 2400
     X = rng.standard_normal((n, 5)) * np.linspace(2.0, 0.5, 5)
@@ -486,3 +488,24 @@ def test_metric_shape_fit_properties():
     assert hb[-1] < 0.9 * hb[0]
     assert abs(G.kruskal_stress(b["coords"], D64) - b["stress"]) <= 1e-12 * b["stress"]
     assert abs(G.kruskal_stress(a["coords"], D32) - a["stress"]) <= 1e-6 * a["stress"]
+
+
+def test_tiny_phase_one_pass(monkeypatch):
+    # the device loop's sub-resolution phase: one difference + gradient pass per iteration (the
+    # gradient at the first trial from the difference pass's own per-pair quantities) instead of the
+    # fused pass + a difference pass; same decisions, trajectory to round-off, fewer passes
+    g = np.random.default_rng(78)
+    n, p = 2600, 784
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < 0.8] = 0.0
+    D = G.pairwise_matrix(X.astype(np.float32), 2.0)
+    Y0 = g.normal(0.0, 0.1, (n, 2))
+    a = G.minimize_stress(D, 2, "kruskal", max_iters=60, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    monkeypatch.setenv("GMDS_NO_TINY", "1")
+    b = G.minimize_stress(D, 2, "kruskal", max_iters=60, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    assert a["iterations"] == b["iterations"] == 60
+    h, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
+    assert np.max(np.abs(h - hb) / hb) <= 1e-7
+    assert a["passes"] < b["passes"] - 10
