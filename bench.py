@@ -420,10 +420,37 @@ def run_engine(args, rank, world, dist):
             t0 = time.perf_counter()
             e2e_call()
             etimes.append(time.perf_counter() - t0)
-        G.lib().gmds_set_stream(ctypes_void(stream.cuda_stream))
         e2e = {"value": npairs / float(np.mean(etimes)), "unit": "pairs/s", "h2d_bytes_per_step": int(X.nbytes),
                "d2h_bytes_per_step": int(Dh.nbytes), "ms_per_step": float(np.mean(etimes)) * 1e3,
                "call": "gmds_pairwise_gini (pairwise_matrix drop-in, fp64 n x n out)"}
+        del Dh
+        # the same call as a C++ caller of the reference API makes it (tools/cpp/facade_e2e.cpp):
+        # const Matrix& D = ginimds::pairwise_matrix(X, MetricSpec::gini(2)).matrix(); X an Eigen-layout
+        # (column-major) fp64 matrix, D the facade's own (pageable) host Matrix
+        try:
+            import ctypes
+
+            Lf = ctypes.CDLL(os.path.join(ROOT, "paper_2605_25124_b200", "lib", "libfacade_e2e.so"))
+            Xcm = np.asfortranarray(X.astype(np.float64))
+            secs, chk = ctypes.c_double(), ctypes.c_double()
+
+            def facade_call():
+                rc = Lf.facade_e2e(ctypes.c_void_p(Xcm.ctypes.data), ctypes.c_int64(N), ctypes.c_int64(P),
+                                   ctypes.c_double(NU), ctypes.byref(secs), ctypes.byref(chk))
+                if rc != 0:
+                    raise RuntimeError("facade_e2e failed")
+                return secs.value
+
+            facade_call()  # warm-up (pinned staging, pool)
+            ftimes = [facade_call() for _ in range(max(1, min(args.steps, 3)))]
+            e2e["facade"] = {"value": npairs / float(np.mean(ftimes)), "unit": "pairs/s",
+                             "ms_per_step": float(np.mean(ftimes)) * 1e3, "h2d_bytes_per_step": int(Xcm.nbytes),
+                             "d2h_bytes_per_step": int(8 * N * N),
+                             "call": "ginimds::pairwise_matrix(X, MetricSpec::gini(2)).matrix() (C++ facade, "
+                                     "fp64 column-major X, host Matrix D)"}
+        except (OSError, RuntimeError) as ex:
+            e2e["facade"] = {"unavailable": str(ex)}
+        G.lib().gmds_set_stream(ctypes_void(stream.cuda_stream))
 
     # ---- roofline of the dominant kernel (gini_gmd_kernel: the whole distance step is this kernel
     # plus a 12 KB LUT upload and two 4-byte flag copies).  Peak: the NOMINAL FP32/INT32 lane-op

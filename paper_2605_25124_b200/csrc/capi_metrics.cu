@@ -72,6 +72,23 @@ std::vector<double> build_lut(int d, const double* nus, int nnu) {
 }
 
 // Host X (row- or column-major) -> device row-major copy.
+// fp64 input whose every value is exactly an fp32 value (data stored as double by the caller,
+// e.g. an Eigen::MatrixXd of image intensities): the same values as fp32, so the kernels that
+// need exact 32-bit keys (the linear-weight, general-nu and merge paths) serve it.  The
+// distances are functions of the values only, so nothing but the dispatch changes.
+const void* narrow_exact_f32(const void* X, gmds_dtype& xt, int64_t m, std::vector<float>& buf) {
+  if (xt != GMDS_F64) return X;
+  const double* x = static_cast<const double*>(X);
+  buf.resize(static_cast<size_t>(m));
+  for (int64_t k = 0; k < m; ++k) {
+    const float f = static_cast<float>(x[k]);
+    if (static_cast<double>(f) != x[k] || (x[k] == 0.0 && std::signbit(x[k]))) return X;  // keep fp64
+    buf[static_cast<size_t>(k)] = f;
+  }
+  xt = GMDS_F32;
+  return buf.data();
+}
+
 DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
                                   cudaStream_t st) {
   const size_t bytes = static_cast<size_t>(n) * p * dtype_size(xt);
@@ -286,6 +303,8 @@ gmds_status gmds_pairwise_gini(const void* X, gmds_dtype xt, gmds_layout lx, int
     if (p < 1) fail(GMDS_INVALID_INPUT, "pairwise_matrix: need at least 1 column");
     require_device();
     Stream st;
+    std::vector<float> narrowed;
+    X = narrow_exact_f32(X, xt, n * p, narrowed);
     DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
     DevBuf<int> flag(1);
     GMDS_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), st.s));

@@ -151,6 +151,35 @@ void pack_full(const double* dfull, int64_t n, gmds_dtype storage, void* dpacked
   check_launch("pack_kernel");
 }
 
+// rows [r0, r1) of the full matrix (zero diagonal) into out[(i - r0) * n + j]
+template <typename TD>
+__global__ void unpack_rows_kernel(const TD* __restrict__ packed, int64_t n, int64_t nb, int64_t r0, int64_t r1,
+                                   double* __restrict__ out) {
+  const int64_t total = (r1 - r0) * n;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = r0 + e / n, j = e % n;
+    double v = 0.0;
+    if (i != j) {
+      const int64_t lo = i < j ? i : j, hi = i < j ? j : i;
+      v = static_cast<double>(packed[packed_offset(lo, hi, nb)]);
+    }
+    out[e] = v;
+  }
+}
+
+void unpack_rows(const void* dpacked, gmds_dtype storage, int64_t n, int64_t r0, int64_t r1, double* dout,
+                 cudaStream_t st) {
+  const int64_t nb = ceil_div(n, kPT);
+  const unsigned g = grid_for((r1 - r0) * n);
+  if (storage == GMDS_F32)
+    unpack_rows_kernel<float><<<g, 256, 0, st>>>(static_cast<const float*>(dpacked), n, nb, r0, r1, dout);
+  else
+    unpack_rows_kernel<double><<<g, 256, 0, st>>>(static_cast<const double*>(dpacked), n, nb, r0, r1, dout);
+  count_launch();
+  check_launch("unpack_rows_kernel");
+}
+
 void unpack_full(const void* dpacked, gmds_dtype storage, int64_t n, double* dfull, bool square, cudaStream_t st) {
   const int64_t nb = ceil_div(n, kPT);
   if (storage == GMDS_F32)

@@ -17,6 +17,9 @@ struct DStats {
 
 void pack_full(const double* dfull, int64_t n, gmds_dtype storage, void* dpacked, cudaStream_t st);
 void unpack_full(const void* dpacked, gmds_dtype storage, int64_t n, double* dfull, bool square, cudaStream_t st);
+// rows [r0, r1) of the full fp64 matrix, row-major into dout ((r1 - r0) x n)
+void unpack_rows(const void* dpacked, gmds_dtype storage, int64_t n, int64_t r0, int64_t r1, double* dout,
+                 cudaStream_t st);
 // statistics over packed blocks [blk_lo, blk_hi) (blk_hi < 0: all)
 DStats packed_stats(const void* dpacked, gmds_dtype storage, int64_t n, cudaStream_t st, int64_t blk_lo = 0,
                     int64_t blk_hi = -1);

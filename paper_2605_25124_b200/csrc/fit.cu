@@ -20,6 +20,7 @@
 #include <map>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -1233,6 +1234,70 @@ void dmat_finish(gmds_dmat* d, cudaStream_t st) {  // stats used by resolve_para
   d->stats = true;
 }
 
+// DistanceMatrix::matrix() for a device handle: the full fp64 matrix into caller (pageable)
+// host memory without a device-side n x n image or a pageable cudaMemcpy.  Row stripes of
+// ~64 MB are unpacked on the device, copied into pinned staging (two buffers, so stripe s + 1
+// moves while stripe s is copied out) and spread into the destination by host threads.
+void download_full(const gmds_dmat* d, double* dst, cudaStream_t st) {
+  const int64_t n = d->n;
+  const int64_t R = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(64) << 20) / (8 * n)));
+  const size_t stripe = static_cast<size_t>(R * n);
+  struct Pinned {
+    double* p[2] = {nullptr, nullptr};
+    size_t cap = 0;
+    ~Pinned() {
+      for (double* q : p)
+        if (q) cudaFreeHost(q);
+    }
+  };
+  static thread_local Pinned pin;
+  if (pin.cap < stripe) {
+    for (double*& q : pin.p) {
+      if (q) cudaFreeHost(q);
+      q = nullptr;
+      GMDS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&q), stripe * sizeof(double), cudaHostAllocDefault));
+    }
+    pin.cap = stripe;
+  }
+  DevBuf<double> dev[2];
+  for (auto& b : dev) b.alloc(stripe);
+  cudaEvent_t ev[2];
+  for (auto& e : ev) GMDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct Ev {
+    cudaEvent_t* e;
+    ~Ev() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } evg{ev};
+  const int64_t nstripes = ceil_div(n, R);
+  auto enqueue = [&](int64_t s) {
+    const int b = static_cast<int>(s & 1);
+    const int64_t r0 = s * R, r1 = std::min(n, r0 + R);
+    unpack_rows(d->ptr(), d->storage, n, r0, r1, dev[b].get(), st);
+    GMDS_CUDA(cudaMemcpyAsync(pin.p[b], dev[b].get(), static_cast<size_t>((r1 - r0) * n) * sizeof(double),
+                              cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaEventRecord(ev[b], st));
+  };
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  enqueue(0);
+  for (int64_t s = 0; s < nstripes; ++s) {
+    if (s + 1 < nstripes) enqueue(s + 1);  // its buffer's previous copy-out (stripe s - 1) is done
+    const int b = static_cast<int>(s & 1);
+    GMDS_CUDA(cudaEventSynchronize(ev[b]));
+    const int64_t r0 = s * R, r1 = std::min(n, r0 + R);
+    const size_t count = static_cast<size_t>((r1 - r0) * n);
+    const double* src = pin.p[b];
+    double* out = dst + static_cast<size_t>(r0 * n);
+    const size_t per = (count + hw - 1) / hw;
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < hw && t * per < count; ++t)
+      th.emplace_back([=] { std::memcpy(out + t * per, src + t * per, std::min(per, count - t * per) * sizeof(double)); });
+    std::memcpy(out, src, std::min(per, count) * sizeof(double));
+    for (auto& x : th) x.join();
+  }
+}
+
 }  // namespace gmds
 
 using namespace gmds;
@@ -1293,6 +1358,8 @@ gmds_status gmds_dmat_gini(const void* X, gmds_dtype xt, gmds_layout lx, int64_t
     check_finite_host(X, xt, n * p, "gen_gini_directed");
     require_device();
     Stream st;
+    std::vector<float> narrowed;
+    X = narrow_exact_f32(X, xt, n * p, narrowed);
     DevBuf<unsigned char> dX = upload_rows(X, xt, lx, n, p, st.s);
     dmat_gini_common(dX.get(), xt, n, p, nu, storage, out, st.s);
   });
@@ -1316,10 +1383,7 @@ gmds_status gmds_dmat_download(const gmds_dmat* d, double* D_full) {
     if (!d) fail(GMDS_INVALID_INPUT, "dmat_download: null handle");
     if (d->sharded()) fail(GMDS_INVALID_INPUT, "dmat_download: row-sharded distance matrix");
     Stream st;
-    DevBuf<double> full(static_cast<size_t>(d->n * d->n));
-    unpack_full(d->ptr(), d->storage, d->n, full.get(), false, st.s);
-    GMDS_CUDA(cudaMemcpyAsync(D_full, full.get(), sizeof(double) * d->n * d->n, cudaMemcpyDeviceToHost, st.s));
-    GMDS_CUDA(cudaStreamSynchronize(st.s));
+    download_full(d, D_full, st.s);
   });
 }
 

@@ -40,6 +40,8 @@ void check_finite_host(const void* X, gmds_dtype xt, int64_t count, const char* 
 std::vector<double> build_lut(int d, const double* nus, int nnu);
 DevBuf<unsigned char> upload_rows(const void* X, gmds_dtype xt, gmds_layout lx, int64_t n, int64_t p,
                                   cudaStream_t st);
+// fp64 host input exactly representable in fp32 -> fp32 copy in buf (xt updated), else X unchanged
+const void* narrow_exact_f32(const void* X, gmds_dtype& xt, int64_t m, std::vector<float>& buf);
 // Fused nu-sweep scoring request: instead of storing D_nu, return per nu
 // num = sum (|y_i - y_j| - D_nu)^2 and den = sum D_nu^2 over i < j (host arrays).
 struct ScoreSpec {
