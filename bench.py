@@ -65,7 +65,7 @@ def ops_per_pair(p, nnu):
 
 def load_traffic():
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             t = json.load(f)
         g = lambda k: t[k]["dram_read_bytes"] + t[k]["dram_write_bytes"]
         return g("gini_gmd_kernel"), g("stress_tma_kernel_fused")

@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
         const int e = lane + 32 * u;
         al[u] = be[u] = 0.f;
         pI[u] = pJ[u] = kMaxC;  // sentinel: qcount -> s, never stored
+        if (u == 1 && s <= 32) break;  // warp-uniform: the second element slot is empty
         if (e < s) {
           const int f = F[e];
           const int w = f >> 5;
@@ -255,8 +256,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
       int rI[2], rJ[2];
       double z[2];
       int mneg = 0, mpos = 0;
+      z[1] = 0.0;
+      rI[1] = rJ[1] = s;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
+        if (u == 1 && s <= 32) break;  // warp-uniform
         rI[u] = qcount(QM, QM + 16, pI[u], s);
         rJ[u] = qcount(QM + 8, QM + 24, pJ[u], s);
         const bool live = lane + 32 * u < s;
@@ -311,6 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
       const bool even = (s & 1) == 0;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
+        if (u == 1 && s <= 32) break;  // warp-uniform
         const int e = lane + 32 * u;
         if (e >= s) continue;
         const double av = al[u], bv = be[u];

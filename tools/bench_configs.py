@@ -110,6 +110,9 @@ def c3():
     ref = O.gini_pairs(Xd, I[keep], J[keep], 2.0)
     full = G.pairwise_gini(X[:600], [2.0])[0]
     err = float(np.max(np.abs(full - O.pairwise_matrix(Xd[:600], 2.0))) / np.max(full))
+    # the sampled pairs against the GPU's own full matrix (the fit's D, unpacked)
+    Dfull = Dm64.download()
+    pair_err = float(np.max(np.abs(Dfull[I[keep], J[keep]] - ref)) / np.max(Dfull))
     rows = 8
     tr = None
     if R.load() is not None:
@@ -122,6 +125,7 @@ def c3():
             "fp64_storage": {"fit_s": tf64, "iterations": e64["iterations"], "final_stress": e64["stress"],
                              "iters_per_s": e64["iterations"] / tf64},
             "D_maxnorm_err_600rows": err, "ref_cpu_distance_s_extrapolated": tr, "checked_pairs": int(keep.sum()),
+            "checked_pairs_maxnorm_err": pair_err,
             "ref_pairs_mean": float(np.mean(ref))}
 
 
