@@ -1043,6 +1043,8 @@ bool small_fit(const gmds_dmat* D, int q, const gmds_stress_cfg& cfg, const Reso
     if (!D->dense) {
       auto b = std::make_shared<DevBuf<double>>(static_cast<size_t>(n * n));
       unpack_full(D->ptr(), D->storage, n, b->get(), false, st);
+      // complete before publishing: another thread's fit on another stream may read it next
+      GMDS_CUDA(cudaStreamSynchronize(st));
       D->dense = b;
     }
     dense = D->dense;

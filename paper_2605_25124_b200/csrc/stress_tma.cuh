@@ -24,11 +24,14 @@
 #include "f32x2.cuh"
 #include "stress_pass.cuh"
 
+#ifndef GMDS_TMA_MINB_FUSED
+#define GMDS_TMA_MINB_FUSED 2
+#endif
 #ifndef GMDS_TMA_MINB
 // CTAs per SM: 3 for loss passes, 2 for gradient passes (128 registers).  At
 // Q >= 3 the gradient passes spill (448 B at Q = 3) yet stay faster than one
 // CTA per SM without spills (n = 20000: 24.2 vs 28.5 ms per 50 iterations)
-#define GMDS_TMA_MINB(MODE, Q) ((MODE) == 0 ? 3 : 2)
+#define GMDS_TMA_MINB(MODE, Q) ((MODE) == 0 ? 3 : ((MODE) == 2 ? GMDS_TMA_MINB_FUSED : 2))
 #endif
 
 namespace gmds {
@@ -39,8 +42,11 @@ namespace tma_detail {
 #define GMDS_TMA_PARTS 2  // 4 bands of 16 KB measured 13.1 vs 12.9 ms per 50 iterations (more barriers)
 #endif
 constexpr int kParts = GMDS_TMA_PARTS;  // TMA units per 128x128 block (row bands of kPT / kParts rows)
-constexpr int kStages = kParts;         // loss passes: one block's bytes in flight (3 CTAs/SM: 192 KB per SM)
-constexpr int kStagesGrad = kParts;  // gradient passes: 64 KB per CTA (3 x 32 KB left one CTA per SM: 288 vs 207 us)
+#ifndef GMDS_TMA_STAGES
+#define GMDS_TMA_STAGES GMDS_TMA_PARTS
+#endif
+constexpr int kStages = GMDS_TMA_STAGES;  // loss passes: one block's bytes in flight (3 CTAs/SM: 192 KB per SM)
+constexpr int kStagesGrad = GMDS_TMA_STAGES;  // gradient passes: 64 KB per CTA (3 x 32 KB left one CTA per SM: 288 vs 207 us)
 constexpr int kHalfRows = kPT / kParts;        // rows per TMA unit ("half" below: one band)
 constexpr int kHalfFloats = kHalfRows * kPT;  // 4096 floats = 16 KB at 4 parts
 constexpr int kMR = kHalfRows / kTG;          // micro-tile rows per band (ti*kMR + x)

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgmds.so")
+LIB_PATH = os.environ.get("GMDS_LIB_PATH") or os.path.join(HERE, "lib", "libgmds.so")  # override: experiments
 
 OK, INVALID_INPUT, INVALID_CONFIG, DEGENERATE_INPUT, NUMERIC_FAILURE, ERROR, CUDA_ERROR, NCCL_ERROR = range(8)
 F32, F64 = 0, 1

@@ -509,3 +509,23 @@ def test_tiny_phase_one_pass(monkeypatch):
     h, hb = np.array(a["stress_history"]), np.array(b["stress_history"])
     assert np.max(np.abs(h - hb) / hb) <= 1e-7
     assert a["passes"] < b["passes"] - 10
+
+
+def test_metric_shape_fp32_gradient_accuracy():
+    # the fused passes accumulate each thread's row sums over up to 8 blocks (1024 pairs) in fp32
+    # before the fp64 reduction: at the metric shape the Kruskal gradient with fp32 storage stays
+    # within 1e-5 (max-normalised) of the fp64-storage gradient (itself oracle-checked)
+    torch = pytest.importorskip("torch")
+    g = np.random.default_rng(2025)
+    n, p = 20000, 784
+    X = g.integers(0, 256, size=(n, p)).astype(np.float64) / 255.0
+    X += g.normal(0.0, 0.1, size=(n, p))
+    np.clip(X, 0.0, 1.0, out=X)
+    X[g.random((n, p)) < 0.8] = 0.0
+    dX = torch.from_numpy(X.astype(np.float32)).cuda()
+    D32 = G.dmat_gini_device(dX.data_ptr(), G.F32, n, p, 2.0, G.F32)
+    D64 = G.dmat_gini_device(dX.data_ptr(), G.F32, n, p, 2.0, G.F64)
+    Y = g.normal(0.0, 30.0, (n, 2))
+    a = G.stress_gradient("kruskal", Y, D32)
+    b = G.stress_gradient("kruskal", Y, D64)
+    assert np.max(np.abs(a - b)) <= 1e-5 * np.max(np.abs(b))
