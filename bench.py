@@ -341,12 +341,15 @@ def run_engine(args, rank, world, dist):
     # ---- stress: S Kruskal iterations on the packed matrix of this step.  One GPU: the
     # device-controlled fit.  Several ranks: the row-sharded device-controlled fit of libgmds.
     Y0 = np.random.default_rng(SEED).normal(0.0, 0.1, (N, Q))
-    if world > 1:
+    # GMDS_BENCH_SHARDED=1 runs the multi-GPU code path at one rank too (a 1-rank NCCL
+    # communicator): the glue below is then exercised on a single-GPU box
+    if world > 1 or os.environ.get("GMDS_BENCH_SHARDED"):
         # libgmds multi-GPU path: an NCCL communicator (unique id shared over torch.distributed),
         # this rank's share of D's packed blocks, and the device-resident sharded fit with one
         # in-stream all-reduce of [gradient | loss sums] per pass
         uid = [G.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
         comm = G.comm_init_nccl(uid[0], world, rank)
         Dm = G.dmat_gini_sharded(comm, dX.data_ptr(), G.F32, N, P, NU, G.F32)
 

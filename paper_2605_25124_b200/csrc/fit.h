@@ -26,7 +26,7 @@ struct Engine {
   bool rows_mode;
   cudaStream_t st;
   int64_t n = 0, nb = 0, nchunks = 0;
-  int64_t chunk_len = 4;  // 128x128 blocks per CTA of a tiled pass
+  int64_t chunk_len = 1;  // 128x128 blocks per CTA of a tiled pass (set from chunk_blocks(nb): up to 8)
   int64_t passes = 0;  // passes over D issued by this engine
   int64_t stride_row = 0, stride_col = 0;
   const void* W = nullptr;

@@ -133,7 +133,14 @@ __global__ void reduce_rows_kernel(const TP* __restrict__ rowpart, const TP* __r
 // term is a contiguous 128 x Q run, read coalesced -- and combine_kernel adds
 // the kRedGroups group sums of each entry in order.  Fixed order throughout.
 // TP: the partials' type (fp32 from the TMA passes, fp64 from the fp64 pass).
-constexpr int kRedGroups = 8;
+#ifndef GMDS_RED_GROUPS
+#define GMDS_RED_GROUPS 8
+#endif
+#ifndef GMDS_RED_UNROLL
+#define GMDS_RED_UNROLL 4
+#endif
+constexpr int kRedGroups = GMDS_RED_GROUPS;
+constexpr int kRedUnroll = GMDS_RED_UNROLL;
 template <typename TP>
 __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* __restrict__ colpart,
                                      const int64_t* __restrict__ strip_first, int64_t nb, int Q,
@@ -156,15 +163,15 @@ __global__ void reduce_groups_kernel(const TP* __restrict__ rowpart, const TP* _
   const int64_t run = static_cast<int64_t>(kPT) * Q;
   double acc = 0.0;
   int64_t t = t0;
-  for (; t + 4 <= t1; t += 4) {  // four loads in flight, added in order
-    TP v[4];
+  for (; t + kRedUnroll <= t1; t += kRedUnroll) {  // kRedUnroll loads in flight, added in order
+    TP v[kRedUnroll];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kRedUnroll; ++u) {
       const int64_t tt = t + u;
       v[u] = ((tt < nrow) ? rowpart + (c0 + tt) * run : colpart + blk_index(tt - nrow, R, nb) * run)[e];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) acc += static_cast<double>(v[u]);
+    for (int u = 0; u < kRedUnroll; ++u) acc += static_cast<double>(v[u]);
   }
   for (; t < t1; ++t) {
     const TP* src = (t < nrow) ? rowpart + (c0 + t) * run : colpart + blk_index(t - nrow, R, nb) * run;
