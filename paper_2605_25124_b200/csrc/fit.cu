@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -427,6 +428,9 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   // the tiny phase's difference + gradient pass (q <= 3); GMDS_NO_TINY=1: every sub-resolution
   // decision takes the fused pass and a difference pass (the host loop's two passes)
   const bool tiny_ok = dev_diff && Q <= 3 && !std::getenv("GMDS_NO_TINY");
+  // solo passes (GdState::solo): slot 0 only, while the full step keeps being accepted on resolved sums;
+  // single device only (a miss costs a host loss pass); GMDS_NO_SOLO=1: always the two-trial fused pass
+  const bool solo_ok = !comm && !std::getenv("GMDS_NO_SOLO");
   for (;;) {
     const int batch = std::max(1, std::min(16, max_iters - issued));
     for (int k = 0; k < batch; ++k) {
@@ -435,7 +439,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
                        sq2.get() + (sqp ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
                        cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
                        rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st, xr, comm ? dsum.get() : nullptr,
-                       tiny_ok);
+                       tiny_ok, solo_ok);
         par ^= 1;
         if (phase == 0 && dev_diff) {
           dpa.gds = gdst.get() + par;
@@ -449,7 +453,9 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       }
       sqp ^= 1;
       b.halt = &gdst.get()[par].halt_fused;
-      launch_pass_fused_f32(b, Q, st);
+      b.gds = gdst.get() + par;
+      launch_pass_fused_f32(b, Q, st);              // both trials (exits when the state says solo)
+      if (solo_ok) launch_pass_solo_f32(b, Q, st);  // slot 0 only (runs when it does)
       if (tiny_ok) {  // tiny phase: one difference + gradient pass (the kernels exit unless tiny)
         PassArgs gp = args(kind, delta);
         gp.Y[0] = Y.get();
@@ -467,10 +473,20 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
     issued += batch;
     GMDS_CUDA(cudaMemcpyAsync(&S, gdst.get() + par, sizeof S, cudaMemcpyDeviceToHost, st));
     GMDS_CUDA(cudaStreamSynchronize(st));
+    if (std::getenv("GMDS_TRACE"))
+      std::fprintf(stderr, "[gmds] device_gd: it=%d step=%.3e f=%.9g pred=%d tiny=%d solo=%d pending=%d stop=%d miss=%d\n",
+                   S.it, S.step, S.f, S.pred, S.tiny, S.solo, S.pending, S.stop, S.solo_miss);
     if (S.stop != 0) break;
   }
   // passes: the prime plus one per decision that continued (all accepted ones but a final stop)
   passes += (S.it - it) - (S.stop == 1 ? 1 : 0) + S.ndiff;  // + the difference passes run on the device
+  if (S.stop == 2 && S.solo_miss) {
+    // the solo pass left the half step's loss unevaluated: one loss pass over both trial points
+    // (slot 0 is recomputed to the same bits; losspart column 0 stays the loss at cand0)
+    const double* Ys[2] = {cand[0].get(), cand[1].get()};
+    const std::vector<double> raws = loss_raw(kind, delta, Ys, 2);
+    S.t1 = raws[1];
+  }
   if (S.it > it) {
     std::vector<double> h(static_cast<size_t>(S.it - it));
     GMDS_CUDA(cudaMemcpyAsync(h.data(), hist.get() + it + 1, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -773,6 +789,9 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
       stalled = true;
       break;
     }
+    if (std::getenv("GMDS_TRACE"))
+      std::fprintf(stderr, "[gmds] host gd: it=%d step=%.4e slot=%d pred=%d have_grad=%d from_device=%d f_new=%.12g\n", it,
+                   step, acc_c, pred, have_grad ? 1 : 0, decided_on_device ? 1 : 0, f_new);
     std::swap(E.Y, E.cand[acc_c]);
     if (have_grad) std::swap(E.graw, E.gnext);
     r.history.push_back(f_new);

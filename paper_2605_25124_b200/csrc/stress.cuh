@@ -48,6 +48,11 @@ struct GdState {
                                 // runs the gradient pass only, and its decision defers directly
   int halt_fused, halt_grad;    // halt flags of the next fused pass / gradient-only pass
   int single;                   // the pending decision's difference pass evaluates the first trial only
+  int solo;                     // the next trial pass evaluates slot 0 only (loss + gradient at cand0): the
+                                // full step was accepted with a resolved margin last time (pred == 0), so
+                                // the half step's loss would go unread; a miss hands the iteration to the host
+  int solo_miss;                // stop == 2 after a solo pass: t1 (the loss at cand1) was not evaluated
+  int streak;                   // consecutive full-step acceptances on resolved sums (solo needs 2)
 };
 
 struct Steps {
@@ -92,7 +97,7 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
                     int phase, cudaStream_t st, const double* xred = nullptr, const double* dsum = nullptr,
-                    bool tiny_ok = false);
+                    bool tiny_ok = false, bool solo_ok = false);
 // row-sharded device loop: gradient groups -> xred[0, nQ), the pass's trial-loss sums -> xred[nQ, nQ + 2)
 void launch_shard_collect(const double* gpart, int64_t n, int Q, const double* losspart, int64_t nparts, int stride,
                           double* xred, const int* halt, cudaStream_t st);
@@ -100,6 +105,8 @@ size_t reduce_rows_scratch(int64_t nb, int q);
 void launch_sum_parts(const double* part, int64_t count, int stride, int m, double* out, cudaStream_t st);
 // fp32 storage, q <= 4: losses at a.Y[0], a.Y[1] and the gradient partials at a.Y[0] in one pass
 void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st);
+// device loop: loss + gradient at a.Y[0] only; runs when a.gds->solo (the fused pass then exits)
+void launch_pass_solo_f32(const PassArgs& a, int Q, cudaStream_t st);
 // fp32 storage, fp64 arithmetic: loss of up to kMaxCand points
 void launch_pass_precise(const PassArgs& a, int Q, cudaStream_t st);
 // fp32 storage, e^2 kinds: losspart slots (sum of e_t^2 - e_0^2 at Y - s_t g for t = 0, 1; sum e_0^2 at Y)

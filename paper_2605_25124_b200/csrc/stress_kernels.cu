@@ -337,7 +337,8 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                const double* __restrict__ gpart, int Q,
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
                                double rel_tol, const double* __restrict__ pre, double precise_rel, int phase,
-                               const double* __restrict__ xred, const double* __restrict__ dsum, int tiny_ok) {
+                               const double* __restrict__ xred, const double* __restrict__ dsum, int tiny_ok,
+                               int solo_ok) {
   // xred (row-sharded loop): the all-reduced [gradient at cand0 (n Q) | trial loss sums (2)]
   // of the last pass; dsum: the all-reduced sums of a difference pass (slots 0, 1, 2)
   pdl_wait();
@@ -382,6 +383,11 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   R.t0 = t0;
   R.t1 = t1;
   R.gsq = gsq;
+  R.solo = 0;
+  R.solo_miss = 0;
+  R.streak = 0;  // (kept only by the accepting path below)
+  // the pass behind this decision was a solo pass: t1 is not there (see GdState::solo)
+  const bool solo = S.solo != 0 && phase == 0 && S.tiny == 0;
   auto loss_of = [&](double raw) {
     if (kind == kKruskal) return sqrt(__ddiv_rn(raw, sum_sq));
     if (kind == kSammon) return __dmul_rn(__ddiv_rn(1.0, sum), raw);
@@ -401,30 +407,6 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   const double tol = precise_rel * fabs(fY);
   // ... or a tested trial whose Armijo margin is inside that resolution (the decision
   // could flip against the reference's fp64 sums): the same deferral (armijo_unresolved)
-  const bool unresolved =
-      !diffdec && precise_rel > 0.0 &&
-      ((fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
-       armijo_unresolved(fY, S.step, gsq, loss_of(S.pred == 0 ? t0 : t1), loss_of(S.pred == 0 ? t1 : t0), tol));
-  if (unresolved && kind == kKruskal) {
-    R.pending = 1;
-    R.single = 0;
-    R.ndiff = S.ndiff + 1;
-    if (lead) publish(R);
-    return;
-  }
-  if (gsq > 0.0 && !unresolved) {
-    for (int c = 0; c < 2; ++c) {  // step, then step/2 (the reference's order)
-      const double sc = (c == 0) ? S.step : __dmul_rn(S.step, 0.5);
-      const int slot = (S.pred == 0) ? c : 1 - c;
-      const double fc = loss_of(slot == 0 ? t0 : t1);
-      if (fc <= __dsub_rn(fY, __dmul_rn(__dmul_rn(1e-4, sc), gsq))) {
-        acc_c = c;
-        f_new = fc;
-        sc_acc = sc;
-        break;
-      }
-    }
-  }
   // the raw gradient at cand0 (combine_kernel's sums, in its order) -> gnext
   auto combine = [&]() {
     if (xred) {  // row-sharded: already combined and all-reduced
@@ -444,9 +426,55 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
       gnext[k] = a;
     }
   };
+  // solo (slot 0 = the full step, tested first): the first clause needs t1 when t0 is within
+  // tol of f, and the second needs it when the full step is rejected outside tol -- both are
+  // misses (below); otherwise the outcome is the two-trial one, bit for bit
+  bool solo_missed = false;
+  if (solo) {
+    const double thr = __dsub_rn(fY, __dmul_rn(__dmul_rn(1e-4, S.step), gsq));
+    const double f0 = loss_of(t0);
+    const bool near_f = precise_rel > 0.0 && fabs(f0 - fY) <= tol;
+    const bool near_thr = precise_rel > 0.0 && fabs(__dsub_rn(f0, thr)) <= tol;
+    solo_missed = near_f || (!near_thr && !(f0 <= thr)) || !(gsq > 0.0);
+  }
+  if (solo_missed) {  // the host evaluates the loss at cand1 and decides (stop = 2)
+    R.stop = 2;
+    R.tiny = 0;
+    R.solo_miss = 1;
+    if (lead) publish(R);
+    combine();
+    return;
+  }
+  const bool unresolved =
+      !diffdec && precise_rel > 0.0 &&
+      (solo ? armijo_unresolved(fY, S.step, gsq, loss_of(t0), loss_of(t0), tol)
+            : ((fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
+               armijo_unresolved(fY, S.step, gsq, loss_of(S.pred == 0 ? t0 : t1), loss_of(S.pred == 0 ? t1 : t0),
+                                 tol)));
+  if (unresolved && kind == kKruskal) {
+    R.pending = 1;
+    R.single = 0;
+    R.ndiff = S.ndiff + 1;
+    if (lead) publish(R);
+    return;
+  }
+  if (gsq > 0.0 && !unresolved) {
+    for (int c = 0; c < (solo ? 1 : 2); ++c) {  // step, then step/2 (the reference's order)
+      const double sc = (c == 0) ? S.step : __dmul_rn(S.step, 0.5);
+      const int slot = (S.pred == 0) ? c : 1 - c;
+      const double fc = loss_of(slot == 0 ? t0 : t1);
+      if (fc <= __dsub_rn(fY, __dmul_rn(__dmul_rn(1e-4, sc), gsq))) {
+        acc_c = c;
+        f_new = fc;
+        sc_acc = sc;
+        break;
+      }
+    }
+  }
   if (acc_c < 0 || ((S.pred == 0) ? acc_c : 1 - acc_c) != 0) {  // host takes this iteration
     R.stop = 2;
     R.tiny = 0;
+    R.solo_miss = solo ? 1 : 0;  // (solo: only an unresolved non-Kruskal decision gets here)
     if (lead) publish(R);
     combine();
     return;
@@ -467,6 +495,12 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   // slot order (if it is rejected the iteration goes to the host, which evaluates both)
   R.tiny = (tiny_ok && diffdec && fabs(__dsub_rn(fY, f_new)) <= 0.25 * tol) ? 1 : 0;
   R.single = (R.tiny != 0 && S.pred == 0) ? 1 : 0;
+  // solo for the next pass: the full step was just accepted on resolved fp32 sums with room to
+  // spare (a change of more than 4 tol), so the doubled step's half-step loss will go unread
+  R.streak = (!diffdec && S.pred == 0 && (precise_rel <= 0.0 || fabs(__dsub_rn(fY, f_new)) > 4.0 * tol))
+                 ? S.streak + 1
+                 : 0;
+  R.solo = (solo_ok && R.tiny == 0 && R.stop == 0 && R.streak >= 2) ? 1 : 0;
   if (lead) {
     history[R.it] = f_new;
     publish(R);
@@ -587,10 +621,11 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
-                    int phase, cudaStream_t st, const double* xred, const double* dsum, bool tiny_ok) {
+                    int phase, cudaStream_t st, const double* xred, const double* dsum, bool tiny_ok,
+                    bool solo_ok) {
   launch_pdl(gd_step_kernel, dim3(nsq), dim3(256), 0, st, st2, par, losspart, nparts, stride, sqprev, nsq, sqnext,
              kind, sum_sq, sum, Y, cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-             precise_rel, phase, xred, dsum, tiny_ok ? 1 : 0);
+             precise_rel, phase, xred, dsum, tiny_ok ? 1 : 0, solo_ok ? 1 : 0);
   count_launch();
   check_launch("gd_step_kernel");
 }

@@ -3,4 +3,5 @@
 
 namespace gmds {
 GMDS_INSTANTIATE_TMA(true)
+GMDS_INSTANTIATE_TMA_SOLO
 }  // namespace gmds

@@ -24,6 +24,12 @@
 #include "f32x2.cuh"
 #include "stress_pass.cuh"
 
+#ifndef GMDS_CSPLIT_DG
+#define GMDS_CSPLIT_DG 0
+#endif
+#ifndef GMDS_CSPLIT_Q2
+#define GMDS_CSPLIT_Q2 0
+#endif
 #ifndef GMDS_TMA_MINB_FUSED
 #define GMDS_TMA_MINB_FUSED 2
 #endif
@@ -127,6 +133,15 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   constexpr int NT = (MODE == 5 || MODE == 7) ? 1 : 2;   // trial steps of a difference pass (5, 7: the first only)
   constexpr bool GRAD = (MODE == 1 || MODE == 2 || DG);  // gradient accumulation (configuration 0 / DG: trial 0)
   constexpr int NCM = (MODE == 1) ? 1 : kTmaCand;
+  // Q >= 3: a thread's 8 columns are processed as two groups of 4 (columns 4tj..4tj+3, then
+  // 64+4tj..) per band, so only one group's coordinates and column sums are live at a time
+  // (the full 8-column tile needs > 128 registers at Q = 3 and spilled 328-944 B per thread)
+  // (GMDS_CSPLIT_DG / GMDS_CSPLIT_Q2: the same split for the q <= 2 difference + gradient passes /
+  // for every q <= 2 loss and gradient mode -- all of them, so their loss sums stay bit-identical)
+  constexpr bool CSPLIT = (Q >= 3) || (DG && GMDS_CSPLIT_DG) || (!DIFF && GMDS_CSPLIT_Q2);
+  constexpr int NCH = CSPLIT ? 2 : 1;        // column groups per band
+  constexpr int NYY = (kMT / 2) / NCH;       // column pairs (y, y+1) per group
+  constexpr int NY = 2 * NYY;                // columns per group
   extern __shared__ __align__(128) unsigned char dyn[];
   constexpr int NS = GRAD ? kStagesGrad : kStages;
   float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
@@ -140,6 +155,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   if (a.halt && *a.halt) return;
+  if constexpr (MODE == 1 || MODE == 2) {  // device loop: the solo pass (MODE 1) or the two-trial fused pass
+    if (a.gds && (a.gds->solo != 0) != (MODE == 1)) return;
+  }
   if constexpr (DG) {  // device loop: run only in the tiny phase, in the matching width
     if (a.gds && (a.gds->tiny == 0 || a.gds->stop != 0 || (a.gds->single != 0) != (NT == 1))) return;
   } else if constexpr (DIFF) {  // device loop: run only for a pending decision, in the matching width
@@ -210,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   }
   // this thread's 8 columns as (y, y+1) pairs, loaded once per block
   constexpr int NCMR = NCM;
-  float2 yj2[NCMR][kMT / 2][Q];
+  float2 yj2[NCMR][NYY][Q];
   // Q = 2: thread (c = tid / 128, r = tid % 128) stages point r of candidate c
   // as one 16-byte load, prefetched a block ahead into registers
   const int sc = tid >> 7, sr = tid & (kPT - 1);
@@ -251,26 +269,36 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       }
     }
     __syncthreads();
+    float2 colacc2[GRAD ? NYY : 1][Q];  // column sums of columns (y, y+1)
+    auto load_cols = [&](int ch) {  // this group's column coordinates (and zeroed column sums)
 #pragma unroll
-    for (int c = 0; c < NCMR; ++c)
+      for (int c = 0; c < NCMR; ++c)
 #pragma unroll
-      for (int k = 0; k < Q; ++k) {  // columns 4tj..4tj+3 and 64+4tj..64+4tj+3: two 16-byte loads
-        const float4 lo = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][4 * tj])
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 hi = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][64 + 4 * tj])
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-        yj2[c][0][k] = make_float2(lo.x, lo.y);
-        yj2[c][1][k] = make_float2(lo.z, lo.w);
-        yj2[c][2][k] = make_float2(hi.x, hi.y);
-        yj2[c][3][k] = make_float2(hi.z, hi.w);
+        for (int k = 0; k < Q; ++k) {  // columns 4tj..4tj+3 and 64+4tj..64+4tj+3: 16-byte loads
+          if constexpr (!CSPLIT) {
+            const float4 lo = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][4 * tj])
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 hi = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][64 + 4 * tj])
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            yj2[c][0][k] = make_float2(lo.x, lo.y);
+            yj2[c][1][k] = make_float2(lo.z, lo.w);
+            yj2[c][NYY - 2][k] = make_float2(hi.x, hi.y);
+            yj2[c][NYY - 1][k] = make_float2(hi.z, hi.w);
+          } else {
+            const float4 v = (c < nc) ? *reinterpret_cast<const float4*>(&sYj[yb][c][k][64 * ch + 4 * tj])
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            yj2[c][0][k] = make_float2(v.x, v.y);
+            yj2[c][1][k] = make_float2(v.z, v.w);
+          }
+        }
+      if constexpr (GRAD) {
+#pragma unroll
+        for (int y = 0; y < NYY; ++y)
+#pragma unroll
+          for (int k = 0; k < Q; ++k) colacc2[y][k] = make_float2(0.f, 0.f);
       }
-    float2 colacc2[GRAD ? kMT / 2 : 1][Q];  // column sums of columns (y, y+1)
-    if constexpr (GRAD) {
-#pragma unroll
-      for (int y = 0; y < kMT / 2; ++y)
-#pragma unroll
-        for (int k = 0; k < Q; ++k) colacc2[y][k] = make_float2(0.f, 0.f);
-    }
+    };
+    if constexpr (!CSPLIT) load_cols(0);
     const int64_t blk = blk_index(I, J, a.nb);
     const bool edge = (I == J) || (J * kPT + kPT > a.n);
 #pragma unroll
@@ -286,18 +314,23 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       float dhalf[3] = {0.f, 0.f, 0.f};  // DIFF: this half's sums
       // the row loop, instantiated per block kind (edge / packed / generic) so the
       // interior-block version is a branch-free, fully unrolled loop over the rows
-      auto row_loop = [&](auto mode_tag) {
+      auto row_loop = [&](auto mode_tag, auto ch_tag) {
       constexpr int MODE_ROWS = decltype(mode_tag)::value;  // 0 packed, 1 edge, 2 generic
+      constexpr int CH = decltype(ch_tag)::value;           // column group (CSPLIT), else 0
+      constexpr int Y0 = CSPLIT ? 4 * CH : 0;               // first column slot (tcol) of the group
 #pragma unroll
       for (int x = 0; x < kMR; ++x) {
         const int rloc = ti * kMR + x;           // row within the half
         const int ri = half * kHalfRows + rloc;  // row within the block
-        const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + 4 * tj);
-        const float4 v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + 64 + 4 * tj);
-        const float dv[kMT] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-        float wv[kMT];
+        const float4 v0 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + 64 * CH + 4 * tj);
+        float4 v1 = v0;
+        if constexpr (!CSPLIT) v1 = *reinterpret_cast<const float4*>(Ds + rloc * kPT + 64 + 4 * tj);
+        float dv[NY];
+        dv[0] = v0.x, dv[1] = v0.y, dv[2] = v0.z, dv[3] = v0.w;
+        if constexpr (!CSPLIT) dv[NY - 4] = v1.x, dv[NY - 3] = v1.y, dv[NY - 2] = v1.z, dv[NY - 1] = v1.w;
+        float wv[NY];
 #pragma unroll
-        for (int y = 0; y < kMT; ++y) wv[y] = Wb ? Wb[rloc * kPT + tcol(tj, y)] : 1.f;
+        for (int y = 0; y < NY; ++y) wv[y] = Wb ? Wb[rloc * kPT + tcol(tj, Y0 + y)] : 1.f;
         float yi[NCM][Q];
 #pragma unroll
         for (int c = 0; c < NCM; ++c) {
@@ -314,8 +347,8 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
         auto pairs = [&](auto edge_tag) {
           constexpr bool EDGE = decltype(edge_tag)::value;
 #pragma unroll
-          for (int y = 0; y < kMT; ++y) {
-            const int rj = tcol(tj, y);
+          for (int y = 0; y < NY; ++y) {
+            const int rj = tcol(tj, Y0 + y);
             bool keep = true;
             if constexpr (EDGE) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
             const float Dv = dv[y];
@@ -359,8 +392,8 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
         // lose them below one ulp of e).
         auto pairs_diff = [&]() {
 #pragma unroll
-          for (int y = 0; y < kMT; ++y) {
-            const int rj = tcol(tj, y);
+          for (int y = 0; y < NY; ++y) {
+            const int rj = tcol(tj, Y0 + y);
             bool keep = true;
             if (edge) keep = (J * kPT + rj < a.n) && (I != J || ri < rj);
             float dy[Q], dg[Q];
@@ -408,8 +441,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
         };
         // DIFF on interior blocks: the same on column pairs (y, y+1) with packed fp32 math
         auto pairs_diff_packed = [&]() {
-          const float2 dvp[kMT / 2] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
-                                       make_float2(v1.z, v1.w)};
+          float2 dvp[NYY];
+          dvp[0] = make_float2(v0.x, v0.y), dvp[1] = make_float2(v0.z, v0.w);
+          if constexpr (!CSPLIT) dvp[NYY - 2] = make_float2(v1.x, v1.y), dvp[NYY - 1] = make_float2(v1.z, v1.w);
           float2 yY[Q], yG[Q];
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
@@ -424,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
           for (int k = 0; k < (DG ? Q : 1); ++k) racc[k] = make_float2(0.f, 0.f);
           const float2 ms0v = make_float2(-ds0, -ds0);
 #pragma unroll
-          for (int yy = 0; yy < kMT / 2; ++yy) {
+          for (int yy = 0; yy < NYY; ++yy) {
             float2 d0 = make_float2(FLT_MIN, FLT_MIN), pp = make_float2(0.f, 0.f), qq = pp;
             float2 dyv[Q], dgv[Q];
 #pragma unroll
@@ -480,8 +514,9 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
         // clamp: coincident points give dy = 0 and add exactly 0)
         auto pairs_packed = [&]() {
           constexpr bool KR = (KIND == kKruskal);
-          const float2 dvp[kMT / 2] = {make_float2(v0.x, v0.y), make_float2(v0.z, v0.w), make_float2(v1.x, v1.y),
-                                       make_float2(v1.z, v1.w)};
+          float2 dvp[NYY];
+          dvp[0] = make_float2(v0.x, v0.y), dvp[1] = make_float2(v0.z, v0.w);
+          if constexpr (!CSPLIT) dvp[NYY - 2] = make_float2(v1.x, v1.y), dvp[NYY - 1] = make_float2(v1.z, v1.w);
 #pragma unroll
           for (int c = 0; c < NCMR; ++c) {
             if (c >= nc) break;
@@ -493,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
 #pragma unroll
             for (int k = 0; k < Q; ++k) racc[k] = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int yy = 0; yy < kMT / 2; ++yy) {
+            for (int yy = 0; yy < NYY; ++yy) {
               float2 dy2[Q];
               float2 d2 = make_float2(FLT_MIN, FLT_MIN);
 #pragma unroll
@@ -541,19 +576,37 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
           pairs(std::false_type{});
       }
       };
-      if (edge)
-        row_loop(std::integral_constant<int, 1>{});
-      else if ((KIND == kKruskal || KIND == kGuttman) && !Wb)
-        row_loop(std::integral_constant<int, 0>{});
-      else
-        row_loop(std::integral_constant<int, 2>{});
+      auto group = [&](auto ch_tag) {
+        constexpr int CH = decltype(ch_tag)::value;
+        if constexpr (CSPLIT) load_cols(CH);
+        if (edge)
+          row_loop(std::integral_constant<int, 1>{}, ch_tag);
+        else if ((KIND == kKruskal || KIND == kGuttman) && !Wb)
+          row_loop(std::integral_constant<int, 0>{}, ch_tag);
+        else
+          row_loop(std::integral_constant<int, 2>{}, ch_tag);
+        if constexpr (CSPLIT && GRAD) {  // this group's column sums of the band -> sRed (each cell one thread's)
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            float4* dst = reinterpret_cast<float4*>(sRed + (k * kTG + ti) * kPT + 64 * CH + 4 * tj);
+            float4 v = make_float4(colacc2[0][k].x, colacc2[0][k].y, colacc2[1][k].x, colacc2[1][k].y);
+            if (half != 0) {
+              const float4 o = *dst;
+              v.x += o.x, v.y += o.y, v.z += o.z, v.w += o.w;
+            }
+            *dst = v;
+          }
+        }
+      };
+      group(std::integral_constant<int, 0>{});
+      if constexpr (CSPLIT) group(std::integral_constant<int, 1>{});
 #pragma unroll
       for (int c = 0; c < NCM; ++c) lossacc[c] += static_cast<double>(lhalf[c].x) + static_cast<double>(lhalf[c].y);
       if constexpr (DIFF) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) diffacc[c] += static_cast<double>(dhalf[c]);
       }
-      if constexpr (GRAD) {
+      if constexpr (GRAD && !CSPLIT) {
         if (half == kParts - 1) {
 #pragma unroll
           for (int k = 0; k < Q; ++k) {  // columns 4tj..+3 and 64+4tj..+3: two 16-byte stores
@@ -696,6 +749,13 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
     GMDS_TMA_SWITCH                                                                                       \
     count_launch();                                                                                       \
     check_launch("stress_tma_kernel (fused)");                                                            \
+  }
+#define GMDS_INSTANTIATE_TMA_SOLO                                                                         \
+  void launch_pass_solo_f32(const PassArgs& a, int Q, cudaStream_t st) {                                  \
+    constexpr int MODE = 1;                                                                               \
+    GMDS_TMA_SWITCH                                                                                       \
+    count_launch();                                                                                       \
+    check_launch("stress_tma_kernel (solo)");                                                             \
   }
 #define GMDS_INSTANTIATE_TMA(GR)                                                                          \
   template <>                                                                                             \

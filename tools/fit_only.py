@@ -12,15 +12,16 @@ from paper_2605_25124_b200 import gmds as G  # noqa: E402
 
 n = int(os.environ.get("FIT_N", "20000"))
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+q = int(os.environ.get("FIT_Q", "2"))
 X = make_image_like(n, 784)
 dX = torch.from_numpy(X).cuda()
 D = G.dmat_gini_device(dX.data_ptr(), G.F32, n, 784, 2.0, G.F32)
-Y0 = np.random.default_rng(2605).normal(0.0, 0.1, (n, 2))
+Y0 = np.random.default_rng(2605).normal(0.0, 0.1, (n, q))
 ts = []
 for _ in range(3):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    e = G.minimize_stress(D, 2, "kruskal", max_iters=iters, rel_tol=1e-300, Y0=Y0)
+    e = G.minimize_stress(D, q, "kruskal", max_iters=iters, rel_tol=1e-300, Y0=Y0)
     e1.record()
     e1.synchronize()
     ts.append(e0.elapsed_time(e1))
