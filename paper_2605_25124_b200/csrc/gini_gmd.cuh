@@ -43,6 +43,8 @@ struct GmdArgs {
   const double* s1;      // per row: sum of values
   const double* tm;      // per row: sum_k v_(k) k
   const uint32_t* tiew;  // per row, 8 words: bit g = (v_(g) == v_(g+1)) (general kernel's tie groups)
+  const uint8_t* bkt;    // per row, 256 bytes: bkt[b] = #{sorted values in a bucket below b} (gini_gmd2_kernel)
+  const float* bscale;   // per row: bucket(v) = min(255, int(v * bscale)), bscale = 256 / (the row's largest value)
 };
 
 namespace gmd_detail {
@@ -367,6 +369,339 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
     __syncthreads();
   }
 }
+
+// ---------------------------------------------------------------------------
+// gini_gmd2_kernel: the same arithmetic as gini_gmd_kernel (every fp64 term and the
+// order it is added in are unchanged, so results are bit-identical), with three
+// changes to the work around it (round 2, profiles/r1_gini_gmd_lines_n4000.txt:
+// F extraction 13%, the 8-probe search 11% of the warp instructions):
+//   * F lists are built for 8 pairs at a time by 4 lanes per pair (each lane walks
+//     every fourth mask word and writes the (row-i index, row-j index) byte pairs of
+//     its common features at its group-prefix offset), instead of one warp-wide scan
+//     and compaction per pair; the element phase reads its list entry directly;
+//   * the lower bound of |z| in a sorted row comes from a 256-bucket table per row
+//     (bkt/bscale, built once per matrix by row_bucket_kernel) and a short scan inside
+//     the bucket, instead of an 8-probe binary search;
+//   * the panel keeps the sorted values and the position map only (feature-order
+//     values are sv[pmap[k]]), which pays for the lists and the tables in shared memory.
+// Rows with more than 255 nonzeros take the overflow list (bucket counters are bytes).
+namespace gmd2_detail {
+constexpr int kBatch = 8;      // pairs per extraction batch (4 lanes each)
+constexpr int kFLStride = 66;  // u16 per list: 64 entries + pad (33 words: lists start on distinct banks)
+constexpr int kMaxC2 = 255;    // max nonzeros per staged row
+// per-warp scratch (8-byte words): QM[32] u32 (16) | PQi[72] | PQj[72] | ZL[2][64] | lists (8 x 66 u16 = 132)
+constexpr int kOffPQi2 = 16, kOffPQj2 = 88, kOffZL2 = 160, kOffFL2 = 288;
+constexpr int kWarpWords2 = kOffFL2 + (kBatch * kFLStride * 2 + 7) / 8;
+}  // namespace gmd2_detail
+
+template <typename TO, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, TO* __restrict__ out) {
+  using namespace gmd_detail;
+  using namespace gmd2_detail;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const SplitArgs& sa = ga.s;
+  const GiniTileArgs& a = sa.g;
+  const int d = a.d;
+  const int W = sa.W;
+  const int stride = sa.maxnnz;  // panel stride (<= kMaxC2): rows with more nonzeros overflow
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  // ---- shared memory
+  double* wscr = reinterpret_cast<double*>(smem_raw) + warp * kWarpWords2;
+  uint32_t* QM = reinterpret_cast<uint32_t*>(wscr);  // qm_i[8] qm_j[8] qp_i[8] qp_j[8]
+  double* PQi = wscr + kOffPQi2;
+  double* PQj = wscr + kOffPQj2;
+  double* ZL = wscr + kOffZL2;  // z on F, stored twice (list order): circular reads without a wrap
+  uint16_t* FL = reinterpret_cast<uint16_t*>(wscr + kOffFL2);  // [kBatch][kFLStride]: ii | jj << 8
+  double* otile = reinterpret_cast<double*>(smem_raw) + kWarps * kWarpWords2;  // [nnu][32][33]
+  double* rs1 = otile + static_cast<size_t>(a.nnu) * kTile * (kTile + 1);
+  double* rtm = rs1 + kRows;
+  int64_t* rbase = reinterpret_cast<int64_t*>(rtm + kRows);
+  int* rcnt = reinterpret_cast<int*>(rbase + kRows);
+  float* rscale = reinterpret_cast<float*>(rcnt + kRows);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(rscale + kRows);  // [64][W]
+  uint16_t* spre = reinterpret_cast<uint16_t*>(smask + kRows * W);
+  uint32_t* ssv = reinterpret_cast<uint32_t*>(spre + ((kRows * W + 1) & ~1));  // [64][stride] sorted value bits
+  uint16_t* spm = reinterpret_cast<uint16_t*>(ssv + kRows * stride);            // [64][stride] sorted position
+  uint8_t* sbk = reinterpret_cast<uint8_t*>(spm + ((kRows * stride + 1) & ~1));  // [64][256] bucket starts
+  const uint32_t* gsv = reinterpret_cast<const uint32_t*>(ga.svs);
+  const double h = 0.5 * static_cast<double>(d + 1);
+  const int tstride = kTile + 1;
+  const int g4 = lane >> 2, sub = lane & 3;
+
+  for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
+    int64_t I, J;
+    decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
+    const int64_t i0 = I * kTile, j0 = J * kTile;
+    for (int e = threadIdx.x; e < kRows * W; e += blockDim.x) {
+      const int r = e / W, w = e - (e / W) * W;
+      const int64_t row = (r < kTile) ? i0 + r : j0 + (r - kTile);
+      smask[e] = (row < a.n) ? sa.masks[row * W + w] : 0u;
+      spre[e] = (row < a.n) ? sa.prefix[row * W + w] : uint16_t(0);
+    }
+    for (int r = warp; r < kRows; r += kWarps) {
+      const int64_t row = (r < kTile) ? i0 + r : j0 + (r - kTile);
+      int cnt = 0;
+      int64_t b = 0;
+      if (row < a.n) {
+        b = sa.rowptr[row];
+        cnt = static_cast<int>(sa.rowptr[row + 1] - b);
+        for (int k = lane; k < cnt && k < stride; k += 32) {
+          ssv[r * stride + k] = gsv[b + k];
+          spm[r * stride + k] = ga.pmap[b + k];
+        }
+        const uint32_t* gb = reinterpret_cast<const uint32_t*>(ga.bkt) + row * 64;
+        uint32_t* sb = reinterpret_cast<uint32_t*>(sbk) + r * 64;
+        sb[lane] = gb[lane];
+        sb[lane + 32] = gb[lane + 32];
+      }
+      if (lane == 0) {
+        rcnt[r] = cnt;
+        rbase[r] = b;
+        rs1[r] = (row < a.n) ? ga.s1[row] : 0.0;
+        rtm[r] = (row < a.n) ? ga.tm[row] : 0.0;
+        rscale[r] = (row < a.n) ? ga.bscale[row] : 0.f;
+      }
+    }
+    __syncthreads();
+
+    for (int t0 = 0; warp + kWarps * t0 < kTile * kTile; t0 += kBatch) {
+      // ---- F lists of this batch: 4 lanes per pair, every fourth mask word each
+      int stat;  // the pair's |F|, or 0x100: overflow list, 0x200: not a pair of this tile
+      {
+        const int kg = warp + kWarps * (t0 + g4);
+        bool valid = kg < kTile * kTile;
+        const int rg = valid ? (kg >> 5) : 0, cg = valid ? (kg & 31) : 0;
+        valid = valid && (j0 + cg < a.n) && (i0 + rg < j0 + cg);
+        const uint32_t* mi = smask + rg * W;
+        const uint32_t* mj = smask + (kTile + cg) * W;
+        int cnt = 0;
+        if (valid)
+          for (int w = sub; w < W; w += 4) cnt += __popc(mi[w] & mj[w]);
+        int incl = cnt;
+        int o = __shfl_up_sync(0xffffffffu, incl, 1, 4);
+        if (sub >= 1) incl += o;
+        o = __shfl_up_sync(0xffffffffu, incl, 2, 4);
+        if (sub >= 2) incl += o;
+        const int sg = __shfl_sync(0xffffffffu, incl, 3, 4);
+        const bool ok = valid && sg <= kCap && rcnt[rg] <= stride && rcnt[kTile + cg] <= stride;
+        if (ok) {
+          int off = incl - cnt;
+          uint16_t* fl = FL + g4 * kFLStride;
+          const uint16_t* pim = spre + rg * W;
+          const uint16_t* pjm = spre + (kTile + cg) * W;
+          for (int w = sub; w < W; w += 4) {
+            const uint32_t wa = mi[w], wb = mj[w];
+            uint32_t m = wa & wb;
+            const int bi = pim[w], bj = pjm[w];
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1u;
+              const uint32_t lo = (1u << bit) - 1u;
+              fl[off++] = static_cast<uint16_t>((bi + __popc(wa & lo)) | ((bj + __popc(wb & lo)) << 8));
+            }
+          }
+        }
+        stat = !valid ? 0x200 : (ok ? sg : 0x100);
+      }
+      __syncwarp();
+
+      for (int gg = 0; gg < kBatch; ++gg) {
+        const int st = __shfl_sync(0xffffffffu, stat, gg * 4);
+        if (st & 0x200) continue;  // warp-uniform
+        const int k0 = warp + kWarps * (t0 + gg);
+        const int r = k0 >> 5, c = k0 & 31;
+        const int64_t gi = i0 + r, gj = j0 + c;
+        const int ri = r, rj = kTile + c;
+        const int ci = rcnt[ri], cj = rcnt[rj];
+        double* ot = otile + r * tstride + c;
+        if (st & 0x100) {  // overflow list: the exact full-sort kernel
+          if (lane == 0) {
+            const unsigned long long slot = atomicAdd(sa.ovf_count, 1ull);
+            if (static_cast<int64_t>(slot) < sa.ovf_cap) {
+              sa.ovf_pairs[2 * slot] = gi;
+              sa.ovf_pairs[2 * slot + 1] = gj;
+            }
+            for (int v = 0; v < a.nnu; ++v) ot[v * kTile * tstride] = -1.0;
+          }
+          continue;
+        }
+        const int s = st;
+        const uint16_t* fl = FL + gg * kFLStride;
+        if (lane < 16) QM[lane] = 0u;
+        __syncwarp();
+        const uint32_t* svi = ssv + ri * stride;
+        const uint32_t* svj = ssv + rj * stride;
+        const uint16_t* pmi = spm + ri * stride;
+        const uint16_t* pmj = spm + rj * stride;
+        // ---- F's values and sorted positions in both rows; position masks
+        float al[2], be[2];
+        int pI[2], pJ[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = lane + 32 * u;
+          al[u] = be[u] = 0.f;
+          pI[u] = pJ[u] = kMaxC;  // sentinel: qcount -> s, never stored
+          if (u == 1 && s <= 32) break;  // warp-uniform: the second element slot is empty
+          if (e < s) {
+            const uint32_t pk = fl[e];
+            pI[u] = pmi[pk & 255u];
+            pJ[u] = pmj[pk >> 8];
+            al[u] = __uint_as_float(svi[pI[u]]);
+            be[u] = __uint_as_float(svj[pJ[u]]);
+            atomicOr(QM + (pI[u] >> 5), 1u << (pI[u] & 31));
+            atomicOr(QM + 8 + (pJ[u] >> 5), 1u << (pJ[u] & 31));
+          }
+        }
+        __syncwarp();
+        {  // word prefixes of the two masks (groups of 8 lanes)
+          const uint32_t wv = (lane < 16) ? QM[lane] : 0u;
+          const int pc = __popc(wv);
+          int x = pc;
+#pragma unroll
+          for (int dd = 1; dd < 8; dd <<= 1) {
+            const int o = __shfl_up_sync(0xffffffffu, x, dd, 8);
+            if ((lane & 7) >= dd) x += o;
+          }
+          if (lane < 16) QM[16 + lane] = static_cast<uint32_t>(x - pc);
+        }
+        __syncwarp();
+        // ---- position-order ranks; F's values scattered in that order
+        int rI[2], rJ[2];
+        double z[2];
+        int mneg = 0, mpos = 0;
+        z[1] = 0.0;
+        rI[1] = rJ[1] = s;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && s <= 32) break;  // warp-uniform
+          rI[u] = qcount(QM, QM + 16, pI[u], s);
+          rJ[u] = qcount(QM + 8, QM + 24, pJ[u], s);
+          const bool live = lane + 32 * u < s;
+          if (live) {
+            PQi[1 + rI[u]] = static_cast<double>(al[u]);
+            PQj[1 + rJ[u]] = static_cast<double>(be[u]);
+          }
+          z[u] = static_cast<double>(al[u]) - static_cast<double>(be[u]);
+          if (live) {
+            ZL[lane + 32 * u] = z[u];
+            ZL[lane + 32 * u + s] = z[u];
+          }
+          mneg += __popc(__ballot_sync(0xffffffffu, z[u] < 0.0));
+          mpos += __popc(__ballot_sync(0xffffffffu, z[u] > 0.0));
+        }
+        __syncwarp();
+        {  // prefix sums PQ[k] = sum of the first k values in position order
+          const int t1a = 1 + 2 * lane, t1b = t1a + 1;
+          const double a0 = (t1a <= s) ? PQi[t1a] : 0.0, a1 = (t1b <= s) ? PQi[t1b] : 0.0;
+          const double b0 = (t1a <= s) ? PQj[t1a] : 0.0, b1 = (t1b <= s) ? PQj[t1b] : 0.0;
+          const double ea = warp_incl(a0 + a1, lane) - (a0 + a1);
+          const double eb = warp_incl(b0 + b1, lane) - (b0 + b1);
+          __syncwarp();
+          if (t1a <= s) {
+            PQi[t1a] = ea + a0;
+            PQj[t1a] = eb + b0;
+          }
+          if (t1b <= s) {
+            PQi[t1b] = ea + a0 + a1;
+            PQj[t1b] = eb + b0 + b1;
+          }
+          if (lane == 0) {
+            PQi[0] = 0.0;
+            PQj[0] = 0.0;
+          }
+        }
+        __syncwarp();
+        const int nP = ci - s + mpos, nN = cj - s + mneg;
+        const double kp = static_cast<double>(1 + nN + (d - nP - nN)) - h, kn = 1.0 - h;
+        const double* sufi = ga.suf + rbase[ri];
+        const double* sufj = ga.suf + rbase[rj];
+        const double s1j = rs1[rj];
+        double acc = 0.0;
+        if (lane == 0) acc = kp * rs1[ri] - kn * s1j + rtm[ri] - (static_cast<double>(cj - 1) * s1j - rtm[rj]);
+        const double sumQi = PQi[s];
+        const double wneg = static_cast<double>(s - mpos);  // |S_ab-| + |Z0|
+        const int half = (s - 1) >> 1;
+        const bool even = (s & 1) == 0;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && s <= 32) break;  // warp-uniform
+          const int e = lane + 32 * u;
+          if (e >= s) continue;
+          const double av = al[u], bv = be[u];
+          // pairs of row i touching F (PM(S_a)) and of row j (minima, PM(S_b))
+          const double si1 = (pI[u] + 1 < ci) ? __ldg(sufi + pI[u] + 1) : 0.0;
+          const double sj0 = __ldg(sufj + pJ[u]);
+          acc += av * static_cast<double>(rI[u] - pI[u]) - si1 - kp * av;
+          acc += (s1j - sj0) + bv * static_cast<double>((cj - 1 - pJ[u]) - (s - 1 - rJ[u])) + kn * bv;
+          const double zz = z[u];
+          // PM(Z) pieces
+          double g0 = 0.0, g1 = 0.0;  // two chains: DADD latency
+          const double* zr = ZL + e + 1;
+          int tq = 0;
+          for (; tq + 1 < half; tq += 2) {
+            g0 += fabs(zz - zr[tq]);
+            g1 += fabs(zz - zr[tq + 1]);
+          }
+          if (tq < half) g0 += fabs(zz - zr[tq]);
+          if (even) g1 += 0.5 * fabs(zz - zr[half]);
+          const double gsum = g0 + g1;
+          acc += 0.5 * gsum + 0.5 * static_cast<double>(s - 1) * zz;
+          if (zz == 0.0) continue;
+          // zz's pairs with the other row's row-only values: #{row values < |zz|} from the
+          // row's bucket table and a scan inside the bucket (sign-selected row)
+          const bool pos = zz > 0.0;
+          const double mg = fabs(zz);
+          const float f = __double2float_rz(mg);
+          const uint32_t tt = __float_as_uint(f) + ((static_cast<double>(f) != mg) ? 1u : 0u);
+          const int prow = pos ? ri : rj;
+          const int n = pos ? ci : cj;
+          const uint32_t* sb = ssv + prow * stride;
+          const uint8_t* tb = sbk + prow * 256;
+          const int bk = min(255, __float2int_rz(f * rscale[prow]));
+          int lb = tb[bk];
+          const int end = (bk < 255) ? static_cast<int>(tb[bk + 1]) : n;
+          while (lb < end && sb[lb] < tt) ++lb;
+          const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
+          const double sl = (lb < n) ? __ldg((pos ? sufi : sufj) + lb) : 0.0;
+          if (pos)
+            acc += (kp - wneg) * zz + zz * static_cast<double>(lb - ql) + sl - sumQi + PQi[ql];
+          else
+            acc += kn * zz - ((s1j - sl) - PQj[ql] + mg * static_cast<double>((cj - lb) - (s - ql)));
+        }
+#pragma unroll
+        for (int dd = 16; dd > 0; dd >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, dd);
+        if (lane == 0) {
+          const double val = clamp_nonneg(acc);
+          ot[0] = val;
+          for (int v = 1; v < a.nnu; ++v) ot[v * kTile * tstride] = val;
+          if (isinf(val)) atomicOr(a.flag, 1);
+        }
+        __syncwarp();
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    tile_epilogue<TO>(a, otile, kTile, tstride, i0, j0, out, nullptr, nullptr);
+    __syncthreads();
+  }
+}
+
+inline size_t gmd2_smem(int W, int maxnnz, int nnu, int nwarps) {
+  using namespace gmd_detail;
+  using namespace gmd2_detail;
+  return static_cast<size_t>(nwarps) * kWarpWords2 * 8 + static_cast<size_t>(nnu) * kTile * (kTile + 1) * 8 +
+         kRows * (8 + 8 + 8 + 4 + 4) + kRows * W * 4 + ((kRows * W + 1) & ~1) * 2 +
+         static_cast<size_t>(kRows) * maxnnz * 4 + ((static_cast<size_t>(kRows) * maxnnz + 1) & ~size_t(1)) * 2 +
+         kRows * 256 + 16;
+}
+
+// per-row bucket tables of the sorted values (gini_gmd2_kernel's search)
+void launch_row_buckets(const float* svs, const int64_t* rowptr, int64_t n, uint8_t* bkt, float* bscale,
+                        cudaStream_t st);
+void launch_gini_gmd2(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
+                      cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // General-nu kernel on the same panels (nu not in {2, 3}, nnu <= 4): every

@@ -349,12 +349,27 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     if (gmd_smem(rs.W, gmd_stride, nnu, gmd_warps) > gmd_budget) gmd_warps = 0;
   }
   if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd_warps = std::atoi(e);
+  // nu in {2, 3}: gini_gmd2_kernel (batched F lists, bucket search; rows of <= 255 nonzeros staged);
+  // GMDS_GMD_V1=1: the round-1 kernel
+  const bool gmd2 = linear && !std::getenv("GMDS_GMD_V1");
+  int gmd2_warps = 0, gmd2_stride = std::min(std::max(1, rs.maxnnz), gmd2_detail::kMaxC2);
+  if (gmd2) {
+    for (int nw : {28, 24})
+      if (!gmd2_warps && gmd2_smem(rs.W, gmd2_stride, nnu, nw) <= gmd_budget) gmd2_warps = nw;
+    if (!gmd2_warps) {
+      gmd2_warps = 24;
+      while (gmd2_stride > 32 && gmd2_smem(rs.W, gmd2_stride, nnu, gmd2_warps) > gmd_budget) gmd2_stride -= 8;
+      if (gmd2_smem(rs.W, gmd2_stride, nnu, gmd2_warps) > gmd_budget) gmd2_warps = 0;
+    }
+    if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd2_warps = std::atoi(e);
+  }
+  const bool use2 = gmd2 && gmd2_warps > 0;
   // other nu (at most 4 per launch, store mode): the general counting kernel on the same panels
   const bool general = !linear && score == nullptr && nnu <= 4 && !std::getenv("GMDS_NO_GEN");
   if ((linear || general) && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 && gmd_warps > 0) {
     // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh);
     // other nu: midranks counted from the same structures, one LUT pass (gini_gen_kernel)
-    const size_t gsm = gmd_smem(rs.W, gmd_stride, nnu, gmd_warps);
+    const size_t gsm = use2 ? gmd2_smem(rs.W, gmd2_stride, nnu, gmd2_warps) : gmd_smem(rs.W, gmd_stride, nnu, gmd_warps);
     a.tile = gmd_detail::kTile;
     a.nbt = ceil_div(n, a.tile);
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
@@ -367,7 +382,7 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     ga.s.rowptr = rs.rowptr.get();
     ga.s.vals = rs.vals.get();
     ga.s.W = rs.W;
-    ga.s.maxnnz = gmd_stride;  // panel stride; longer rows overflow
+    ga.s.maxnnz = use2 ? gmd2_stride : gmd_stride;  // panel stride; longer rows overflow
     ga.s.sparse = 1;
     ga.pmap = rs.pmap.get();
     ga.svs = reinterpret_cast<const float*>(rs.svs.get());
@@ -375,6 +390,17 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     ga.s1 = rs.s1.get();
     ga.tm = rs.tm.get();
     ga.tiew = rs.tiew.get();
+    DevBuf<uint8_t> bkt;
+    DevBuf<float> bscale;
+    if (use2) {  // per-row bucket tables of the sorted values
+      bkt.alloc(static_cast<size_t>(n) * 256);
+      bscale.alloc(static_cast<size_t>(n));
+      launch_row_buckets(ga.svs, rs.rowptr.get(), n, bkt.get(), bscale.get(), st);
+      count_launch();
+      check_launch("row_bucket_kernel");
+      ga.bkt = bkt.get();
+      ga.bscale = bscale.get();
+    }
     const int64_t shard_pairs = (a.tile_end - a.tile_begin) * static_cast<int64_t>(a.tile) * a.tile;
     ga.s.ovf_cap = std::min<int64_t>(shard_pairs, int64_t(1) << 20);
     DevBuf<int64_t> ovf(static_cast<size_t>(2 * ga.s.ovf_cap));
@@ -385,7 +411,9 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     chunked(a, [&](GiniTileArgs& g) {
       ga.s.g = g;
       const unsigned blk = static_cast<unsigned>(std::min<int64_t>(g.tile_end - g.tile_begin, int64_t(1) << 30));
-      if (linear)
+      if (use2)
+        launch_gini_gmd2(ga, dD, ot, gsm, blk, gmd2_warps, st);
+      else if (linear)
         launch_gini_gmd(ga, dD, ot, gsm, blk, gmd_warps, st);
       else
         launch_gini_gen(ga, dD, ot, gsm, blk, gmd_warps, st);
