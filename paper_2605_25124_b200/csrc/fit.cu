@@ -431,15 +431,20 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   // solo passes (GdState::solo): slot 0 only, while the full step keeps being accepted on resolved sums;
   // single device only (a miss costs a host loss pass); GMDS_NO_SOLO=1: always the two-trial fused pass
   const bool solo_ok = !comm && !std::getenv("GMDS_NO_SOLO");
+  // slot-1 acceptances, further halvings and solo misses decided on the device (GdState::fix / rt);
+  // GMDS_NO_ONDEV=1: those iterations go back to the host loop
+  const bool ondev = !std::getenv("GMDS_NO_ONDEV");
   for (;;) {
-    const int batch = std::max(1, std::min(16, max_iters - issued));
+    // units per batch: an iteration takes one unit, or two when it needs a fix / re-trial unit
+    const int left = max_iters - S.it;
+    const int batch = std::max(1, std::min(16, left + (ondev ? std::min(left, 4) : 0)));
     for (int k = 0; k < batch; ++k) {
       for (int phase = 0; phase < (dev_diff ? 2 : 1); ++phase) {
         launch_gd_step(gdst.get(), par, losspart.get(), nchunks, kMaxCand, sq2.get() + sqp * kSqBlocks, nsq,
                        sq2.get() + (sqp ^ 1) * kSqBlocks, kind, D->sum_sq, D->sum, Y.get(), cand[0].get(),
                        cand[1].get(), gnext.get(), gpart.get(), Q, graw.get(), n * Q, hist.get(), max_iters,
                        rel_tol, have_pre ? pre : nullptr, precise_rel, phase, st, xr, comm ? dsum.get() : nullptr,
-                       tiny_ok, solo_ok);
+                       tiny_ok, solo_ok, ondev);
         par ^= 1;
         if (phase == 0 && dev_diff) {
           dpa.gds = gdst.get() + par;
@@ -455,7 +460,10 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       b.halt = &gdst.get()[par].halt_fused;
       b.gds = gdst.get() + par;
       launch_pass_fused_f32(b, Q, st);              // both trials (exits when the state says solo)
-      if (solo_ok) launch_pass_solo_f32(b, Q, st);  // slot 0 only (runs when it does)
+      if (solo_ok || ondev) {  // one point: slot 0 (solo) or Y after a slot-1 acceptance (fix)
+        b.Y[2] = Y.get();
+        launch_pass_solo_f32(b, Q, st);
+      }
       if (tiny_ok) {  // tiny phase: one difference + gradient pass (the kernels exit unless tiny)
         PassArgs gp = args(kind, delta);
         gp.Y[0] = Y.get();
@@ -479,7 +487,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
     if (S.stop != 0) break;
   }
   // passes: the prime plus one per decision that continued (all accepted ones but a final stop)
-  passes += (S.it - it) - (S.stop == 1 ? 1 : 0) + S.ndiff;  // + the difference passes run on the device
+  passes += (S.it - it) - (S.stop == 1 ? 1 : 0) + S.ndiff + S.nextra;  // + difference / fix / re-trial passes
   if (S.stop == 2 && S.solo_miss) {
     // the solo pass left the half step's loss unevaluated: one loss pass over both trial points
     // (slot 0 is recomputed to the same bits; losspart column 0 stays the loss at cand0)

@@ -53,6 +53,15 @@ struct GdState {
                                 // the half step's loss would go unread; a miss hands the iteration to the host
   int solo_miss;                // stop == 2 after a solo pass: t1 (the loss at cand1) was not evaluated
   int streak;                   // consecutive full-step acceptances on resolved sums (solo needs 2)
+  // Decisions the predicted slot does not cover, kept on the device (one extra unit of the
+  // enqueued chain each, no host round trip):
+  int fix;                      // the trial in slot 1 was accepted: Y moved there, the next pass is the
+                                // gradient pass at Y (MODE 1), and the gd_step after it forms the trials
+  int rt;                       // neither trial was accepted: the trials were re-formed at step / 4 and
+                                // step / 8 (natural slot order, embed.cpp:242-250's further halvings) and
+                                // the next decision tests those (no fp32 re-evaluation, as on the host)
+  int halv;                     // halvings spent on this iteration (the reference allows 60)
+  int nextra;                   // passes run for these units (pass accounting)
 };
 
 struct Steps {
@@ -97,7 +106,7 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
                     int phase, cudaStream_t st, const double* xred = nullptr, const double* dsum = nullptr,
-                    bool tiny_ok = false, bool solo_ok = false);
+                    bool tiny_ok = false, bool solo_ok = false, bool ondev = false);
 // row-sharded device loop: gradient groups -> xred[0, nQ), the pass's trial-loss sums -> xred[nQ, nQ + 2)
 void launch_shard_collect(const double* gpart, int64_t n, int Q, const double* losspart, int64_t nparts, int stride,
                           double* xred, const int* halt, cudaStream_t st);

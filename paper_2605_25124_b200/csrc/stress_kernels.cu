@@ -338,7 +338,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
                                double* __restrict__ graw, int64_t m, double* __restrict__ history, int max_iters,
                                double rel_tol, const double* __restrict__ pre, double precise_rel, int phase,
                                const double* __restrict__ xred, const double* __restrict__ dsum, int tiny_ok,
-                               int solo_ok) {
+                               int solo_ok, int ondev) {
   // xred (row-sharded loop): the all-reduced [gradient at cand0 (n Q) | trial loss sums (2)]
   // of the last pass; dsum: the all-reduced sums of a difference pass (slots 0, 1, 2)
   pdl_wait();
@@ -355,6 +355,36 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   };
   if (S.stop || (phase == 1 && !S.pending)) {
     if (lead) publish(S);
+    return;
+  }
+  if (S.fix) {
+    // The last pass was the gradient pass at Y (the accepted slot-1 point): what the host's
+    // next iteration does first (grad_raw, then finish_grad): scale from the raw loss at Y,
+    // the scaled gradient, the trial pair of iteration S.it, |g|^2 partials.  No decision.
+    GdState R = S;
+    R.fix = 0;
+    if (lead) publish(R);
+    const double raw = xred ? xred[m] : (pre ? pre[2] : tree_sum<256>(losspart, nparts, stride, 0, red));
+    const double scale = grad_scale(kind, raw, sum_sq, sum);
+    const double s0 = (S.pred == 0) ? S.step : __dmul_rn(S.step, 0.5);
+    const double s1 = (S.pred == 0) ? __dmul_rn(S.step, 0.5) : S.step;
+    if (xred) {
+      for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+           k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        gnext[k] = xred[k];
+    } else {
+      const int64_t run = static_cast<int64_t>(kPT) * Q;
+      for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+           k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = k / Q, Rr = r / kPT;
+        const int64_t e = (r % kPT) * Q + k % Q;
+        double a = 0.0;
+#pragma unroll
+        for (int g = 0; g < kRedGroups; ++g) a += gpart[(Rr * kRedGroups + g) * run + e];
+        gnext[k] = a;
+      }
+    }
+    finish_body(scale, graw, Y, m, s0, s1, cand0, cand1, sqnext, red, nullptr, gnext);
     return;
   }
   // A decision on difference sums: phase 1 (a difference pass ran for a pending decision)
@@ -386,8 +416,11 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   R.solo = 0;
   R.solo_miss = 0;
   R.streak = 0;  // (kept only by the accepting path below)
+  R.rt = 0;
+  R.halv = 0;
   // the pass behind this decision was a solo pass: t1 is not there (see GdState::solo)
   const bool solo = S.solo != 0 && phase == 0 && S.tiny == 0;
+  const bool rt = S.rt != 0 && !diffdec;  // a re-trial decision: natural slot order, no fp32 re-evaluation
   auto loss_of = [&](double raw) {
     if (kind == kKruskal) return sqrt(__ddiv_rn(raw, sum_sq));
     if (kind == kSammon) return __dmul_rn(__ddiv_rn(1.0, sum), raw);
@@ -437,6 +470,14 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     const bool near_thr = precise_rel > 0.0 && fabs(__dsub_rn(f0, thr)) <= tol;
     solo_missed = near_f || (!near_thr && !(f0 <= thr)) || !(gsq > 0.0);
   }
+  if (solo_missed && ondev) {
+    // the same trial pair again through the two-trial fused pass (this unit's); |g|^2 carried over
+    R.tiny = 0;
+    R.nextra = S.nextra + 1;
+    if (lead) publish(R);
+    if (threadIdx.x == 0 && static_cast<int>(blockIdx.x) < nsq) sqnext[blockIdx.x] = sqprev[blockIdx.x];
+    return;
+  }
   if (solo_missed) {  // the host evaluates the loss at cand1 and decides (stop = 2)
     R.stop = 2;
     R.tiny = 0;
@@ -446,7 +487,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     return;
   }
   const bool unresolved =
-      !diffdec && precise_rel > 0.0 &&
+      !diffdec && !rt && precise_rel > 0.0 &&
       (solo ? armijo_unresolved(fY, S.step, gsq, loss_of(t0), loss_of(t0), tol)
             : ((fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
                armijo_unresolved(fY, S.step, gsq, loss_of(S.pred == 0 ? t0 : t1), loss_of(S.pred == 0 ? t1 : t0),
@@ -461,7 +502,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   if (gsq > 0.0 && !unresolved) {
     for (int c = 0; c < (solo ? 1 : 2); ++c) {  // step, then step/2 (the reference's order)
       const double sc = (c == 0) ? S.step : __dmul_rn(S.step, 0.5);
-      const int slot = (S.pred == 0) ? c : 1 - c;
+      const int slot = (rt || S.pred == 0) ? c : 1 - c;
       const double fc = loss_of(slot == 0 ? t0 : t1);
       if (fc <= __dsub_rn(fY, __dmul_rn(__dmul_rn(1e-4, sc), gsq))) {
         acc_c = c;
@@ -471,7 +512,61 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
       }
     }
   }
-  if (acc_c < 0 || ((S.pred == 0) ? acc_c : 1 - acc_c) != 0) {  // host takes this iteration
+  const int acc_slot = (acc_c < 0) ? -1 : ((rt || S.pred == 0) ? acc_c : 1 - acc_c);
+  // (also after a pending decision's two-trial difference pass, phase 1 -- the borderline full steps
+  // land there; the tiny phase's decisions stay with the host)
+  const bool devok = ondev != 0 && (!diffdec || (phase == 1 && S.single == 0 && S.tiny == 0));
+  if (devok && acc_slot == 1) {
+    // The other trial was accepted (embed.cpp:244-256 with the point in slot 1): Y moves there;
+    // its gradient comes from this unit's pass (MODE 1 at Y) and the next gd_step forms the
+    // trials (S.fix above).  pred follows the first two trials only (fit.cu gradient_descent).
+    const double decrease = __ddiv_rn(__dsub_rn(fY, f_new), fmax(fY, 1e-300));
+    R.f = f_new;
+    R.it = S.it + 1;
+    R.step = __dmul_rn(sc_acc, 2.0);
+    if (!rt) R.pred = acc_c;
+    R.tiny = 0;
+    if (decrease < rel_tol) {
+      R.stop = 1;
+      R.stalled = 1;
+    } else if (R.it >= max_iters) {
+      R.stop = 1;
+    }
+    if (!R.stop) {
+      R.fix = 1;
+      R.nextra = S.nextra + 1;
+    }
+    if (lead) {
+      history[R.it] = f_new;
+      publish(R);
+    }
+    for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < m;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      Y[k] = cand1[k];
+    return;
+  }
+  if (devok && acc_c < 0 && gsq > 0.0 && !unresolved) {
+    // Neither trial accepted: the reference halves on (embed.cpp:242-250; fit.cu's loop: step / 4
+    // and step / 8 next, two per round, 60 halvings at most).  The trials are re-formed from Y and
+    // the scaled gradient (finish_body with scale 1: the same y - s g as axpy_cand_kernel, and the
+    // same |g|^2 partials again) and this unit's fused pass evaluates them.
+    const int halv = (rt ? S.halv : 0) + 2;
+    R.tiny = 0;
+    if (halv >= 60) {  // no descent direction at double precision (embed.cpp:252-255)
+      R.stop = 1;
+      R.stalled = 1;
+      if (lead) publish(R);
+      return;
+    }
+    R.rt = 1;
+    R.halv = halv;
+    R.step = __dmul_rn(S.step, 0.25);
+    R.nextra = S.nextra + 1;
+    if (lead) publish(R);
+    finish_body(1.0, graw, Y, m, R.step, __dmul_rn(R.step, 0.5), cand0, cand1, sqnext, red);
+    return;
+  }
+  if (acc_c < 0 || acc_slot != 0) {  // host takes this iteration
     R.stop = 2;
     R.tiny = 0;
     R.solo_miss = solo ? 1 : 0;  // (solo: only an unresolved non-Kruskal decision gets here)
@@ -497,7 +592,7 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   R.single = (R.tiny != 0 && S.pred == 0) ? 1 : 0;
   // solo for the next pass: the full step was just accepted on resolved fp32 sums with room to
   // spare (a change of more than 4 tol), so the doubled step's half-step loss will go unread
-  R.streak = (!diffdec && S.pred == 0 && (precise_rel <= 0.0 || fabs(__dsub_rn(fY, f_new)) > 4.0 * tol))
+  R.streak = (!diffdec && !rt && S.pred == 0 && (precise_rel <= 0.0 || fabs(__dsub_rn(fY, f_new)) > 4.0 * tol))
                  ? S.streak + 1
                  : 0;
   R.solo = (solo_ok && R.tiny == 0 && R.stop == 0 && R.streak >= 2) ? 1 : 0;
@@ -622,10 +717,10 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
                     double* history, int max_iters, double rel_tol, const double* pre, double precise_rel,
                     int phase, cudaStream_t st, const double* xred, const double* dsum, bool tiny_ok,
-                    bool solo_ok) {
+                    bool solo_ok, bool ondev) {
   launch_pdl(gd_step_kernel, dim3(nsq), dim3(256), 0, st, st2, par, losspart, nparts, stride, sqprev, nsq, sqnext,
              kind, sum_sq, sum, Y, cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-             precise_rel, phase, xred, dsum, tiny_ok ? 1 : 0, solo_ok ? 1 : 0);
+             precise_rel, phase, xred, dsum, tiny_ok ? 1 : 0, solo_ok ? 1 : 0, ondev ? 1 : 0);
   count_launch();
   check_launch("gd_step_kernel");
 }

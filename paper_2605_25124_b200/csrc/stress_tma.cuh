@@ -155,8 +155,17 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   __shared__ double sLoss[kThreads / 32][kMaxCand];
 
   if (a.halt && *a.halt) return;
-  if constexpr (MODE == 1 || MODE == 2) {  // device loop: the solo pass (MODE 1) or the two-trial fused pass
-    if (a.gds && (a.gds->solo != 0) != (MODE == 1)) return;
+  // device loop: the one-point pass (MODE 1: a solo pass at cand0, or the gradient pass at Y after a
+  // slot-1 acceptance, GdState::fix) or the two-trial fused pass
+  const double* Yc[NCM];
+#pragma unroll
+  for (int c = 0; c < NCM; ++c) Yc[c] = a.Y[c];
+  if constexpr (MODE == 1 || MODE == 2) {
+    if (a.gds) {
+      const bool one = a.gds->solo != 0 || a.gds->fix != 0;
+      if (one != (MODE == 1)) return;
+      if (MODE == 1 && a.gds->fix != 0) Yc[0] = a.Y[2];
+    }
   }
   if constexpr (DG) {  // device loop: run only in the tiny phase, in the matching width
     if (a.gds && (a.gds->tiny == 0 || a.gds->stop != 0 || (a.gds->single != 0) != (NT == 1))) return;
@@ -195,14 +204,14 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     const int r = tid & (kPT - 1);
     const int64_t i = I * kPT + r;
     for (int c = tid >> 7; c < NCM; c += 2) {
-      const double2 v = (c < nc && i < a.n) ? reinterpret_cast<const double2*>(a.Y[c])[i] : make_double2(0.0, 0.0);
+      const double2 v = (c < nc && i < a.n) ? reinterpret_cast<const double2*>(Yc[c])[i] : make_double2(0.0, 0.0);
       *reinterpret_cast<float2*>(&sYi[c][r][0]) = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
     }
   } else {
     for (int e = tid; e < nc * kPT * Q; e += kThreads) {
       const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
       const int64_t i = I * kPT + r;
-      sYi[c][r][k] = (i < a.n) ? static_cast<float>(a.Y[c][i * Q + k]) : 0.f;
+      sYi[c][r][k] = (i < a.n) ? static_cast<float>(Yc[c][i * Q + k]) : 0.f;
     }
   }
   double lossacc[NCM];
@@ -235,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   constexpr int NSC = (NCM + 1) / 2;  // configurations staged per thread (thread c stages c, c + 2)
   auto col_load = [&](int64_t J, int c) {
     const int64_t j = J * kPT + sr;
-    return (c < nc && j < a.n) ? reinterpret_cast<const double2*>(a.Y[c])[j] : make_double2(0.0, 0.0);
+    return (c < nc && j < a.n) ? reinterpret_cast<const double2*>(Yc[c])[j] : make_double2(0.0, 0.0);
   };
   double2 ycol[NSC];
 #pragma unroll
@@ -265,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       for (int e = tid; e < nc * kPT * Q; e += kThreads) {
         const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
         const int64_t j = J * kPT + r;
-        sYj[yb][c][k][r] = (j < a.n) ? static_cast<float>(a.Y[c][j * Q + k]) : 0.f;
+        sYj[yb][c][k][r] = (j < a.n) ? static_cast<float>(Yc[c][j * Q + k]) : 0.f;
       }
     }
     __syncthreads();

@@ -376,10 +376,12 @@ def test_device_resident_descent_identical(monkeypatch, kind, rel_tol, iters):
     assert a["iterations"] == b["iterations"] and a["converged"] == b["converged"]
     assert np.array_equal(np.array(a["stress_history"]), np.array(b["stress_history"]))
     assert np.array_equal(a["coords"], b["coords"])
-    # a solo pass (slot 0 only, GdState::solo) that misses costs one extra loss pass
-    assert b["passes"] <= a["passes"] <= b["passes"] + max(3, iters // 20)
+    # a solo pass (slot 0 only, GdState::solo) that misses costs one extra pass; further halvings
+    # decided on the device (GdState::rt) save the host loop's separate gradient pass
+    assert a["passes"] <= b["passes"] + max(3, iters // 20)
     monkeypatch.delenv("GMDS_HOST_GD")
     monkeypatch.setenv("GMDS_NO_SOLO", "1")
+    monkeypatch.setenv("GMDS_NO_ONDEV", "1")
     c = G.minimize_stress(D, 2, kind, huber_delta=hd, max_iters=iters, rel_tol=rel_tol, Y0=Y0, storage=G.F32)
     assert np.array_equal(np.array(c["stress_history"]), np.array(b["stress_history"]))
     assert np.array_equal(c["coords"], b["coords"])
