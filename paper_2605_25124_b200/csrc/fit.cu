@@ -434,6 +434,8 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   // slot-1 acceptances, further halvings and solo misses decided on the device (GdState::fix / rt);
   // GMDS_NO_ONDEV=1: those iterations go back to the host loop
   const bool ondev = !std::getenv("GMDS_NO_ONDEV");
+  // kruskal, q <= 3: the unit's passes behind two launches (stress_tma_multi_kernel) instead of six
+  const bool multi = tiny_ok && ondev && !std::getenv("GMDS_NO_MULTI");
   for (;;) {
     // units per batch: an iteration takes one unit, or two when it needs a fix / re-trial unit
     const int left = max_iters - S.it;
@@ -448,8 +450,14 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
         par ^= 1;
         if (phase == 0 && dev_diff) {
           dpa.gds = gdst.get() + par;
-          launch_pass_diff_f32(dpa, Q, st);   // both trials (runs unless the decision is single)
-          launch_pass_diff1_f32(dpa, Q, st);  // the first trial only (runs if single)
+          if (multi) {
+            PassArgs b0 = b;
+            b0.gds = dpa.gds;
+            launch_pass_multi_f32(b0, dpa, Q, 0, st);
+          } else {
+            launch_pass_diff_f32(dpa, Q, st);   // both trials (runs unless the decision is single)
+            launch_pass_diff1_f32(dpa, Q, st);  // the first trial only (runs if single)
+          }
           if (comm) {  // the difference sums over the ranks (read by phase 1 only when pending)
             launch_sum_parts(losspart.get(), nchunks, kMaxCand, 3, dsum.get(), st);
             comm->allreduce(dsum.get(), 3, RedOp::kSum, st);
@@ -459,19 +467,21 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       sqp ^= 1;
       b.halt = &gdst.get()[par].halt_fused;
       b.gds = gdst.get() + par;
-      launch_pass_fused_f32(b, Q, st);              // both trials (exits when the state says solo)
-      if (solo_ok || ondev) {  // one point: slot 0 (solo) or Y after a slot-1 acceptance (fix)
-        b.Y[2] = Y.get();
-        launch_pass_solo_f32(b, Q, st);
-      }
-      if (tiny_ok) {  // tiny phase: one difference + gradient pass (the kernels exit unless tiny)
-        PassArgs gp = args(kind, delta);
-        gp.Y[0] = Y.get();
-        gp.Y[1] = graw.get();
-        gp.ncand = 2;
-        gp.gds = gdst.get() + par;
-        launch_pass_diffgrad_f32(gp, Q, false, st);  // both trials
-        launch_pass_diffgrad_f32(gp, Q, true, st);   // the first trial (when it leads the slot order)
+      b.Y[2] = Y.get();
+      PassArgs gp = args(kind, delta);  // tiny phase: one difference + gradient pass
+      gp.Y[0] = Y.get();
+      gp.Y[1] = graw.get();
+      gp.ncand = 2;
+      gp.gds = gdst.get() + par;
+      if (multi) {
+        launch_pass_multi_f32(b, gp, Q, 1, st);
+      } else {
+        launch_pass_fused_f32(b, Q, st);                        // both trials (exits when the state says one point)
+        if (solo_ok || ondev) launch_pass_solo_f32(b, Q, st);   // slot 0 (solo) or Y after a slot-1 acceptance (fix)
+        if (tiny_ok) {  // (the kernels exit unless tiny)
+          launch_pass_diffgrad_f32(gp, Q, false, st);  // both trials
+          launch_pass_diffgrad_f32(gp, Q, true, st);   // the first trial (when it leads the slot order)
+        }
       }
       b.halt = &gdst.get()[par].stop;
       launch_reduce_rows(rowpart.get(), colpart.get(), strip_first.get(), n, nb, Q, nullptr, st, gpart.get(),

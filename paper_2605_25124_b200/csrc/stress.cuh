@@ -125,6 +125,10 @@ void launch_pass_diff1_f32(const PassArgs& a, int Q, cudaStream_t st);
 // kruskal, device loop's tiny phase: the difference pass (both trials, or the first when single)
 // plus the raw gradient at a.Y[2] (the first trial point) -- runs only when a.gds->tiny
 void launch_pass_diffgrad_f32(const PassArgs& a, int Q, bool single, cudaStream_t st);
+// kruskal device loop, q <= 3: one launch for whichever pass the GdState (a.gds) asks for --
+// which 0: the pending decision's difference pass (d: its arguments); which 1: the unit's main
+// pass (a: the fused / one-point arguments, d: the difference + gradient pass's)
+void launch_pass_multi_f32(const PassArgs& a, const PassArgs& d, int Q, int which, cudaStream_t st);
 constexpr int kSqBlocks = 148;
 void launch_scale_sqnorm(double* g, int64_t m, double scale, double* out, double* part, cudaStream_t st);
 // raw loss (from the pass partials) -> scale -> g *= scale, trial points T0/T1, |g|^2 block partials;

@@ -123,10 +123,21 @@ __device__ __forceinline__ void kind_terms(float Dv, float invD, float dist, flo
 // gradient at the first trial point, from the same per-pair quantities (y_i - y_j -
 // s_0 (g_i - g_j) and the trial distance the difference needs anyway: no extra MUFU) --
 // one pass per tiny iteration instead of a difference pass and a gradient pass.
+// Shared memory of one pass, all of it carved from the dynamic allocation (ring first), so one
+// kernel can hold several modes' bodies (stress_tma_multi_kernel) without adding up static arrays.
+template <int Q, int MODE>
+constexpr size_t tma_smem_bytes() {
+  constexpr bool DG = (MODE == 6 || MODE == 7);
+  constexpr bool GRAD = (MODE == 1 || MODE == 2 || DG);
+  constexpr int NCM = (MODE == 1) ? 1 : tma_detail::kTmaCand;
+  constexpr int NS = GRAD ? tma_detail::kStagesGrad : tma_detail::kStages;
+  return static_cast<size_t>(NS) * tma_detail::kHalfFloats * 4 + 128 /* barriers */ +
+         (kThreads / 32) * kMaxCand * 8 /* sLoss */ + static_cast<size_t>(NCM) * kPT * Q * 4 /* sYi */ +
+         static_cast<size_t>(2) * NCM * Q * kPT * 4 /* sYj */ + (GRAD ? static_cast<size_t>(Q) * kTG * kPT * 4 : 16);
+}
+
 template <int Q, int MODE, int KIND>
-__global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void stress_tma_body(const PassArgs& a, unsigned char* dyn) {
   using namespace tma_detail;
   constexpr bool DG = (MODE == 6 || MODE == 7);      // difference + gradient at the first trial point
   constexpr bool DIFF = (MODE == 3 || MODE == 5 || DG);  // loss differences: configurations are Y and the gradient
@@ -142,31 +153,35 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   constexpr int NCH = CSPLIT ? 2 : 1;        // column groups per band
   constexpr int NYY = (kMT / 2) / NCH;       // column pairs (y, y+1) per group
   constexpr int NY = 2 * NYY;                // columns per group
-  extern __shared__ __align__(128) unsigned char dyn[];
   constexpr int NS = GRAD ? kStagesGrad : kStages;
   float* ring = reinterpret_cast<float*>(dyn);  // [NS][kHalfFloats]: half h lives in stage h % NS
-  __shared__ __align__(8) uint64_t bars[NS];
-  __shared__ __align__(16) float sYi[NCM][kPT][Q];
+  unsigned char* sp = dyn + static_cast<size_t>(NS) * kHalfFloats * 4;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp);  // [NS]
+  sp += 128;
+  double (*sLoss)[kMaxCand] = reinterpret_cast<double (*)[kMaxCand]>(sp);  // [kThreads / 32][kMaxCand]
+  sp += (kThreads / 32) * kMaxCand * 8;
+  float (*sYi)[kPT][Q] = reinterpret_cast<float (*)[kPT][Q]>(sp);  // [NCM][kPT][Q]
+  sp += static_cast<size_t>(NCM) * kPT * Q * 4;
   // [block parity][cand][k][column]: one coordinate of consecutive columns is contiguous, so a
   // thread's column pairs (y, y+1) arrive as one 16-byte load per 4 columns (no register moves
   // to form the FFMA2 operand pairs); double-buffered
-  __shared__ __align__(16) float sYj[2][NCM][Q][kPT];
-  __shared__ __align__(16) float sRed[GRAD ? Q * kTG * kPT : 1];  // column partials of one block, all k at once
-  __shared__ double sLoss[kThreads / 32][kMaxCand];
+  float (*sYj)[NCM][Q][kPT] = reinterpret_cast<float (*)[NCM][Q][kPT]>(sp);  // [2][NCM][Q][kPT]
+  sp += static_cast<size_t>(2) * NCM * Q * kPT * 4;
+  float* sRed = reinterpret_cast<float*>(sp);  // [Q kTG kPT] (GRAD): column partials of one block, all k at once
 
   if (a.halt && *a.halt) return;
   // device loop: the one-point pass (MODE 1: a solo pass at cand0, or the gradient pass at Y after a
   // slot-1 acceptance, GdState::fix) or the two-trial fused pass
-  const double* Yc[NCM];
-#pragma unroll
-  for (int c = 0; c < NCM; ++c) Yc[c] = a.Y[c];
+  const double* y0p = a.Y[0];
   if constexpr (MODE == 1 || MODE == 2) {
     if (a.gds) {
       const bool one = a.gds->solo != 0 || a.gds->fix != 0;
       if (one != (MODE == 1)) return;
-      if (MODE == 1 && a.gds->fix != 0) Yc[0] = a.Y[2];
+      if (MODE == 1 && a.gds->fix != 0) y0p = a.Y[2];
     }
   }
+  // configuration c's coordinates (a.Y[c] stays a constant-bank read; no local array)
+  auto Yof = [&](int c) { return (MODE == 1) ? y0p : a.Y[c]; };
   if constexpr (DG) {  // device loop: run only in the tiny phase, in the matching width
     if (a.gds && (a.gds->tiny == 0 || a.gds->stop != 0 || (a.gds->single != 0) != (NT == 1))) return;
   } else if constexpr (DIFF) {  // device loop: run only for a pending decision, in the matching width
@@ -204,14 +219,14 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
     const int r = tid & (kPT - 1);
     const int64_t i = I * kPT + r;
     for (int c = tid >> 7; c < NCM; c += 2) {
-      const double2 v = (c < nc && i < a.n) ? reinterpret_cast<const double2*>(Yc[c])[i] : make_double2(0.0, 0.0);
+      const double2 v = (c < nc && i < a.n) ? reinterpret_cast<const double2*>(Yof(c))[i] : make_double2(0.0, 0.0);
       *reinterpret_cast<float2*>(&sYi[c][r][0]) = make_float2(static_cast<float>(v.x), static_cast<float>(v.y));
     }
   } else {
     for (int e = tid; e < nc * kPT * Q; e += kThreads) {
       const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
       const int64_t i = I * kPT + r;
-      sYi[c][r][k] = (i < a.n) ? static_cast<float>(Yc[c][i * Q + k]) : 0.f;
+      sYi[c][r][k] = (i < a.n) ? static_cast<float>(Yof(c)[i * Q + k]) : 0.f;
     }
   }
   double lossacc[NCM];
@@ -244,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   constexpr int NSC = (NCM + 1) / 2;  // configurations staged per thread (thread c stages c, c + 2)
   auto col_load = [&](int64_t J, int c) {
     const int64_t j = J * kPT + sr;
-    return (c < nc && j < a.n) ? reinterpret_cast<const double2*>(Yc[c])[j] : make_double2(0.0, 0.0);
+    return (c < nc && j < a.n) ? reinterpret_cast<const double2*>(Yof(c))[j] : make_double2(0.0, 0.0);
   };
   double2 ycol[NSC];
 #pragma unroll
@@ -274,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
       for (int e = tid; e < nc * kPT * Q; e += kThreads) {
         const int c = e / (kPT * Q), r = (e / Q) % kPT, k = e % Q;
         const int64_t j = J * kPT + r;
-        sYj[yb][c][k][r] = (j < a.n) ? static_cast<float>(Yc[c][j * Q + k]) : 0.f;
+        sYj[yb][c][k][r] = (j < a.n) ? static_cast<float>(Yof(c)[j * Q + k]) : 0.f;
       }
     }
     __syncthreads();
@@ -688,15 +703,57 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
   }
 }
 
-constexpr size_t kTmaSmemLoss = static_cast<size_t>(tma_detail::kStages) * tma_detail::kHalfFloats * 4;
-constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * tma_detail::kHalfFloats * 4;
+template <int Q, int MODE, int KIND>
+__global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_kernel(PassArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(128) unsigned char dyn[];
+  stress_tma_body<Q, MODE, KIND>(a, dyn);
+}
+
+// Device loop, kruskal, q <= 3: the passes a unit of the enqueued chain may need, behind two
+// launches instead of six (each skipped pass used to cost an empty launch): WHICH 0 = the
+// difference pass of a pending decision (MODE 3, or 5 when single), WHICH 1 = the unit's main
+// pass -- two-trial fused (2), one-point (1: solo / fix), or the tiny phase's difference +
+// gradient pass (6 / 7).  The GdState the passes' own guards read selects the body.
+template <int Q, int WHICH>
+__global__ void __launch_bounds__(kThreads, 2) stress_tma_multi_kernel(PassArgs a, PassArgs d) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(128) unsigned char dyn[];
+  const GdState* g = a.gds;
+  if (g->stop != 0) return;
+  if constexpr (WHICH == 0) {
+    if (g->pending == 0) return;
+    if (g->single != 0) stress_tma_body<Q, 5, kKruskal>(d, dyn);
+    else stress_tma_body<Q, 3, kKruskal>(d, dyn);
+  } else {
+    if (g->tiny != 0) {
+      if (g->single != 0) stress_tma_body<Q, 7, kKruskal>(d, dyn);
+      else stress_tma_body<Q, 6, kKruskal>(d, dyn);
+    } else if (g->solo != 0 || g->fix != 0) {
+      stress_tma_body<Q, 1, kKruskal>(a, dyn);
+    } else {
+      stress_tma_body<Q, 2, kKruskal>(a, dyn);
+    }
+  }
+}
+
+template <int Q>
+constexpr size_t tma_multi_smem() {
+  size_t m = tma_smem_bytes<Q, 1>();
+  if (tma_smem_bytes<Q, 2>() > m) m = tma_smem_bytes<Q, 2>();
+  if (tma_smem_bytes<Q, 3>() > m) m = tma_smem_bytes<Q, 3>();
+  if (tma_smem_bytes<Q, 6>() > m) m = tma_smem_bytes<Q, 6>();
+  return m;
+}
 
 #define GMDS_TMA_KIND(QQ, KK)                                                                              \
   case KK:                                                                                                 \
     GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, MODE, KK>,                                        \
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,                            \
-                                   static_cast<int>(MODE ? kTmaSmemGrad : kTmaSmemLoss)));                 \
-    launch_pdl(stress_tma_kernel<QQ, MODE, KK>, dim3(g), dim3(kThreads), MODE ? kTmaSmemGrad : kTmaSmemLoss, st, a); \
+                                   static_cast<int>(tma_smem_bytes<QQ, MODE>())));                         \
+    launch_pdl(stress_tma_kernel<QQ, MODE, KK>, dim3(g), dim3(kThreads), tma_smem_bytes<QQ, MODE>(), st, a); \
     break;
 #define GMDS_TMA_Q(QQ)                                                                                    \
   case QQ:                                                                                                \
@@ -729,8 +786,9 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
 #define GMDS_TMA_DG_Q(QQ)                                                                                 \
   case QQ:                                                                                                \
     GMDS_CUDA(cudaFuncSetAttribute(stress_tma_kernel<QQ, MODE, kKruskal>,                                  \
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kTmaSmemGrad))); \
-    launch_pdl(stress_tma_kernel<QQ, MODE, kKruskal>, dim3(g), dim3(kThreads), kTmaSmemGrad, st, a);       \
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,                            \
+                                   static_cast<int>(tma_smem_bytes<QQ, MODE>())));                         \
+    launch_pdl(stress_tma_kernel<QQ, MODE, kKruskal>, dim3(g), dim3(kThreads), tma_smem_bytes<QQ, MODE>(), st, a); \
     break;
 #define GMDS_INSTANTIATE_TMA_DG                                                                           \
   void launch_pass_diffgrad_f32(const PassArgs& a, int Q, bool single, cudaStream_t st) {                 \
@@ -751,6 +809,29 @@ constexpr size_t kTmaSmemGrad = static_cast<size_t>(tma_detail::kStagesGrad) * t
     }                                                                                                     \
     count_launch();                                                                                       \
     check_launch("stress_tma_kernel (difference + gradient)");                                            \
+  }
+#define GMDS_TMA_MULTI_Q(QQ)                                                                              \
+  case QQ:                                                                                                \
+    if (which == 0) {                                                                                     \
+      GMDS_CUDA(cudaFuncSetAttribute(stress_tma_multi_kernel<QQ, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     static_cast<int>(tma_multi_smem<QQ>())));                            \
+      launch_pdl(stress_tma_multi_kernel<QQ, 0>, dim3(g), dim3(kThreads), tma_multi_smem<QQ>(), st, a, d); \
+    } else {                                                                                              \
+      GMDS_CUDA(cudaFuncSetAttribute(stress_tma_multi_kernel<QQ, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     static_cast<int>(tma_multi_smem<QQ>())));                            \
+      launch_pdl(stress_tma_multi_kernel<QQ, 1>, dim3(g), dim3(kThreads), tma_multi_smem<QQ>(), st, a, d); \
+    }                                                                                                     \
+    break;
+#define GMDS_INSTANTIATE_TMA_MULTI                                                                        \
+  void launch_pass_multi_f32(const PassArgs& a, const PassArgs& d, int Q, int which, cudaStream_t st) {   \
+    if (a.kind != kKruskal || !a.gds) fail(GMDS_ERROR, "multi pass: kruskal device loop only");           \
+    const unsigned g = static_cast<unsigned>(a.nchunks);                                                  \
+    switch (Q) {                                                                                          \
+      GMDS_TMA_MULTI_Q(1) GMDS_TMA_MULTI_Q(2) GMDS_TMA_MULTI_Q(3)                                         \
+      default: fail(GMDS_ERROR, "multi pass: q <= 3");                                                    \
+    }                                                                                                     \
+    count_launch();                                                                                       \
+    check_launch("stress_tma_multi_kernel");                                                              \
   }
 #define GMDS_INSTANTIATE_TMA_FUSED                                                                        \
   void launch_pass_fused_f32(const PassArgs& a, int Q, cudaStream_t st) {                                 \
