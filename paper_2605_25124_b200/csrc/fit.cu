@@ -434,7 +434,7 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   // slot-1 acceptances, further halvings and solo misses decided on the device (GdState::fix / rt);
   // GMDS_NO_ONDEV=1: those iterations go back to the host loop
   const bool ondev = !std::getenv("GMDS_NO_ONDEV");
-  // kruskal, q <= 3: the unit's passes behind two launches (stress_tma_multi_kernel) instead of six
+  // kruskal, q <= 3: the difference passes behind one launch and the fused / one-point pass behind one (stress_tma_multi_kernel)
   const bool multi = tiny_ok && ondev && !std::getenv("GMDS_NO_MULTI");
   for (;;) {
     // units per batch: an iteration takes one unit, or two when it needs a fix / re-trial unit
@@ -474,7 +474,9 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
       gp.ncand = 2;
       gp.gds = gdst.get() + par;
       if (multi) {
-        launch_pass_multi_f32(b, gp, Q, 1, st);
+        launch_pass_multi_f32(b, gp, Q, 1, st);      // fused / one point
+        launch_pass_diffgrad_f32(gp, Q, false, st);  // tiny phase, both trials (merged, the two bodies
+        launch_pass_diffgrad_f32(gp, Q, true, st);   // spilled 384 B at q = 2 against 168 / 100 B apart)
       } else {
         launch_pass_fused_f32(b, Q, st);                        // both trials (exits when the state says one point)
         if (solo_ok || ondev) launch_pass_solo_f32(b, Q, st);   // slot 0 (solo) or Y after a slot-1 acceptance (fix)

@@ -93,6 +93,34 @@ static void launch_gen_t(const GmdArgs& ga, TO* out, size_t smem, unsigned block
   }
 }
 
+template <typename TO, int NW, int NNU>
+static void launch_gen2_one(const GmdArgs& ga, TO* out, size_t smem, unsigned blocks, cudaStream_t st) {
+  GMDS_CUDA(cudaFuncSetAttribute(gini_gen2_kernel<TO, NW, NNU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  gini_gen2_kernel<TO, NW, NNU><<<blocks, NW * 32, smem, st>>>(ga, out);
+}
+
+template <typename TO>
+static void launch_gen2_t(const GmdArgs& ga, TO* out, size_t smem, unsigned blocks, int nwarps, cudaStream_t st) {
+  const bool one = ga.s.g.nnu == 1;
+  if (nwarps >= 28) {
+    if (one) launch_gen2_one<TO, 28, 1>(ga, out, smem, blocks, st);
+    else launch_gen2_one<TO, 28, 4>(ga, out, smem, blocks, st);
+  } else {
+    if (one) launch_gen2_one<TO, 24, 1>(ga, out, smem, blocks, st);
+    else launch_gen2_one<TO, 24, 4>(ga, out, smem, blocks, st);
+  }
+}
+
+void launch_gini_gen2(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
+                      cudaStream_t st) {
+  if (ga.s.g.nnu > 4) fail(GMDS_ERROR, "gini_gen2_kernel: at most 4 nu per launch");
+  if (ot == GMDS_F32)
+    launch_gen2_t(ga, static_cast<float*>(dout), smem, blocks, nwarps, st);
+  else
+    launch_gen2_t(ga, static_cast<double*>(dout), smem, blocks, nwarps, st);
+}
+
 void launch_gini_gen(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
                      cudaStream_t st) {
   if (ga.s.g.nnu > 4) fail(GMDS_ERROR, "gini_gen_kernel: at most 4 nu per launch");

@@ -392,6 +392,9 @@ constexpr int kMaxC2 = 255;    // max nonzeros per staged row
 // per-warp scratch (8-byte words): QM[32] u32 (16) | PQi[72] | PQj[72] | ZL[2][64] | lists (8 x 66 u16 = 132)
 constexpr int kOffPQi2 = 16, kOffPQj2 = 88, kOffZL2 = 160, kOffFL2 = 288;
 constexpr int kWarpWords2 = kOffFL2 + (kBatch * kFLStride * 2 + 7) / 8;
+// gini_gen2_kernel: QM[32] u32 (16) | BL[2][64] (128) | HI, HJ: 2 x 256 u16 counters (128) | lists (132)
+constexpr int kGenOffBL = 16, kGenOffH = 144, kGenOffFL = 272;
+constexpr int kGenWords2 = kGenOffFL + (kBatch * kFLStride * 2 + 7) / 8;
 }  // namespace gmd2_detail
 
 template <typename TO, int kWarps>
@@ -1031,6 +1034,362 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen_kernel(GmdArgs ga, TO
   }
   score_flush(a, s_score);
 }
+
+// gini_gen2_kernel: gini_gen_kernel with gini_gmd2_kernel's batched F lists, bucket-table lower
+// bounds and the (sorted values, position map) panel; same counts, LUT indices and sums.
+template <typename TO, int kWarps, int NNU>
+__global__ void __launch_bounds__(kWarps * 32, 1) gini_gen2_kernel(GmdArgs ga, TO* __restrict__ out) {
+  using namespace gmd_detail;
+  using namespace gmd2_detail;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const SplitArgs& sa = ga.s;
+  const GiniTileArgs& a = sa.g;
+  const int d = a.d;
+  const int W = sa.W;
+  const int stride = sa.maxnnz;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  double* wscr = reinterpret_cast<double*>(smem_raw) + warp * kGenWords2;
+  uint32_t* QM = reinterpret_cast<uint32_t*>(wscr);  // qm_i[8] qm_j[8] qp_i[8] qp_j[8]
+  double* BL = wscr + kGenOffBL;                     // [0, 64): S_ab- values, [64, 128): S_ab+
+  uint32_t* HI = reinterpret_cast<uint32_t*>(wscr + kGenOffH);  // 256 u16 counters
+  uint32_t* HJ = HI + 128;
+  uint16_t* FL = reinterpret_cast<uint16_t*>(wscr + kGenOffFL);  // [kBatch][kFLStride]: ii | jj << 8
+  double* otile = reinterpret_cast<double*>(smem_raw) + kWarps * kGenWords2;  // [nnu][32][33]
+  double* rs1 = otile + static_cast<size_t>(a.nnu) * kTile * (kTile + 1);
+  double* rtm = rs1 + kRows;
+  int64_t* rbase = reinterpret_cast<int64_t*>(rtm + kRows);
+  int* rcnt = reinterpret_cast<int*>(rbase + kRows);
+  float* rscale = reinterpret_cast<float*>(rcnt + kRows);
+  uint32_t* smask = reinterpret_cast<uint32_t*>(rscale + kRows);  // [64][W]
+  uint16_t* spre = reinterpret_cast<uint16_t*>(smask + kRows * W);
+  float* ssv = reinterpret_cast<float*>(spre + ((kRows * W + 1) & ~1));      // [64][stride] sorted values
+  uint16_t* spm = reinterpret_cast<uint16_t*>(ssv + kRows * stride);         // [64][stride] sorted position
+  uint32_t* stie = reinterpret_cast<uint32_t*>(spm + ((kRows * stride + 1) & ~1));  // [64][8]
+  uint8_t* sbk = reinterpret_cast<uint8_t*>(stie + kRows * 8);               // [64][256] bucket starts
+  const int g4 = lane >> 2, sub = lane & 3;
+  const double half_p = 0.5 * static_cast<double>(d);
+  const int tstride = kTile + 1;
+  const int nnu = (NNU == 1) ? 1 : a.nnu;
+  const int lstride = 2 * d;
+  __shared__ double s_score[2 * kMaxScoreNu];
+  __shared__ double s_red[32 * 8];
+  for (int e = threadIdx.x; e < 2 * kMaxScoreNu; e += blockDim.x) s_score[e] = 0.0;
+  for (int e = lane; e < 256; e += 32) HI[e] = 0u;  // HI and HJ: left zero after every pair
+
+  for (int64_t t = a.tile_begin + blockIdx.x; t < a.tile_end; t += gridDim.x) {
+    int64_t I, J;
+    decode_tile(t, a.nbt, I, J);
+    if (!tile_in_blocks(a, I, J)) continue;
+    const int64_t i0 = I * kTile, j0 = J * kTile;
+    for (int e = threadIdx.x; e < kRows * W; e += blockDim.x) {
+      const int r = e / W, w = e - (e / W) * W;
+      const int64_t row = (r < kTile) ? i0 + r : j0 + (r - kTile);
+      smask[e] = (row < a.n) ? sa.masks[row * W + w] : 0u;
+      spre[e] = (row < a.n) ? sa.prefix[row * W + w] : uint16_t(0);
+    }
+    for (int r = warp; r < kRows; r += kWarps) {
+      const int64_t row = (r < kTile) ? i0 + r : j0 + (r - kTile);
+      int cnt = 0;
+      if (row < a.n) {
+        const int64_t b = sa.rowptr[row];
+        cnt = static_cast<int>(sa.rowptr[row + 1] - b);
+        for (int k = lane; k < cnt && k < stride; k += 32) {
+          ssv[r * stride + k] = ga.svs[b + k];
+          spm[r * stride + k] = ga.pmap[b + k];
+        }
+        const uint32_t* gb = reinterpret_cast<const uint32_t*>(ga.bkt) + row * 64;
+        uint32_t* sb = reinterpret_cast<uint32_t*>(sbk) + r * 64;
+        sb[lane] = gb[lane];
+        sb[lane + 32] = gb[lane + 32];
+      }
+      if (lane == 0) {
+        rcnt[r] = cnt;
+        rscale[r] = (row < a.n) ? ga.bscale[row] : 0.f;
+      }
+      if (lane < 8) stie[r * 8 + lane] = (row < a.n) ? ga.tiew[row * 8 + lane] : 0u;
+    }
+    __syncthreads();
+
+    for (int t0 = 0; warp + kWarps * t0 < kTile * kTile; t0 += kBatch) {
+      // ---- F lists of this batch: 4 lanes per pair, every fourth mask word each (gini_gmd2_kernel)
+      int stat;  // the pair's |F|, or 0x100: overflow list, 0x200: not a pair of this tile
+      {
+        const int kg = warp + kWarps * (t0 + g4);
+        bool valid = kg < kTile * kTile;
+        const int rg = valid ? (kg >> 5) : 0, cg = valid ? (kg & 31) : 0;
+        valid = valid && (j0 + cg < a.n) && (i0 + rg < j0 + cg);
+        const uint32_t* mi = smask + rg * W;
+        const uint32_t* mj = smask + (kTile + cg) * W;
+        int cnt = 0;
+        if (valid)
+          for (int w = sub; w < W; w += 4) cnt += __popc(mi[w] & mj[w]);
+        int incl = cnt;
+        int o = __shfl_up_sync(0xffffffffu, incl, 1, 4);
+        if (sub >= 1) incl += o;
+        o = __shfl_up_sync(0xffffffffu, incl, 2, 4);
+        if (sub >= 2) incl += o;
+        const int sg = __shfl_sync(0xffffffffu, incl, 3, 4);
+        const bool ok = valid && sg <= kCap && rcnt[rg] <= stride && rcnt[kTile + cg] <= stride;
+        if (ok) {
+          int off = incl - cnt;
+          uint16_t* fl = FL + g4 * kFLStride;
+          const uint16_t* pim = spre + rg * W;
+          const uint16_t* pjm = spre + (kTile + cg) * W;
+          for (int w = sub; w < W; w += 4) {
+            const uint32_t wa = mi[w], wb = mj[w];
+            uint32_t m = wa & wb;
+            const int bi = pim[w], bj = pjm[w];
+            while (m) {
+              const int bit = __ffs(m) - 1;
+              m &= m - 1u;
+              const uint32_t lo = (1u << bit) - 1u;
+              fl[off++] = static_cast<uint16_t>((bi + __popc(wa & lo)) | ((bj + __popc(wb & lo)) << 8));
+            }
+          }
+        }
+        stat = !valid ? 0x200 : (ok ? sg : 0x100);
+      }
+      __syncwarp();
+      for (int gg = 0; gg < kBatch; ++gg) {
+      const int st = __shfl_sync(0xffffffffu, stat, gg * 4);
+      if (st & 0x200) continue;  // warp-uniform
+      const int k0 = warp + kWarps * (t0 + gg);
+      const int r = k0 >> 5, c = k0 & 31;
+      const int64_t gi = i0 + r, gj = j0 + c;
+      const int ri = r, rj = kTile + c;
+      const int ci = rcnt[ri], cj = rcnt[rj];
+      double* ot = otile + r * tstride + c;
+      auto overflow = [&]() {
+        if (lane == 0) {
+          const unsigned long long slot = atomicAdd(sa.ovf_count, 1ull);
+          if (static_cast<int64_t>(slot) < sa.ovf_cap) {
+            sa.ovf_pairs[2 * slot] = gi;
+            sa.ovf_pairs[2 * slot + 1] = gj;
+          }
+          for (int v = 0; v < nnu; ++v) ot[v * kTile * tstride] = -1.0;
+        }
+      };
+      if (st & 0x100) {
+        overflow();
+        continue;
+      }
+      const int s = st;
+      const uint16_t* fl = FL + gg * kFLStride;
+      if (lane < 16) QM[lane] = 0u;
+      __syncwarp();
+      const float* svi = ssv + ri * stride;
+      const float* svj = ssv + rj * stride;
+      // ---- F's values and sorted positions in both rows; position masks
+      double z[2];
+      int lbp[2];  // histogram position of this lane's S_ab values (-1: none)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = lane + 32 * u;
+        z[u] = 0.0;
+        lbp[u] = -1;
+        if (e < s) {
+          const uint32_t pk = fl[e];
+          const int pI = spm[ri * stride + (pk & 255u)], pJ = spm[rj * stride + (pk >> 8)];
+          z[u] = static_cast<double>(svi[pI]) - static_cast<double>(svj[pJ]);
+          atomicOr(QM + (pI >> 5), 1u << (pI & 31));
+          atomicOr(QM + 8 + (pJ >> 5), 1u << (pJ & 31));
+        }
+      }
+      int mneg = 0, mpos = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const unsigned bn = __ballot_sync(0xffffffffu, z[u] < 0.0);
+        const unsigned bq = __ballot_sync(0xffffffffu, z[u] > 0.0);
+        if (z[u] < 0.0) BL[mneg + __popc(bn & lt)] = z[u];
+        if (z[u] > 0.0) BL[kCap + mpos + __popc(bq & lt)] = z[u];
+        mneg += __popc(bn);
+        mpos += __popc(bq);
+      }
+      __syncwarp();
+      {  // word prefixes of the two masks (groups of 8 lanes)
+        const uint32_t wv = (lane < 16) ? QM[lane] : 0u;
+        const int pc = __popc(wv);
+        int x = pc;
+#pragma unroll
+        for (int dd = 1; dd < 8; dd <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, x, dd, 8);
+          if ((lane & 7) >= dd) x += o;
+        }
+        if (lane < 16) QM[16 + lane] = static_cast<uint32_t>(x - pc);
+      }
+      __syncwarp();
+      const int n_neg = (cj - s) + mneg, n_pos = (ci - s) + mpos;
+      const int zeros = d - n_neg - n_pos;
+      // ---- S_ab values: rank in their sign group, lower bound in the other row
+      bool bad = false;
+      int bidx[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        bidx[u] = -1;
+        const double zz = z[u];
+        if (zz == 0.0) continue;
+        const bool pos = zz > 0.0;
+        const double* L = BL + (pos ? kCap : 0);
+        const int len = pos ? mpos : mneg;
+        int cl = 0, ce = 0;
+        for (int q = 0; q < len; ++q) {
+          const double o = L[q];
+          cl += (o < zz) ? 1 : 0;
+          ce += (o == zz) ? 1 : 0;
+        }
+        if (ce != 1) bad = true;  // two equal S_ab values
+        const double mg = fabs(zz);
+        const float f = __double2float_rz(mg);
+        const bool inexact = static_cast<double>(f) != mg;
+        const uint32_t tt = __float_as_uint(f) + (inexact ? 1u : 0u);
+        const int n = pos ? ci : cj;
+        const int prow = pos ? ri : rj;
+        const uint32_t* sb = reinterpret_cast<const uint32_t*>(ssv) + prow * stride;
+        const uint8_t* tb = sbk + prow * 256;
+        const int bk = min(255, __float2int_rz(f * rscale[prow]));
+        int lb = tb[bk];
+        const int end = (bk < 255) ? static_cast<int>(tb[bk + 1]) : n;
+        while (lb < end && sb[lb] < tt) ++lb;  // #{row values < |zz|}
+        if (!inexact && lb < n && sb[lb] == tt) bad = true;  // equal to a value of the other row
+        const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
+        const int less = pos ? n_neg + zeros + cl + (lb - ql) : cl + (cj - lb) - (s - ql);
+        bidx[u] = 2 * less + 1;
+        lbp[u] = (lb < n) ? (pos ? lb : 256 + lb) : -1;
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+        overflow();
+        continue;
+      }
+      double acc[NNU];
+#pragma unroll
+      for (int v = 0; v < NNU; ++v) acc[v] = 0.0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (lbp[u] >= 0) hist_add(HI, lbp[u]);  // HJ == HI + 128: position 256 + lb
+        if (bidx[u] >= 0) {
+#pragma unroll
+          for (int v = 0; v < NNU; ++v)
+            if (NNU == 1 || v < nnu) acc[v] = fma(z[u], __ldg(a.lut + v * lstride + bidx[u]), acc[v]);
+        }
+      }
+      __syncwarp();
+      // ---- one pass over each row's nonzeros (S_a of row i, S_b of row j)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const bool RI = side == 0;
+        const int cnt = RI ? ci : cj;
+        const float* sv = RI ? svi : svj;
+        const uint32_t* qm = QM + (RI ? 0 : 8);
+        const uint32_t* qp = QM + (RI ? 16 : 24);
+        const uint32_t* H = RI ? HI : HJ;
+        int carry = 0;
+        for (int base = 0; base < cnt; base += 32) {
+          const int k = base + lane;
+          const bool in = k < cnt;
+          const uint32_t qw = qm[base >> 5];
+          const int rem = (qw >> lane) & 1u;
+          const bool live = in && !rem;
+          const float x = in ? sv[k] : -2.f;
+          // S_ab values counted at positions <= k: a popc of the chunk's occupied
+          // positions, or a warp scan when a position holds more than one
+          const int hc = in ? hist_get(H, k) : 0;
+          const unsigned occ = __ballot_sync(0xffffffffu, hc > 0);
+          int hs;
+          if (__any_sync(0xffffffffu, hc > 1)) {
+            hs = hc;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+              const int o = __shfl_up_sync(0xffffffffu, hs, dd);
+              if (lane >= dd) hs += o;
+            }
+            hs += carry;
+            carry = __shfl_sync(0xffffffffu, hs, 31);
+          } else {
+            hs = carry + __popc(occ & (lt | (1u << lane)));
+            carry += __popc(occ);
+          }
+          int g0 = k, g1 = k + 1;
+          int rb0 = static_cast<int>(qp[base >> 5]) + __popc(qw & lt);
+          int rb1 = rb0 + rem;
+          // tie groups in the row (clipped values, repeats) from the row's tie bits:
+          // group bounds by bit scans; only a group crossing a 32-entry chunk walks the row
+          const int prow = RI ? ri : rj;
+          const uint32_t tw = stie[prow * 8 + (base >> 5)];
+          const uint32_t pbit = (base > 0) ? (stie[prow * 8 + (base >> 5) - 1] >> 31) : 0u;
+          const bool tied = live && ((lane > 0 ? (tw >> (lane - 1)) & 1u : pbit) || ((tw >> lane) & 1u));
+          if (tied) {
+            const uint32_t below = ~tw & lt;                    // positions t < lane with v_t != v_(t+1)
+            const uint32_t above = ~tw & (0xffffffffu << lane);  // positions t >= lane with v_t != v_(t+1)
+            bool cross = false;
+            if (below) {
+              g0 = base + 32 - __clz(below);
+            } else {
+              g0 = base;
+              cross = pbit != 0;
+            }
+            if (above) {
+              g1 = base + __ffs(above);
+            } else {
+              g1 = base + 32;
+              cross = true;
+            }
+            if (cross) {
+              while (g0 > 0 && sv[g0 - 1] == x) --g0;
+              while (g1 < cnt && sv[g1] == x) ++g1;
+            }
+            rb0 = qcount(qm, qp, g0, s);
+            rb1 = qcount(qm, qp, g1, s);
+          }
+          if (live) {
+            const int eq = (g1 - g0) - (rb1 - rb0);
+            const int less = RI ? n_neg + zeros + (g0 - rb0) + hs : (cnt - g1) - (s - rb1) + (mneg - hs);
+            const int idx = 2 * less + eq;
+            const double zv = RI ? static_cast<double>(x) : -static_cast<double>(x);
+#pragma unroll
+            for (int v = 0; v < NNU; ++v)
+              if (NNU == 1 || v < nnu) acc[v] = fma(zv, __ldg(a.lut + v * lstride + idx), acc[v]);
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (lbp[u] >= 0) HI[lbp[u] >> 1] = 0u;  // leave the histograms zero
+#pragma unroll
+      for (int v = 0; v < NNU; ++v) {
+        if (NNU > 1 && v >= nnu) break;
+        double sum = acc[v];
+#pragma unroll
+        for (int dd = 16; dd > 0; dd >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, dd);
+        if (lane == 0) {
+          const double val = clamp_nonneg(half_p * sum);
+          ot[v * kTile * tstride] = val;
+          if (isinf(val)) atomicOr(a.flag, 1);
+        }
+      }
+      __syncwarp();
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    tile_epilogue<TO>(a, otile, kTile, tstride, i0, j0, out, s_score, s_red);
+    __syncthreads();
+  }
+  score_flush(a, s_score);
+}
+
+inline size_t gen2_smem(int W, int maxnnz, int nnu, int nwarps) {
+  using namespace gmd_detail;
+  using namespace gmd2_detail;
+  return static_cast<size_t>(nwarps) * kGenWords2 * 8 + static_cast<size_t>(nnu) * kTile * (kTile + 1) * 8 +
+         kRows * (8 + 8 + 8 + 4 + 4) + kRows * W * 4 + ((kRows * W + 1) & ~1) * 2 +
+         static_cast<size_t>(kRows) * maxnnz * 4 + ((static_cast<size_t>(kRows) * maxnnz + 1) & ~size_t(1)) * 2 +
+         kRows * 8 * 4 + kRows * 256 + 16;
+}
+void launch_gini_gen2(const GmdArgs& ga, void* dout, gmds_dtype ot, size_t smem, unsigned blocks, int nwarps,
+                      cudaStream_t st);
 
 inline size_t gmd_smem(int W, int maxnnz, int nnu, int nwarps) {
   using namespace gmd_detail;

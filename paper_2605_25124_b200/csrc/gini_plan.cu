@@ -363,13 +363,27 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     }
     if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd2_warps = std::atoi(e);
   }
-  const bool use2 = gmd2 && gmd2_warps > 0;
+  bool use2 = gmd2 && gmd2_warps > 0;
   // other nu (at most 4 per launch, store mode): the general counting kernel on the same panels
   const bool general = !linear && score == nullptr && nnu <= 4 && !std::getenv("GMDS_NO_GEN");
+  // ... as gini_gen2_kernel (the same three changes; GMDS_GEN_V1=1: the round-1 kernel)
+  if (general && !std::getenv("GMDS_GEN_V1")) {
+    for (int nw : {28, 24})
+      if (!gmd2_warps && gen2_smem(rs.W, gmd2_stride, nnu, nw) <= gmd_budget) gmd2_warps = nw;
+    if (!gmd2_warps) {
+      gmd2_warps = 24;
+      while (gmd2_stride > 32 && gen2_smem(rs.W, gmd2_stride, nnu, gmd2_warps) > gmd_budget) gmd2_stride -= 8;
+      if (gen2_smem(rs.W, gmd2_stride, nnu, gmd2_warps) > gmd_budget) gmd2_warps = 0;
+    }
+    if (const char* e = std::getenv("GMDS_GMD_WARPS")) gmd2_warps = std::atoi(e);
+    use2 = gmd2_warps > 0;
+  }
   if ((linear || general) && sparse && rs.nonneg && p > 32 && xt == GMDS_F32 && gmd_warps > 0) {
     // nu in {2, 3}: D from per-row prefix sums and the shared features (gini_gmd.cuh);
     // other nu: midranks counted from the same structures, one LUT pass (gini_gen_kernel)
-    const size_t gsm = use2 ? gmd2_smem(rs.W, gmd2_stride, nnu, gmd2_warps) : gmd_smem(rs.W, gmd_stride, nnu, gmd_warps);
+    const size_t gsm = !use2 ? gmd_smem(rs.W, gmd_stride, nnu, gmd_warps)
+                             : (linear ? gmd2_smem(rs.W, gmd2_stride, nnu, gmd2_warps)
+                                       : gen2_smem(rs.W, gmd2_stride, nnu, gmd2_warps));
     a.tile = gmd_detail::kTile;
     a.nbt = ceil_div(n, a.tile);
     const int64_t units = a.nbt * (a.nbt + 1) / 2;
@@ -411,8 +425,10 @@ void run_gini(const void* dX, gmds_dtype xt, int64_t n, int64_t p, const double*
     chunked(a, [&](GiniTileArgs& g) {
       ga.s.g = g;
       const unsigned blk = static_cast<unsigned>(std::min<int64_t>(g.tile_end - g.tile_begin, int64_t(1) << 30));
-      if (use2)
+      if (use2 && linear)
         launch_gini_gmd2(ga, dD, ot, gsm, blk, gmd2_warps, st);
+      else if (use2)
+        launch_gini_gen2(ga, dD, ot, gsm, blk, gmd2_warps, st);
       else if (linear)
         launch_gini_gmd(ga, dD, ot, gsm, blk, gmd_warps, st);
       else

@@ -712,10 +712,11 @@ __global__ void __launch_bounds__(kThreads, GMDS_TMA_MINB(MODE, Q)) stress_tma_k
 }
 
 // Device loop, kruskal, q <= 3: the passes a unit of the enqueued chain may need, behind two
-// launches instead of six (each skipped pass used to cost an empty launch): WHICH 0 = the
+// three launches instead of six (each skipped pass used to cost an empty launch): WHICH 0 = the
 // difference pass of a pending decision (MODE 3, or 5 when single), WHICH 1 = the unit's main
-// pass -- two-trial fused (2), one-point (1: solo / fix), or the tiny phase's difference +
-// gradient pass (6 / 7).  The GdState the passes' own guards read selects the body.
+// pass -- two-trial fused (2) or one-point (1: solo / fix), WHICH 2 = the tiny phase's
+// difference + gradient pass (6 / 7; with the main pass in one kernel the fused body spilled
+// 388 B at q = 2).  The GdState the passes' own guards read selects the body.
 template <int Q, int WHICH>
 __global__ void __launch_bounds__(kThreads, 2) stress_tma_multi_kernel(PassArgs a, PassArgs d) {
   pdl_wait();
@@ -727,15 +728,14 @@ __global__ void __launch_bounds__(kThreads, 2) stress_tma_multi_kernel(PassArgs 
     if (g->pending == 0) return;
     if (g->single != 0) stress_tma_body<Q, 5, kKruskal>(d, dyn);
     else stress_tma_body<Q, 3, kKruskal>(d, dyn);
+  } else if constexpr (WHICH == 1) {
+    if (g->tiny != 0) return;
+    if (g->solo != 0 || g->fix != 0) stress_tma_body<Q, 1, kKruskal>(a, dyn);
+    else stress_tma_body<Q, 2, kKruskal>(a, dyn);
   } else {
-    if (g->tiny != 0) {
-      if (g->single != 0) stress_tma_body<Q, 7, kKruskal>(d, dyn);
-      else stress_tma_body<Q, 6, kKruskal>(d, dyn);
-    } else if (g->solo != 0 || g->fix != 0) {
-      stress_tma_body<Q, 1, kKruskal>(a, dyn);
-    } else {
-      stress_tma_body<Q, 2, kKruskal>(a, dyn);
-    }
+    if (g->tiny == 0) return;
+    if (g->single != 0) stress_tma_body<Q, 7, kKruskal>(d, dyn);
+    else stress_tma_body<Q, 6, kKruskal>(d, dyn);
   }
 }
 
@@ -816,6 +816,10 @@ constexpr size_t tma_multi_smem() {
       GMDS_CUDA(cudaFuncSetAttribute(stress_tma_multi_kernel<QQ, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      static_cast<int>(tma_multi_smem<QQ>())));                            \
       launch_pdl(stress_tma_multi_kernel<QQ, 0>, dim3(g), dim3(kThreads), tma_multi_smem<QQ>(), st, a, d); \
+    } else if (which == 2) {                                                                              \
+      GMDS_CUDA(cudaFuncSetAttribute(stress_tma_multi_kernel<QQ, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     static_cast<int>(tma_multi_smem<QQ>())));                            \
+      launch_pdl(stress_tma_multi_kernel<QQ, 2>, dim3(g), dim3(kThreads), tma_multi_smem<QQ>(), st, a, d); \
     } else {                                                                                              \
       GMDS_CUDA(cudaFuncSetAttribute(stress_tma_multi_kernel<QQ, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                      static_cast<int>(tma_multi_smem<QQ>())));                            \
