@@ -489,7 +489,7 @@ def run_engine(args, rank, world, dist):
                    "parallelism": f"dp{world}: distance pair tiles and the fit's packed blocks sharded over {world} GPU(s), one NCCL all-reduce per stress pass"},
         "distance_ms": t_dist * 1e3,
         "distance_general_nu": {"nu": NU_GENERAL, "ms": t_general * 1e3, "pairs_per_s": npairs / t_general,
-                                "kernel": "gini_gen_kernel (midranks counted, one LUT pass)",
+                                "kernel": "gini_gen2_kernel (midranks counted, one LUT pass)",
                                 "alu_frac_of_nominal": npairs * ops_pair / t_general / alu_nominal},
         "stress_iters_per_sec": iters_per_sec,
         "stress_resolved_steps": resolved,
@@ -498,7 +498,7 @@ def run_engine(args, rank, world, dist):
         "gpu_launches": int(dist_launches + stress_launches),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": alu_nominal / 1e12, "unit": "Tops/s",
                      "frac": achieved / alu_nominal, "traffic": traffic_dist, "traffic_unit": "bytes/launch (ncu)",
-                     "kernel": "gini_gmd_kernel (nu = 2: linear-weight path)", "ops_per_pair": ops_pair,
+                     "kernel": "gini_gmd2_kernel (nu = 2: linear-weight path)", "ops_per_pair": ops_pair,
                      "peak_source": f"nominal: {props.multi_processor_count} SMs x 128 lanes x {sm_max:.0f} MHz "
                                     "(MEASURED_PEAKS.json has no ALU figure)",
                      "probe_peak": alu.value / 1e12, "frac_of_probe": achieved / alu.value,
@@ -508,7 +508,7 @@ def run_engine(args, rank, world, dist):
                             "bytes_per_iter": bytes_iter,
                             "achieved": ach_iter, "frac": ach_iter / hbm,
                             "iterations": f"1-{STRESS_ITERS} of the fit (the bench's stress step)",
-                            "traffic": traffic_stress, "kernel": "stress_tma_kernel fused (+ reductions, gd_step)"},
+                            "traffic": traffic_stress, "kernel": "stress_tma_multi_kernel<2,1> fused body (+ reductions, gd_step)"},
         "clocks": clk.summary(),
         "clocks_stress": clk2.summary(),
     }

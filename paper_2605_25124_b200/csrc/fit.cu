@@ -494,8 +494,11 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
     GMDS_CUDA(cudaMemcpyAsync(&S, gdst.get() + par, sizeof S, cudaMemcpyDeviceToHost, st));
     GMDS_CUDA(cudaStreamSynchronize(st));
     if (std::getenv("GMDS_TRACE"))
-      std::fprintf(stderr, "[gmds] device_gd: it=%d step=%.3e f=%.9g pred=%d tiny=%d solo=%d pending=%d stop=%d miss=%d\n",
-                   S.it, S.step, S.f, S.pred, S.tiny, S.solo, S.pending, S.stop, S.solo_miss);
+      std::fprintf(stderr,
+                   "[gmds] device_gd: it=%d step=%.3e f=%.9g pred=%d tiny=%d solo=%d pending=%d stop=%d miss=%d fix=%d rt=%d "
+                   "halv=%d nextra=%d ndiff=%d t0=%.12g t1=%.12g gsq=%.6g\n",
+                   S.it, S.step, S.f, S.pred, S.tiny, S.solo, S.pending, S.stop, S.solo_miss, S.fix, S.rt, S.halv,
+                   S.nextra, S.ndiff, S.t0, S.t1, S.gsq);
     if (S.stop != 0) break;
   }
   // passes: the prime plus one per decision that continued (all accepted ones but a final stop)

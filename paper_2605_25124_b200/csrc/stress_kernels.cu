@@ -513,9 +513,10 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     }
   }
   const int acc_slot = (acc_c < 0) ? -1 : ((rt || S.pred == 0) ? acc_c : 1 - acc_c);
-  // (also after a pending decision's two-trial difference pass, phase 1 -- the borderline full steps
-  // land there; the tiny phase's decisions stay with the host)
-  const bool devok = ondev != 0 && (!diffdec || (phase == 1 && S.single == 0 && S.tiny == 0));
+  // (also after a two-trial difference pass -- a pending decision's, phase 1, where the borderline
+  // full steps land, or the tiny phase's both-trial pass; a first-trial-only pass that rejects its
+  // trial is repeated as a pending two-trial decision, below)
+  const bool devok = ondev != 0 && (!diffdec || S.single == 0);
   if (devok && acc_slot == 1) {
     // The other trial was accepted (embed.cpp:244-256 with the point in slot 1): Y moves there;
     // its gradient comes from this unit's pass (MODE 1 at Y) and the next gd_step forms the
@@ -564,6 +565,16 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     R.nextra = S.nextra + 1;
     if (lead) publish(R);
     finish_body(1.0, graw, Y, m, R.step, __dmul_rn(R.step, 0.5), cand0, cand1, sqnext, red);
+    return;
+  }
+  if (ondev && acc_c < 0 && diffdec && phase == 0 && S.single != 0 && kind == kKruskal && gsq > 0.0) {
+    // tiny phase, first trial only, rejected: both trials by differences in this unit's difference
+    // slot, decided by phase 1 (whose outcomes all stay on the device)
+    R.pending = 1;
+    R.single = 0;
+    R.tiny = 0;
+    R.ndiff = S.ndiff + 1;
+    if (lead) publish(R);
     return;
   }
   if (acc_c < 0 || acc_slot != 0) {  // host takes this iteration

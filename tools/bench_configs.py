@@ -179,7 +179,9 @@ def warmup():
         G.minimize_stress(D, 2, kind, max_iters=3)
         G.minimize_stress(D, 3, kind, max_iters=3)
     G.pairwise_gini(X.astype(np.float32), [2.0])
-    G.pairwise_gini(np.abs(X).astype(np.float32) * (X > 0), [2.0])
+    Xs = (np.abs(X) * (rng.random(X.shape) < 0.25)).astype(np.float32)  # sparse, non-negative, p > 32
+    G.pairwise_gini(Xs, [2.0])   # gini_gmd2_kernel (lazy kernel load)
+    G.pairwise_gini(Xs, [2.5])   # gini_gen2_kernel
 
 
 def main():
