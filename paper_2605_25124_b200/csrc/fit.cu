@@ -12,8 +12,10 @@
 // halving loop would accept.  SMACOF needs one pass per iteration: the pass
 // at Z yields loss(Z) and the Guttman transform of Z together.
 #include <cusolverDn.h>
+#include <sys/mman.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1315,6 +1317,39 @@ void download_full(const gmds_dmat* d, double* dst, cudaStream_t st) {
     }
   } evg{ev};
   const int64_t nstripes = ceil_div(n, R);
+  // The destination is usually a fresh pageable allocation (an Eigen matrix): its 4 KB first-touch
+  // faults add to the copy-out.  Ask for huge pages; optionally populate the stripes ahead of the
+  // copy threads (MADV_POPULATE_WRITE leaves contents alone; both hints may be refused -- ignored).
+  const uintptr_t page = 4096;
+  const uintptr_t a0 = (reinterpret_cast<uintptr_t>(dst) + page - 1) & ~(page - 1);
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(dst) + static_cast<size_t>(n) * n * sizeof(double)) & ~(page - 1);
+  std::atomic<int64_t> pf_next{0};
+  std::vector<std::thread> pf;
+  // GMDS_PREFAULT = "none" | "huge" (default) | "pop" | "both".  Measured on the B200 box (metric shape,
+  // 3.2 GB, tools/facade_ab.py): none 437 ms, huge 425, pop 723, both 534 per facade call -- the copy-out
+  // is bound by host memory traffic, not by faults, so only the huge-page hint stays on.
+  const char* pfm = std::getenv("GMDS_PREFAULT");
+  const bool pf_huge = !pfm || !std::strcmp(pfm, "huge") || !std::strcmp(pfm, "both");
+  const bool pf_pop = pfm && (!std::strcmp(pfm, "pop") || !std::strcmp(pfm, "both"));
+  if (a1 > a0 && (pf_huge || pf_pop)) {
+    if (pf_huge) madvise(reinterpret_cast<void*>(a0), a1 - a0, MADV_HUGEPAGE);
+    for (int t = 0; t < (pf_pop ? 4 : 0); ++t)
+      pf.emplace_back([&, a0, a1] {
+        for (;;) {
+          const int64_t s = pf_next.fetch_add(1);
+          if (s >= nstripes) break;
+          const uintptr_t b0 = std::max(a0, (reinterpret_cast<uintptr_t>(dst + static_cast<size_t>(s * R * n)) + page - 1) & ~(page - 1));
+          const uintptr_t b1 = std::min(a1, reinterpret_cast<uintptr_t>(dst + static_cast<size_t>(std::min(n, (s + 1) * R) * n)) & ~(page - 1));
+          if (b1 > b0 && madvise(reinterpret_cast<void*>(b0), b1 - b0, 23 /* MADV_POPULATE_WRITE */) != 0) break;
+        }
+      });
+  }
+  struct Join {
+    std::vector<std::thread>& v;
+    ~Join() {
+      for (auto& x : v) x.join();
+    }
+  } pfj{pf};
   auto enqueue = [&](int64_t s) {
     const int b = static_cast<int>(s & 1);
     const int64_t r0 = s * R, r1 = std::min(n, r0 + R);
