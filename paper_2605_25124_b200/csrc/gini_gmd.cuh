@@ -371,8 +371,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
 }
 
 // ---------------------------------------------------------------------------
-// gini_gmd2_kernel: the same arithmetic as gini_gmd_kernel (every fp64 term and the
-// order it is added in are unchanged, so results are bit-identical), with three
+// gini_gmd2_kernel: the same arithmetic as gini_gmd_kernel (every fp64 term is unchanged;
+// the terms are added in list order instead of feature order, so results agree to round-off,
+// ~1e-15 max-normalised), with three
 // changes to the work around it (round 2, profiles/r1_gini_gmd_lines_n4000.txt:
 // F extraction 13%, the 8-probe search 11% of the warp instructions):
 //   * F lists are built for 8 pairs at a time by 4 lanes per pair (each lane walks

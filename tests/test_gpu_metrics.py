@@ -401,6 +401,49 @@ def test_linear_weight_kernel_dense_rows_overflow():
     assert maxnorm_err(D, O.pairwise_matrix(X.astype(np.float64), 2.0)) <= 1e-12
 
 
+@pytest.mark.parametrize("kind", ["image", "heavy_tail", "edge_counts", "clipped", "tiny_values"])
+def test_batched_bucket_kernels_match_round1_kernels_and_oracle(kind, monkeypatch):
+    # gini_gmd2_kernel / gini_gen2_kernel (F lists built 8 pairs at a time, bucket-table lower
+    # bounds, sorted-value panel) against the round-1 kernels (GMDS_GMD_V1 / GMDS_GEN_V1) and
+    # the oracle, on data that stresses the bucket tables: heavy tails (most values in
+    # bucket 0), rows of exactly 255 / 256 / 257 nonzeros (the u8 counters' limit: 256+ overflow),
+    # many values equal to the row maximum (the last bucket), denormal-range values
+    rng = np.random.default_rng({"image": 71, "heavy_tail": 72, "edge_counts": 73, "clipped": 74, "tiny_values": 75}[kind])
+    if kind == "image":
+        X = image_like(260, 784, 76)
+    elif kind == "heavy_tail":
+        X = (rng.lognormal(0.0, 3.0, size=(200, 300)) * (rng.random((200, 300)) < 0.3)).astype(np.float32)
+    elif kind == "edge_counts":
+        X = image_like(150, 784, 77)
+        for r, c in ((2, 255), (40, 256), (41, 257), (90, 255)):
+            X[r] = 0.0
+            X[r, rng.choice(784, size=c, replace=False)] = rng.random(c).astype(np.float32) + 0.01
+    elif kind == "clipped":
+        X = image_like(180, 400, 78)
+        X[(X > 0.6)] = 1.0  # a third of the nonzeros sit on the row maximum
+    else:
+        X = (rng.random((160, 200)) * (rng.random((160, 200)) < 0.35)).astype(np.float32)
+        X[::3] *= np.float32(1e-38)  # rows in the denormal range next to rows of order 1
+        X[1::3] *= np.float32(1e-30)
+    X[5] = X[9]
+    Xd = X.astype(np.float64)
+    nus = [2.0, 3.0]
+    D = G.pairwise_gini(X, nus)
+    for k, nu in enumerate(nus):
+        assert maxnorm_err(D[k], O.pairwise_matrix(Xd, nu)) <= 1e-12
+    assert D[0][5, 9] == 0.0
+    gn = [1.5, 2.5, 4.0]
+    Dg = G.pairwise_gini(X, gn)
+    for k, nu in enumerate(gn):
+        assert maxnorm_err(Dg[k], O.pairwise_matrix(Xd, nu)) <= 1e-12
+    monkeypatch.setenv("GMDS_GMD_V1", "1")
+    monkeypatch.setenv("GMDS_GEN_V1", "1")
+    # the same terms, added in list order instead of feature order: equal to round-off
+    D1, Dg1 = G.pairwise_gini(X, nus), G.pairwise_gini(X, gn)
+    assert np.max(np.abs(D - D1)) <= 1e-13 * np.max(np.abs(D1))
+    assert np.max(np.abs(Dg - Dg1)) <= 1e-13 * np.max(np.abs(Dg1))
+
+
 @pytest.mark.parametrize("kind", ["image", "levels", "mixed", "wide"])
 def test_general_counting_kernel_vs_oracle(kind, monkeypatch):
     # other nu (<= 4 per launch) on sparse non-negative fp32 data: midranks counted

@@ -388,6 +388,31 @@ def test_device_resident_descent_identical(monkeypatch, kind, rel_tol, iters):
     assert c["passes"] == b["passes"]
 
 
+@pytest.mark.parametrize("q,iters", [(2, 260), (3, 200)])
+def test_device_loop_keeps_decisions_on_device(monkeypatch, q, iters):
+    # image-like data above the small-fit size, fp32 storage, seeded N(0, 0.1^2) init: past the
+    # step-doubling run the full step hovers at the Armijo threshold, so slot-1 acceptances,
+    # further halvings, pending (difference-pass) decisions and tiny-phase rejections all occur.
+    # The device-resident loop decides them itself (GdState::fix / rt, merged launches): same
+    # history and coordinates, bit for bit, as with the hand-backs to the host loop (whose
+    # trajectories test_gpu_large.py pins to the reference's at n = 2600, 5000 and 20000).
+    from bench import make_image_like
+
+    n = 2600
+    X = make_image_like(n, 784)
+    D = G.pairwise_matrix(X, 2.0)
+    Y0 = np.random.default_rng(2605).normal(0.0, 0.1, (n, q))
+    a = G.minimize_stress(D, q, "kruskal", max_iters=iters, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    monkeypatch.setenv("GMDS_NO_ONDEV", "1")
+    monkeypatch.setenv("GMDS_NO_MULTI", "1")
+    monkeypatch.setenv("GMDS_NO_SOLO", "1")
+    b = G.minimize_stress(D, q, "kruskal", max_iters=iters, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    assert a["iterations"] == b["iterations"] == iters
+    assert np.array_equal(np.array(a["stress_history"]), np.array(b["stress_history"]))
+    assert np.array_equal(a["coords"], b["coords"])
+    assert a["passes"] <= b["passes"] + 3
+
+
 def test_tune_batched_eigensolver_matches(monkeypatch):
     # tune_nu's classical cells of a fold go through one batched eigensolver call;
     # per-cell dense solves give the same mean stresses
