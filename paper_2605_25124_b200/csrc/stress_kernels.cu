@@ -599,7 +599,16 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
   // quarter of the resolution threshold, so the doubled step will not be resolved either: the
   // next pass is the difference + gradient pass, of the first trial only when it leads the
   // slot order (if it is rejected the iteration goes to the host, which evaluates both)
-  R.tiny = (tiny_ok && diffdec && fabs(__dsub_rn(fY, f_new)) <= 0.25 * tol) ? 1 : 0;
+  // ... or this decision, taken on difference sums, would have been unresolved on plain fp32 sums
+  // (the full step sitting at the Armijo threshold, run after run in the late regime): the next
+  // iteration's fused pass would need a difference pass again -- one difference + gradient pass
+  // instead of the two (tiny_ok == 2: q <= 2, where that pass does not spill -- at q = 3 it measured
+  // no faster than the two; GMDS_TINY_STICKY=0 keeps the magnitude rule alone)
+  const bool would_unres =
+      tiny_ok == 2 && diffdec && precise_rel > 0.0 &&
+      ((fabs(loss_of(t0) - fY) <= tol && fabs(loss_of(t1) - fY) <= tol) ||
+       armijo_unresolved(fY, S.step, gsq, loss_of(S.pred == 0 ? t0 : t1), loss_of(S.pred == 0 ? t1 : t0), tol));
+  R.tiny = (tiny_ok && diffdec && (fabs(__dsub_rn(fY, f_new)) <= 0.25 * tol || would_unres)) ? 1 : 0;
   R.single = (R.tiny != 0 && S.pred == 0) ? 1 : 0;
   // solo for the next pass: the full step was just accepted on resolved fp32 sums with room to
   // spare (a change of more than 4 tol), so the doubled step's half-step loss will go unread
@@ -723,6 +732,14 @@ int launch_finish_grad(const double* losspart, int64_t nparts, int stride, int k
   return blocks;
 }
 
+static bool tiny_sticky() {
+  static const bool on = [] {
+    const char* e = std::getenv("GMDS_TINY_STICKY");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t nparts, int stride, const double* sqprev,
                     int nsq, double* sqnext, int kind, double sum_sq, double sum, double* Y, double* cand0,
                     double* cand1, double* gnext, const double* gpart, int Q, double* graw, int64_t m,
@@ -731,7 +748,7 @@ void launch_gd_step(GdState* st2, int par, const double* losspart, int64_t npart
                     bool solo_ok, bool ondev) {
   launch_pdl(gd_step_kernel, dim3(nsq), dim3(256), 0, st, st2, par, losspart, nparts, stride, sqprev, nsq, sqnext,
              kind, sum_sq, sum, Y, cand0, cand1, gnext, gpart, Q, graw, m, history, max_iters, rel_tol, pre,
-             precise_rel, phase, xred, dsum, tiny_ok ? 1 : 0, solo_ok ? 1 : 0, ondev ? 1 : 0);
+             precise_rel, phase, xred, dsum, tiny_ok ? ((tiny_sticky() && Q <= 2) ? 2 : 1) : 0, solo_ok ? 1 : 0, ondev ? 1 : 0);
   count_launch();
   check_launch("gd_step_kernel");
 }
