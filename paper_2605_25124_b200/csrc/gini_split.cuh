@@ -82,11 +82,11 @@ __device__ __forceinline__ void warp_bitonic_upto(double (&v)[K], int lane, int 
         const double o1 = __shfl_xor_sync(kFull, v[r2], m);
         if (r2 != r) {
           const double o2 = __shfl_xor_sync(kFull, v[r], m);
-          const bool t2 = keep_lo ? (o2 < v[r2]) : (v[r2] < o2);
-          v[r2] = t2 ? o2 : v[r2];
+          const bool lt2 = o2 < v[r2], gt2 = v[r2] < o2;
+          v[r2] = sel64(keep_lo ? lt2 : gt2, o2, v[r2]);
         }
-        const bool t1 = keep_lo ? (o1 < v[r]) : (v[r] < o1);
-        v[r] = t1 ? o1 : v[r];
+        const bool lt1 = o1 < v[r], gt1 = v[r] < o1;
+        v[r] = sel64(keep_lo ? lt1 : gt1, o1, v[r]);
       }
     }
 #pragma unroll
@@ -101,8 +101,8 @@ __device__ __forceinline__ void warp_bitonic_upto(double (&v)[K], int lane, int 
 #pragma unroll
         for (int r = 0; r < K; ++r) {
           const double o = __shfl_xor_sync(kFull, v[r], m);
-          const bool tk = keep_lo ? (o < v[r]) : (v[r] < o);
-          v[r] = tk ? o : v[r];
+          const bool lt = o < v[r], gt = v[r] < o;
+          v[r] = sel64(keep_lo ? lt : gt, o, v[r]);
         }
       }
     }
@@ -128,8 +128,8 @@ __device__ __forceinline__ void warp_bitonic_merge(double (&v)[K], int lane) {
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         const double o = __shfl_xor_sync(kFull, v[r], m);
-        const bool tk = keep_lo ? (o < v[r]) : (v[r] < o);
-        v[r] = tk ? o : v[r];
+        const bool lt = o < v[r], gt = v[r] < o;
+        v[r] = sel64(keep_lo ? lt : gt, o, v[r]);
       }
     }
   }

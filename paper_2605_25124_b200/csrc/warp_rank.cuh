@@ -26,11 +26,18 @@ namespace gmds {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// c ? a : b as two 32-bit selects.  (ptxas compiled the fp64 `?:` of the cross-lane sort steps
+// into BRA / MOV / BSYNC triples -- 36% of gini_split_kernel's warp instructions at the C4 shape,
+// profiles/r2b_split_c4_lines_n4000.txt; the halves select as SEL.)
+__device__ __forceinline__ double sel64(bool c, double a, double b) {
+  return __hiloint2double(c ? __double2hiint(a) : __double2hiint(b), c ? __double2loint(a) : __double2loint(b));
+}
+
 // Compare-exchange, ascending (lower slot keeps the smaller key).
 __device__ __forceinline__ void ce_asc(double& a, double& b) {
   const bool sw = b < a;
-  const double lo = sw ? b : a;
-  const double hi = sw ? a : b;
+  const double lo = sel64(sw, b, a);
+  const double hi = sel64(sw, a, b);
   a = lo;
   b = hi;
 }
@@ -59,8 +66,8 @@ __device__ __forceinline__ void ce_asc_p(double (&v)[K], typename Payload<kPaylo
                                          int r2) {
   const bool sw = v[r2] < v[r1];
   const double a = v[r1], b = v[r2];
-  v[r1] = sw ? b : a;
-  v[r2] = sw ? a : b;
+  v[r1] = sel64(sw, b, a);
+  v[r2] = sel64(sw, a, b);
   if constexpr (kPayload) {
     const int ia = idx[r1], ib = idx[r2];
     idx[r1] = sw ? ib : ia;
@@ -72,8 +79,9 @@ __device__ __forceinline__ void ce_asc_p(double (&v)[K], typename Payload<kPaylo
 // keep the min if `keep_lo`, else the max.
 template <bool kPayload>
 __device__ __forceinline__ void xchg(double& a, double o, int& ia, int io, bool keep_lo) {
-  const bool take = keep_lo ? (o < a) : (a < o);
-  a = take ? o : a;
+  const bool lt = o < a, gt = a < o;
+  const bool take = keep_lo ? lt : gt;
+  a = sel64(take, o, a);
   if constexpr (kPayload) ia = take ? io : ia;
 }
 
