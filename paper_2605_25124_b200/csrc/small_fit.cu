@@ -168,7 +168,7 @@ __device__ void pass(const Ctx& x, const Src* Zp, double* g, double* mat, const 
               default: term = e * e; cc = Dv; break;  // Guttman: smacof loss + B(Z) Z numerator
             }
             if (ok && j > r) lacc[c] += term;
-            if (GRAD && ok && dist > 0.0) {
+            if (GRAD && c == 0 && ok && dist > 0.0) {  // the gradient belongs to configuration 0
               const double ci = cc / dist;
 #pragma unroll
               for (int k = 0; k < Q; ++k) gacc[k] += ci * dy[k];
@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kSFThreads, 1) small_fit_kernel(SmallFitArgs a
     f = loss_of(raw);
     if (lead) a.history[0] = f;
     double step = 1.0;
+    int pred = 0;  // slot order of the next first-round trial pair (0: step in slot 0)
     for (; it < a.max_iters; ++it) {
       double scale = 1.0;
       if (a.kind == kKruskal) {
@@ -328,15 +329,21 @@ __global__ void __launch_bounds__(kSFThreads, 1) small_fit_kernel(SmallFitArgs a
         scale = 2.0 * (1.0 / a.sum);
       }
       // Armijo trial points in pairs (step, step/2), evaluated inline from
-      // (Y, scaled gradient); the same pass yields |g|^2.
+      // (Y, scaled gradient); the same pass yields |g|^2.  Speculation, as in the
+      // tiled engine (fit.cu gradient_descent): the trial predicted to be accepted
+      // (the same choice, step or step / 2, as the last first-round acceptance) sits
+      // in slot 0, and the pass also takes the gradient and the coordinates there --
+      // a correct prediction saves the separate gradient pass and its grid barrier.
+      // The trials are still tested in the reference's order (step, then step / 2).
       Src tr[2] = {{Yb[yb], Gb[gb], step, scale, 1.0, kStep}, {Yb[yb], Gb[gb], step * 0.5, scale, 1.0, kStep}};
       bool accepted = false, stalled = false;
-      int acc = 0;
-      double f_new = f;
+      int acc = 0;  // slot of the accepted trial
+      double f_new = f, raw_acc = 0.0;
       for (int halvings = 0; halvings < 60; halvings += 2) {
-        tr[0].s = step;
-        tr[1].s = step * 0.5;
-        pass<Q, 2, false>(x, tr, nullptr, nullptr, Gb[gb], scale, lp(), sm);
+        const int first = (halvings == 0) ? pred : 0;  // slot of `step` (later rounds: natural order)
+        tr[first].s = step;
+        tr[first ^ 1].s = step * 0.5;
+        pass<Q, 2, true>(x, tr, Gb[gb ^ 1], Yb[yb ^ 1], Gb[gb], scale, lp(), sm);
         ++npass;
         double tot[3];
         grid.sync();
@@ -346,18 +353,22 @@ __global__ void __launch_bounds__(kSFThreads, 1) small_fit_kernel(SmallFitArgs a
           stalled = true;
           break;
         }
-        const double f0 = loss_of(tot[0]), f1 = loss_of(tot[1]);
+        const double f0 = loss_of(tot[first]), f1 = loss_of(tot[first ^ 1]);  // at step, at step / 2
         if (f0 <= f - 1e-4 * step * tot[2]) {
           accepted = true;
-          acc = 0;
+          acc = first;
           f_new = f0;
+          raw_acc = tot[first];
+          if (halvings == 0) pred = 0;
           break;
         }
         if (f1 <= f - 1e-4 * (step * 0.5) * tot[2]) {
           accepted = true;
-          acc = 1;
+          acc = first ^ 1;
           f_new = f1;
+          raw_acc = tot[first ^ 1];
           step *= 0.5;
+          if (halvings == 0) pred = 1;
           break;
         }
         step *= 0.25;
@@ -376,6 +387,14 @@ __global__ void __launch_bounds__(kSFThreads, 1) small_fit_kernel(SmallFitArgs a
         ++it;
         conv = true;
         break;
+      }
+      if (acc == 0) {
+        // predicted: the trial pass left the gradient, the coordinates and the raw loss there
+        gb ^= 1;
+        yb ^= 1;
+        fin = Src{Yb[yb], nullptr, 0.0, 0.0, 1.0, kPlain};
+        raw = raw_acc;
+        continue;
       }
       // gradient pass at the accepted point; it also materialises its own rows
       pass<Q, 1, true>(x, &fin, Gb[gb ^ 1], Yb[yb ^ 1], nullptr, 0.0, lp(), sm);
