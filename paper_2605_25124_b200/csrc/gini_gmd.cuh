@@ -92,6 +92,13 @@ __device__ __forceinline__ int qcount(const uint32_t* QM, const uint32_t* QP, in
   return static_cast<int>(QP[w]) + __popc(QM[w] & ((1u << (pos & 31)) - 1u));
 }
 
+// the same without the sentinel test, for callers whose positions are < kMaxC whenever the result
+// is used (gini_gmd2_kernel: rows of <= 255 nonzeros; dead lanes pass kMaxC and ignore the result)
+__device__ __forceinline__ int qcount2(const uint32_t* QM, const uint32_t* QP, int pos) {
+  const int w = (pos >> 5) & 7;
+  return static_cast<int>(QP[w]) + __popc(QM[w] & ((1u << (pos & 31)) - 1u));
+}
+
 // per-warp histograms of u16 counters packed two per u32 word
 __device__ __forceinline__ void hist_add(uint32_t* H, int pos) { atomicAdd(H + (pos >> 1), 1u << ((pos & 1) << 4)); }
 __device__ __forceinline__ int hist_get(const uint32_t* H, int pos) { return (H[pos >> 1] >> ((pos & 1) << 4)) & 0xFFFF; }
@@ -580,8 +587,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           if (u == 1 && s <= 32) break;  // warp-uniform
-          rI[u] = qcount(QM, QM + 16, pI[u], s);
-          rJ[u] = qcount(QM + 8, QM + 24, pJ[u], s);
+          rI[u] = qcount2(QM, QM + 16, pI[u]);
+          rJ[u] = qcount2(QM + 8, QM + 24, pJ[u]);
           const bool live = lane + 32 * u < s;
           if (live) {
             PQi[1 + rI[u]] = static_cast<double>(al[u]);
@@ -635,7 +642,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
           if (e >= s) continue;
           const double av = al[u], bv = be[u];
           // pairs of row i touching F (PM(S_a)) and of row j (minima, PM(S_b))
-          const double si1 = (pI[u] + 1 < ci) ? __ldg(sufi + pI[u] + 1) : 0.0;
+          const double si1v = __ldg(sufi + min(pI[u] + 1, ci - 1));  // clamped: no branch around the load
+          const double si1 = (pI[u] + 1 < ci) ? si1v : 0.0;
           const double sj0 = __ldg(sufj + pJ[u]);
           acc += av * static_cast<double>(rI[u] - pI[u]) - si1 - kp * av;
           acc += (s1j - sj0) + bv * static_cast<double>((cj - 1 - pJ[u]) - (s - 1 - rJ[u])) + kn * bv;
@@ -667,8 +675,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
           int lb = tb[bk];
           const int end = (bk < 255) ? static_cast<int>(tb[bk + 1]) : n;
           while (lb < end && sb[lb] < tt) ++lb;
-          const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
-          const double sl = (lb < n) ? __ldg((pos ? sufi : sufj) + lb) : 0.0;
+          const int ql = qcount2(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb);
+          const double slv = __ldg((pos ? sufi : sufj) + min(lb, n - 1));
+          const double sl = (lb < n) ? slv : 0.0;
           if (pos)
             acc += (kp - wneg) * zz + zz * static_cast<double>(lb - ql) + sl - sumQi + PQi[ql];
           else
