@@ -430,12 +430,13 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   // the tiny phase's difference + gradient pass (q <= 3); GMDS_NO_TINY=1: every sub-resolution
   // decision takes the fused pass and a difference pass (the host loop's two passes)
   const bool tiny_ok = dev_diff && Q <= 3 && !std::getenv("GMDS_NO_TINY");
-  // solo passes (GdState::solo): slot 0 only, while the full step keeps being accepted on resolved sums;
-  // single device only (a miss costs a host loss pass); GMDS_NO_SOLO=1: always the two-trial fused pass
-  const bool solo_ok = !comm && !std::getenv("GMDS_NO_SOLO");
   // slot-1 acceptances, further halvings and solo misses decided on the device (GdState::fix / rt);
   // GMDS_NO_ONDEV=1: those iterations go back to the host loop
   const bool ondev = !std::getenv("GMDS_NO_ONDEV");
+  // solo passes (GdState::solo): slot 0 only, while the full step keeps being accepted on resolved sums;
+  // GMDS_NO_SOLO=1: always the two-trial fused pass.  (Row-sharded fits: only with the on-device
+  // miss handling -- the host's miss path is a loss pass without the all-reduce.)
+  const bool solo_ok = (!comm || ondev) && !std::getenv("GMDS_NO_SOLO");
   // kruskal, q <= 3: the difference passes behind one launch and the fused / one-point pass behind one (stress_tma_multi_kernel)
   const bool multi = tiny_ok && ondev && !std::getenv("GMDS_NO_MULTI");
   for (;;) {
