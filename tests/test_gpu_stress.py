@@ -388,6 +388,28 @@ def test_device_resident_descent_identical(monkeypatch, kind, rel_tol, iters):
     assert c["passes"] == b["passes"]
 
 
+@pytest.mark.parametrize("kind,q,iters", [("kruskal", 1, 150), ("kruskal", 3, 150), ("kruskal", 4, 120),
+                                          ("sammon", 3, 120), ("huber", 1, 120), ("huber", 4, 100)])
+def test_device_loop_identical_to_host_loop_other_q(monkeypatch, kind, q, iters):
+    # the on-device fix / re-trial units (GdState::fix, rt) and solo passes at q = 1, 3, 4 and for
+    # the kinds without a difference pass: same history and coordinates, bit for bit, as the
+    # host loop (GMDS_HOST_GD=1); the tiny phase is off on both sides as in the q = 2 test above
+    monkeypatch.setenv("GMDS_NO_TINY", "1")
+    rng = np.random.default_rng(100 + 7 * q + len(kind))
+    n = 2300 + 37 * q
+    X = rng.standard_normal((n, 6)) * np.linspace(2.0, 0.5, 6)
+    D = G.pairwise_matrix(X, 2.0)
+    Y0 = rng.normal(0.0, 0.1, (n, q))
+    hd = 0.5 * float(np.median(D)) if kind == "huber" else None
+    a = G.minimize_stress(D, q, kind, huber_delta=hd, max_iters=iters, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    monkeypatch.setenv("GMDS_HOST_GD", "1")
+    b = G.minimize_stress(D, q, kind, huber_delta=hd, max_iters=iters, rel_tol=1e-300, Y0=Y0, storage=G.F32)
+    assert a["iterations"] == b["iterations"] and a["converged"] == b["converged"]
+    assert np.array_equal(np.array(a["stress_history"]), np.array(b["stress_history"]))
+    assert np.array_equal(a["coords"], b["coords"])
+    assert a["passes"] <= b["passes"] + max(3, iters // 20)
+
+
 @pytest.mark.parametrize("q,iters", [(2, 260), (3, 200)])
 def test_device_loop_keeps_decisions_on_device(monkeypatch, q, iters):
     # image-like data above the small-fit size, fp32 storage, seeded N(0, 0.1^2) init: past the
