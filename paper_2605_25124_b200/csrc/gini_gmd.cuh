@@ -31,6 +31,8 @@
 // the overflow list (exact full-sort kernel).
 #pragma once
 
+#include <cstdio>
+
 #include "gini_split.cuh"
 
 namespace gmds {
@@ -393,6 +395,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd_kernel(GmdArgs ga, TO
 //   * the panel keeps the sorted values and the position map only (feature-order
 //     values are sv[pmap[k]]), which pays for the lists and the tables in shared memory.
 // Rows with more than 255 nonzeros take the overflow list (bucket counters are bytes).
+// -DGMDS_BOUNDS_CHECK: every index the round-2b kernels form is checked and a violation traps (the
+// stand-in for compute-sanitizer memcheck, which is closed on the GPU pool: tools/gpu/bounds_check.sh)
+#ifdef GMDS_BOUNDS_CHECK
+#define GMDS_CHK(cond)                                                                  \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("GMDS_BOUNDS_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);      \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define GMDS_CHK(cond) ((void)0)
+#endif
+
 namespace gmd2_detail {
 constexpr int kBatch = 8;      // pairs per extraction batch (4 lanes each)
 constexpr int kFLStride = 66;  // u16 per list: 64 entries + pad (33 words: lists start on distinct banks)
@@ -510,6 +526,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
               const int bit = __ffs(m) - 1;
               m &= m - 1u;
               const uint32_t lo = (1u << bit) - 1u;
+              GMDS_CHK(off >= 0 && off < kCap && bi + __popc(wa & lo) < 256 && bj + __popc(wb & lo) < 256);
               fl[off++] = static_cast<uint16_t>((bi + __popc(wa & lo)) | ((bj + __popc(wb & lo)) << 8));
             }
           }
@@ -557,8 +574,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
           if (u == 1 && s <= 32) break;  // warp-uniform: the second element slot is empty
           if (e < s) {
             const uint32_t pk = fl[e];
+            GMDS_CHK(static_cast<int>(pk & 255u) < ci && static_cast<int>(pk >> 8) < cj && ci <= stride && cj <= stride);
             pI[u] = pmi[pk & 255u];
             pJ[u] = pmj[pk >> 8];
+            GMDS_CHK(pI[u] < ci && pJ[u] < cj);
             al[u] = __uint_as_float(svi[pI[u]]);
             be[u] = __uint_as_float(svj[pJ[u]]);
             atomicOr(QM + (pI[u] >> 5), 1u << (pI[u] & 31));
@@ -591,6 +610,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
           rJ[u] = qcount2(QM + 8, QM + 24, pJ[u]);
           const bool live = lane + 32 * u < s;
           if (live) {
+            GMDS_CHK(rI[u] >= 0 && rI[u] < s && rJ[u] >= 0 && rJ[u] < s && s <= kCap);
             PQi[1 + rI[u]] = static_cast<double>(al[u]);
             PQj[1 + rJ[u]] = static_cast<double>(be[u]);
           }
@@ -672,9 +692,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gmd2_kernel(GmdArgs ga, T
           const uint32_t* sb = ssv + prow * stride;
           const uint8_t* tb = sbk + prow * 256;
           const int bk = min(255, __float2int_rz(f * rscale[prow]));
+          GMDS_CHK(bk >= 0 && n >= 1 && n <= stride);
           int lb = tb[bk];
           const int end = (bk < 255) ? static_cast<int>(tb[bk + 1]) : n;
+          GMDS_CHK(lb <= end && end <= n);
           while (lb < end && sb[lb] < tt) ++lb;
+          GMDS_CHK(lb == n || sb[lb] >= tt);
+          GMDS_CHK(lb == 0 || sb[lb - 1] < tt);  // the bucket scan found the exact lower bound
           const int ql = qcount2(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb);
           const double slv = __ldg((pos ? sufi : sufj) + min(lb, n - 1));
           const double sl = (lb < n) ? slv : 0.0;
@@ -1155,6 +1179,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen2_kernel(GmdArgs ga, T
               const int bit = __ffs(m) - 1;
               m &= m - 1u;
               const uint32_t lo = (1u << bit) - 1u;
+              GMDS_CHK(off >= 0 && off < kCap && bi + __popc(wa & lo) < 256 && bj + __popc(wb & lo) < 256);
               fl[off++] = static_cast<uint16_t>((bi + __popc(wa & lo)) | ((bj + __popc(wb & lo)) << 8));
             }
           }
@@ -1201,7 +1226,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen2_kernel(GmdArgs ga, T
         lbp[u] = -1;
         if (e < s) {
           const uint32_t pk = fl[e];
+          GMDS_CHK(static_cast<int>(pk & 255u) < ci && static_cast<int>(pk >> 8) < cj && ci <= stride && cj <= stride);
           const int pI = spm[ri * stride + (pk & 255u)], pJ = spm[rj * stride + (pk >> 8)];
+          GMDS_CHK(pI < ci && pJ < cj);
           z[u] = static_cast<double>(svi[pI]) - static_cast<double>(svj[pJ]);
           atomicOr(QM + (pI >> 5), 1u << (pI & 31));
           atomicOr(QM + 8 + (pJ >> 5), 1u << (pJ & 31));
@@ -1259,9 +1286,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) gini_gen2_kernel(GmdArgs ga, T
         const uint32_t* sb = reinterpret_cast<const uint32_t*>(ssv) + prow * stride;
         const uint8_t* tb = sbk + prow * 256;
         const int bk = min(255, __float2int_rz(f * rscale[prow]));
+        GMDS_CHK(bk >= 0 && n >= 1 && n <= stride);
         int lb = tb[bk];
         const int end = (bk < 255) ? static_cast<int>(tb[bk + 1]) : n;
+        GMDS_CHK(lb <= end && end <= n);
         while (lb < end && sb[lb] < tt) ++lb;  // #{row values < |zz|}
+        GMDS_CHK((lb == n || sb[lb] >= tt) && (lb == 0 || sb[lb - 1] < tt));
         if (!inexact && lb < n && sb[lb] == tt) bad = true;  // equal to a value of the other row
         const int ql = qcount(QM + (pos ? 0 : 8), QM + (pos ? 16 : 24), lb, s);
         const int less = pos ? n_neg + zeros + cl + (lb - ql) : cl + (cj - lb) - (s - ql);
