@@ -382,8 +382,12 @@ Engine::GradTrials Engine::fused_trials(int kind, double delta, double s0, doubl
   return r;
 }
 
+// need_grad: graw does not hold the gradient at Y -- the loop is primed with the one-point pass at Y and
+// the fix state (its first gd_step forms the trials, as after a slot-1 acceptance); init: that pass is the
+// fit's first, its loss is f(Y0) = history[it] (embed.cpp:226).
 GdState Engine::device_gd(int kind, double delta, double f, double step, int it, int pred, int max_iters,
-                          double rel_tol, std::vector<double>& history, double precise_rel) {
+                          double rel_tol, std::vector<double>& history, double precise_rel, bool need_grad,
+                          bool init) {
   if (!sq2.get()) {
     sq2.alloc(2 * kSqBlocks);
     gdst.alloc(2);
@@ -391,15 +395,25 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   if (hist.n < static_cast<size_t>(max_iters) + 1) hist.alloc(static_cast<size_t>(max_iters) + 1);
   if (!gnext.get()) gnext.alloc(static_cast<size_t>(n * Q));
   const double s0 = pred == 0 ? step : step * 0.5, s1 = pred == 0 ? step * 0.5 : step;
-  // prime: the trial pair of iteration `it` and its fused pass (as fused_trials, without the round trip)
-  const int nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(),
-                                     n * Q, s0, s1, cand[0].get(), cand[1].get(), sq2.get(), scal.get(), st,
-                                     comm ? rawy.get() : nullptr);
   PassArgs b = args(kind, delta);
+  int nsq;
+  if (need_grad) {
+    // prime: the gradient pass at Y (as grad_raw, without the round trip); gd_step's fix block finishes it
+    nsq = static_cast<int>(std::min<int64_t>(kSqBlocks, std::max<int64_t>(1, ceil_div(n * Q, 256))));
+    PassArgs g1 = args(kind, delta);
+    g1.Y[0] = Y.get();
+    g1.ncand = 1;
+    launch_stress_pass(g1, Q, true, D->storage, st);
+  } else {
+    // prime: the trial pair of iteration `it` and its fused pass (as fused_trials, without the round trip)
+    nsq = launch_finish_grad(losspart.get(), nchunks, kMaxCand, kind, D->sum_sq, D->sum, graw.get(), Y.get(), n * Q,
+                             s0, s1, cand[0].get(), cand[1].get(), sq2.get(), scal.get(), st,
+                             comm ? rawy.get() : nullptr);
+  }
   b.Y[0] = cand[0].get();
   b.Y[1] = cand[1].get();
   b.ncand = 2;
-  launch_pass_fused_f32(b, Q, st);
+  if (!need_grad) launch_pass_fused_f32(b, Q, st);
   double* pre = scal.get() + 5;  // the pass's loss sums (reduction launch's extra CTA; q >= 2)
   const bool have_pre = kPT * Q >= 256 && !comm;
   // row-sharded: this rank's [gradient | trial loss sums] -> xred, all-reduced (one collective per pass)
@@ -418,7 +432,14 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
   S.step = step;
   S.it = it;
   S.pred = pred;
+  S.fix = need_grad ? 1 : 0;
+  S.init = (need_grad && init) ? 1 : 0;
   GMDS_CUDA(cudaMemcpyAsync(gdst.get(), &S, sizeof S, cudaMemcpyHostToDevice, st));
+  // history[it] lives on the device for the loop: a decision on difference sums re-bases it (as the host
+  // loop re-bases history.back()); read back below
+  const bool entry_hist = !(need_grad && init) && !history.empty();
+  double f_entry = entry_hist ? history.back() : 0.0;
+  if (entry_hist) GMDS_CUDA(cudaMemcpyAsync(hist.get() + it, &f_entry, sizeof(double), cudaMemcpyHostToDevice, st));
   int par = 0;  // state buffer (flips per gd_step launch)
   int sqp = 0;  // |g|^2 partials buffer (flips per iteration)
   int issued = it;
@@ -512,6 +533,12 @@ GdState Engine::device_gd(int kind, double delta, double f, double step, int it,
     const double* Ys[2] = {cand[0].get(), cand[1].get()};
     const std::vector<double> raws = loss_raw(kind, delta, Ys, 2);
     S.t1 = raws[1];
+  }
+  if ((need_grad && init) || entry_hist) {  // f(Y0) written by the fix block / the entry value, re-based or not
+    double f0 = 0.0;
+    GMDS_CUDA(cudaMemcpyAsync(&f0, hist.get() + it, sizeof(double), cudaMemcpyDeviceToHost, st));
+    GMDS_CUDA(cudaStreamSynchronize(st));
+    if (entry_hist) history.back() = f0; else history.push_back(f0);
   }
   if (S.it > it) {
     std::vector<double> h(static_cast<size_t>(S.it - it));
@@ -687,15 +714,19 @@ IterResult gradient_descent(Engine& E, const Resolved& rp, int max_iters, double
   // accepted run without a host round trip (gd_step_kernel); GMDS_HOST_GD=1
   // keeps every decision on the host (same arithmetic, same trajectory).
   const bool devloop = spec && !std::getenv("GMDS_HOST_GD");
+  const bool dev_nograd = devloop && !std::getenv("GMDS_NO_ONDEV");
   const bool precise_ok = !std::getenv("GMDS_NO_PRECISE");
   const bool diff_ok = !std::getenv("GMDS_NO_DIFF");  // GMDS_NO_DIFF=1: fp64-arithmetic re-evaluation instead
   for (; it < max_iters; ++it) {
     Engine::GradTrials gt;
     int slot_of[2] = {0, 1};  // slot of (step, step/2) in gt.trial / E.cand
     bool decided_on_device = false;
-    if (devloop && have_grad) {
+    // (without the gradient at Y -- the first iteration, or after an iteration decided here -- the device
+    // loop primes itself with the gradient pass; GMDS_NO_ONDEV=1: the host takes that pass and the trials)
+    if (devloop && (have_grad || dev_nograd)) {
+      const bool first = r.history.empty();
       const GdState S = E.device_gd(kind, rp.delta, f, step, it, pred, max_iters, rel_tol, r.history,
-                                    precise_ok ? kPreciseRel : 0.0);
+                                    precise_ok ? kPreciseRel : 0.0, !have_grad, first);
       it = S.it;
       f = S.f;
       step = S.step;

@@ -79,7 +79,7 @@ struct Engine {
   // host (stop 2: that iteration's trial losses and |g|^2 are in the state).
   // Appends the accepted losses to history.
   GdState device_gd(int kind, double delta, double f, double step, int it, int pred, int max_iters, double rel_tol,
-                    std::vector<double>& history, double precise_rel);
+                    std::vector<double>& history, double precise_rel, bool need_grad = false, bool init = false);
   DevBuf<double> sq2, hist;
   DevBuf<GdState> gdst;
   double loss_of(int kind, double raw) const;

@@ -62,6 +62,7 @@ struct GdState {
                                 // the next decision tests those (no fp32 re-evaluation, as on the host)
   int halv;                     // halvings spent on this iteration (the reference allows 60)
   int nextra;                   // passes run for these units (pass accounting)
+  int init;                     // with fix: the pass at Y is the fit's first -- its loss is f(Y0), history[it]
 };
 
 struct Steps {

@@ -363,6 +363,13 @@ __global__ void gd_step_kernel(GdState* st, int par, const double* __restrict__ 
     // the scaled gradient, the trial pair of iteration S.it, |g|^2 partials.  No decision.
     GdState R = S;
     R.fix = 0;
+    if (S.init) {  // the loss before the loop (embed.cpp:226): the host's order of the same sums (sum_parts_kernel)
+      const double raw0 = xred ? xred[m] : (pre ? pre[0] : tree_sum<1024>(losspart, nparts, stride, 0, red));
+      R.f = (kind == kKruskal) ? sqrt(__ddiv_rn(raw0, sum_sq))
+                               : ((kind == kSammon) ? __dmul_rn(__ddiv_rn(1.0, sum), raw0) : raw0);
+      R.init = 0;
+      if (lead) history[S.it] = R.f;
+    }
     if (lead) publish(R);
     const double raw = xred ? xred[m] : (pre ? pre[2] : tree_sum<256>(losspart, nparts, stride, 0, red));
     const double scale = grad_scale(kind, raw, sum_sq, sum);
